@@ -1,0 +1,139 @@
+/*
+ * xmhd_b200.h — C-ABI of the B200 (sm_100a) Leja / FD-JVP / MHD-RHS hot path.
+ *
+ * Drop-in boundary for the reference's operator interface (arxiv/paper_2108_13622,
+ * Python package xmhd).  The reference binds its hot path through Python
+ * duck-typing; each entry point below replaces one reference callable and is
+ * bound from the Python host mirror (paper_2108_13622_b200/_lib.py) with ctypes.
+ *
+ * Conventions
+ *   - All vector pointers are DEVICE pointers to fp64 data in the reference's
+ *     flat field-major layout (8, ny, nx): index f*ny*nx + j*nx + i
+ *     (mhd.py:51-70).  Buffers are owned by the caller (PyTorch allocations);
+ *     the context owns only scratch (reductions, Leja ping-pong, control block).
+ *   - All work is enqueued on the context's CUDA stream (xmhd_set_stream).
+ *   - Return value: XMHD_OK, XMHD_NONFINITE (a non-finite RHS cell: the caller
+ *     raises RhsBlowupError, mhd.py:225-231), XMHD_BADARG, XMHD_CUDA_ERROR.
+ *     xmhd_last_error() describes the last failure of the calling thread.
+ *   - Numerics: element-wise results reproduce the reference's NumPy IEEE
+ *     operation sequence bit for bit; norms are deterministic device
+ *     reductions (same value on every run, not OpenBLAS's summation order).
+ */
+#ifndef XMHD_B200_H
+#define XMHD_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XMHD_OK 0
+#define XMHD_NONFINITE 1
+#define XMHD_BADARG 2
+#define XMHD_CUDA_ERROR 3
+
+/* Boundary kinds: mhd.py:34-36 (XMHD_BC_HALO = y-strip rows from neighbour ranks). */
+#define XMHD_BC_PERIODIC 0
+#define XMHD_BC_REFLECTING 1
+#define XMHD_BC_HALO 2
+
+/* Leja status (leja.py:103-150). */
+#define XMHD_LEJA_RUNNING 0
+#define XMHD_LEJA_CONVERGED 1
+#define XMHD_LEJA_BLOWUP 2        /* non-converged result, residual = inf (leja.py:135-139) */
+#define XMHD_LEJA_RHS_NONFINITE 3 /* matvec hit a non-finite RHS: caller raises            */
+#define XMHD_LEJA_NEED_COEFFS 4   /* grow the coefficient chunk (leja.py:128-130)           */
+#define XMHD_LEJA_EXHAUSTED 5     /* 499 terms, not converged (leja.py:149-150)            */
+
+typedef struct xmhd_ctx xmhd_ctx;
+
+typedef struct xmhd_leja_state {
+  int status;      /* XMHD_LEJA_* */
+  int iterations;  /* matvecs performed = PhiApplyResult.iterations        */
+  int rhs_calls;   /* RHS evaluations (advance RhsOperator.calls by this)   */
+  int m;           /* next Newton index                                     */
+  double residual; /* PhiApplyResult.residual                              */
+  double eps;      /* FD step of the last matvec (diagnostics, blow-up repro) */
+  double ynorm;    /* ||y|| of the current Newton basis vector              */
+} xmhd_leja_state;
+
+/* Context for one (local) grid: the geometry + MHDParams captured by
+ * RhsOperator(lambda flat: mhd_rhs(geometry.with_flat(flat), params))
+ * (harness.py:129; mhd.py:39-48, 51-70).  `stream` is a cudaStream_t (0 = legacy). */
+int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu, double eta,
+                double kappa, double gamma, double mu0, int bc_x, int bc_y, void* stream);
+int xmhd_destroy(xmhd_ctx* ctx);
+int xmhd_set_stream(xmhd_ctx* ctx, void* stream);
+const char* xmhd_last_error(void);
+/* Launch geometry chosen for the stencil (units, grid) — diagnostics/benchmarks. */
+int xmhd_plan_info(xmhd_ctx* ctx, int* out4);
+/* Kernels launched by this context since creation (bench "gpu_launches"). */
+long long xmhd_launch_count(xmhd_ctx* ctx);
+
+/* y-strip decomposition: halo rows (2 rows above / below, layout [field][2][nx])
+ * for the base state and for the current JVP direction.  Only with bc_y == XMHD_BC_HALO. */
+int xmhd_set_halo(xmhd_ctx* ctx, const double* lo, const double* hi, const double* lo_dir,
+                  const double* hi_dir);
+
+/* mhd_rhs (mhd.py:127-232): f = F(u). */
+int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f);
+
+/* jvp (linearize.py:56-67): out = (F(u + eps*w) - fu) / eps with
+ * eps = sqrt(eps_mach)*max(1,unorm)/max(||w||,1e-300); zero w -> zeros, no RHS call.
+ * *called = number of RHS evaluations (0 or 1); *out_norm = ||out|| (may be NULL). */
+int xmhd_jvp(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w,
+             double* out, int* called, double* out_norm);
+
+/* np.linalg.norm(x) (deterministic device reduction). */
+int xmhd_norm(xmhd_ctx* ctx, const double* x, long long n, double* out);
+
+/* out = ((c0*v0 + c1*v1) + c2*v2) + c3*v3, the stage algebra of integrators.py:139-199.
+ * norm_out / nonfinite_out may be NULL (then no reduction is performed). */
+int xmhd_lincomb(xmhd_ctx* ctx, double* out, long long n, const double* const* v,
+                 const double* c, int nterms, double* norm_out, int* nonfinite_out);
+
+/* out = x / d elementwise (IEEE), optionally ||out|| (w/||w||, jw/mag, v/l!). */
+int xmhd_divide(xmhd_ctx* ctx, double* out, const double* x, double d, long long n,
+                double* norm_out);
+
+/* error_norm pieces (integrators.py:88-96): out[0] = ||a-b||, out[1] = ||b||. */
+int xmhd_diff_norms(xmhd_ctx* ctx, const double* a, const double* b, long long n, double* out);
+
+/* Diagnostics: max|discrete_div_b| (mhd.py:235-240), per-field sums
+ * (conserved_totals before the area factor, mhd.py:243-247), and the two
+ * CFL speed maxima of harness.py:105-116. */
+int xmhd_divb(xmhd_ctx* ctx, const double* u, double* field, double* out_max);
+int xmhd_field_sums(xmhd_ctx* ctx, const double* u, double* out8);
+int xmhd_cfl_speeds(xmhd_ctx* ctx, const double* u, double* out2);
+
+/* apply_phi_leja with matvec = jvp(lin, .) fused into the stencil (leja.py:103-150;
+ * integrators.py:117-136).  xi: 500 Leja points (host), coeffs: ncoef Newton
+ * coefficients (host).  Runs device-side until the status leaves RUNNING. */
+int xmhd_leja_start(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                    const double* v, double dt, double q, double theta, double tol,
+                    const double* xi, const double* coeffs, int ncoef, xmhd_leja_state* st);
+/* After XMHD_LEJA_NEED_COEFFS: upload the grown chunk and continue. */
+int xmhd_leja_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef, xmhd_leja_state* st);
+/* Copy the interpolant p of the finished call into p_out (device, 8*nx*ny). */
+int xmhd_leja_result(xmhd_ctx* ctx, double* p_out);
+/* Copy the current Newton basis vector y into dst (generic matvec input, RHS blow-up replay). */
+int xmhd_leja_current_y(xmhd_ctx* ctx, double* dst);
+
+/* apply_phi_leja for an arbitrary caller-supplied matvec (leja.py:103-150):
+ * start -> loop { current_y; w = matvec(y) on the caller side; step } -> result. */
+int xmhd_leja_generic_start(xmhd_ctx* ctx, const double* v, long long n, double dt, double q,
+                            double theta, double tol, const double* xi, const double* coeffs,
+                            int ncoef, xmhd_leja_state* st);
+int xmhd_leja_generic_step(xmhd_ctx* ctx, const double* w, xmhd_leja_state* st);
+int xmhd_leja_generic_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef,
+                             xmhd_leja_state* st);
+int xmhd_leja_generic_result(xmhd_ctx* ctx, double* p_out);
+
+/* Host C++ port of _phi_divided_diffs (phi.py:99-144): first column of
+ * phi_l of the bidiagonal node matrix, bitwise equal to the NumPy routine.
+ * out has n entries. */
+int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double subdiag, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XMHD_B200_H */

@@ -1,0 +1,179 @@
+"""ctypes binding of the C-ABI in ``include/xmhd_b200.h`` (``_xmhd_b200.so``).
+
+The product path has no CPU fallback: if the shared library or a CUDA device is
+missing, every entry point raises ``NativeUnavailable`` loudly.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+import torch
+
+from paper_2108_13622_b200 import build as _build
+
+OK, NONFINITE, BADARG, CUDA_ERROR = 0, 1, 2, 3
+BC_PERIODIC, BC_REFLECTING, BC_HALO = 0, 1, 2
+(LEJA_RUNNING, LEJA_CONVERGED, LEJA_BLOWUP, LEJA_RHS_NONFINITE, LEJA_NEED_COEFFS,
+ LEJA_EXHAUSTED) = range(6)
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a library or the CUDA device is not available."""
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class LejaState(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("iterations", ctypes.c_int),
+                ("rhs_calls", ctypes.c_int), ("m", ctypes.c_int),
+                ("residual", ctypes.c_double), ("eps", ctypes.c_double),
+                ("ynorm", ctypes.c_double)]
+
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I = ctypes.c_int
+_L = ctypes.c_longlong
+_PD = ctypes.POINTER(ctypes.c_double)
+_PI = ctypes.POINTER(ctypes.c_int)
+
+_SIGS = {
+    "xmhd_create": (_I, [ctypes.POINTER(_P), _I, _I, _D, _D, _D, _D, _D, _D, _D, _I, _I, _P]),
+    "xmhd_destroy": (_I, [_P]),
+    "xmhd_set_stream": (_I, [_P, _P]),
+    "xmhd_last_error": (ctypes.c_char_p, []),
+    "xmhd_plan_info": (_I, [_P, _PI]),
+    "xmhd_launch_count": (_L, [_P]),
+    "xmhd_set_halo": (_I, [_P, _P, _P, _P, _P]),
+    "xmhd_rhs": (_I, [_P, _P, _P]),
+    "xmhd_jvp": (_I, [_P, _P, _P, _D, _P, _P, _PI, _PD]),
+    "xmhd_norm": (_I, [_P, _P, _L, _PD]),
+    "xmhd_lincomb": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD, _PI]),
+    "xmhd_divide": (_I, [_P, _P, _P, _D, _L, _PD]),
+    "xmhd_diff_norms": (_I, [_P, _P, _P, _L, _PD]),
+    "xmhd_divb": (_I, [_P, _P, _P, _PD]),
+    "xmhd_field_sums": (_I, [_P, _P, _PD]),
+    "xmhd_cfl_speeds": (_I, [_P, _P, _PD]),
+    "xmhd_leja_start": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I,
+                             ctypes.POINTER(LejaState)]),
+    "xmhd_leja_resume": (_I, [_P, _PD, _I, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_result": (_I, [_P, _P]),
+    "xmhd_leja_current_y": (_I, [_P, _P]),
+    "xmhd_leja_generic_start": (_I, [_P, _P, _L, _D, _D, _D, _D, _PD, _PD, _I,
+                                     ctypes.POINTER(LejaState)]),
+    "xmhd_leja_generic_step": (_I, [_P, _P, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_generic_resume": (_I, [_P, _PD, _I, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_generic_result": (_I, [_P, _P]),
+    "xmhd_phi_divided_diffs": (_I, [_I, _PD, _I, _D, _PD]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path():
+    return _build.SO_PATH
+
+
+def load(build_if_missing=True):
+    """Load (building in-tree first if needed) and type the shared library."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if build_if_missing:
+            try:
+                _build.build_so()
+            except (OSError, RuntimeError) as exc:
+                if not os.path.exists(path):
+                    raise NativeUnavailable(f"cannot build {path}: {exc}") from exc
+        if not os.path.exists(path):
+            raise NativeUnavailable(f"missing native library {path}; run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("the B200 hot path needs a CUDA device; none is visible "
+                                "(no CPU fallback by design)")
+
+
+def err_text():
+    return load().xmhd_last_error().decode(errors="replace")
+
+
+def check(rc, what):
+    if rc == OK:
+        return rc
+    if rc == NONFINITE:
+        return rc
+    raise NativeError(f"{what} failed ({rc}): {err_text()}")
+
+
+def ptr(t):
+    """Device address of a contiguous CUDA float64 tensor."""
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous CUDA float64 tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def host_doubles(arr):
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    return a, a.ctypes.data_as(_PD)
+
+
+def current_stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Context:
+    """Owner of one native ``xmhd_ctx`` (a grid + physics parameter set)."""
+
+    def __init__(self, nx, ny, dx, dy, mu, eta, kappa, gamma, mu0, bc_x, bc_y):
+        require_cuda()
+        self.lib = load()
+        self.nx, self.ny = int(nx), int(ny)
+        self.n = 8 * self.nx * self.ny
+        h = ctypes.c_void_p()
+        torch.cuda.init()
+        rc = self.lib.xmhd_create(ctypes.byref(h), self.nx, self.ny, float(dx), float(dy),
+                                  float(mu), float(eta), float(kappa), float(gamma),
+                                  float(mu0), int(bc_x), int(bc_y), current_stream_handle())
+        check(rc, "xmhd_create")
+        self.h = h
+
+    def bind_stream(self):
+        self.lib.xmhd_set_stream(self.h, current_stream_handle())
+        return self.h
+
+    def plan(self):
+        out = (ctypes.c_int * 4)()
+        check(self.lib.xmhd_plan_info(self.h, out), "xmhd_plan_info")
+        return dict(units_x=out[0], units=out[1], seg_rows=out[2], grid=out[3])
+
+    def launches(self):
+        return int(self.lib.xmhd_launch_count(self.h))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            try:
+                self.lib.xmhd_destroy(h)
+            except Exception:
+                pass
+            self.h = None

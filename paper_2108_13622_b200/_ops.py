@@ -1,0 +1,121 @@
+"""Device vector primitives over the C-ABI (norms, linear combinations, division).
+
+All vectors are contiguous CUDA float64 tensors.  Element-wise results follow
+the reference's NumPy operation order exactly; norms are deterministic device
+reductions.
+"""
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+from paper_2108_13622_b200 import _lib
+
+_util = {}
+_util_lock = threading.Lock()
+
+
+def util_ctx():
+    """A geometry-free context used for reductions on arbitrary vectors."""
+    dev = torch.cuda.current_device()
+    with _util_lock:
+        c = _util.get(dev)
+        if c is None:
+            c = _lib.Context(2, 2, 1.0, 1.0, 0.0, 0.0, 0.0, 5.0 / 3.0, 1.0,
+                             _lib.BC_PERIODIC, _lib.BC_PERIODIC)
+            _util[dev] = c
+    return c
+
+
+def is_host(x):
+    return isinstance(x, np.ndarray) or (torch.is_tensor(x) and not x.is_cuda) or \
+        isinstance(x, (list, tuple, float, int))
+
+
+def as_device(x, copy=False):
+    """Contiguous CUDA float64 tensor view/copy of x (numpy, list, or tensor)."""
+    if torch.is_tensor(x):
+        t = x
+        if not t.is_cuda:
+            t = t.to(dtype=torch.float64).contiguous()
+            t = t.to("cuda", non_blocking=t.is_pinned())
+            return t
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        t = t.contiguous()
+        return t.clone() if copy else t
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    _lib.require_cuda()
+    return torch.from_numpy(a).to("cuda")
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+def like(result, template):
+    """Return `result` (device tensor) in the container type of `template`."""
+    return to_host(result) if is_host(template) else result
+
+
+def _h(ctx):
+    return (ctx or util_ctx()).bind_stream()
+
+
+def norm(x, ctx=None):
+    """np.linalg.norm(x) of a device vector."""
+    lib = _lib.load()
+    out = ctypes.c_double()
+    _lib.check(lib.xmhd_norm(_h(ctx), _lib.ptr(x), x.numel(), ctypes.byref(out)), "xmhd_norm")
+    return float(out.value)
+
+
+def lincomb(coeffs, vecs, out=None, want_norm=False, ctx=None):
+    """((c0*v0 + c1*v1) + c2*v2) + c3*v3 with one rounding per operation.
+
+    Returns out, or (out, norm, nonfinite) when want_norm.
+    """
+    assert 1 <= len(vecs) == len(coeffs) <= 4
+    lib = _lib.load()
+    n = vecs[0].numel()
+    if out is None:
+        out = torch.empty_like(vecs[0])
+    arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(v.data_ptr()) for v in vecs])
+    cs = (ctypes.c_double * 4)(*[float(c) for c in coeffs])
+    if want_norm:
+        nrm = ctypes.c_double()
+        bad = ctypes.c_int()
+        rc = lib.xmhd_lincomb(_h(ctx), _lib.ptr(out), n, arr, cs, len(vecs), ctypes.byref(nrm),
+                              ctypes.byref(bad))
+        _lib.check(rc, "xmhd_lincomb")
+        return out, float(nrm.value), bool(bad.value)
+    rc = lib.xmhd_lincomb(_h(ctx), _lib.ptr(out), n, arr, cs, len(vecs), None, None)
+    _lib.check(rc, "xmhd_lincomb")
+    return out
+
+
+def divide(x, d, out=None, want_norm=False, ctx=None):
+    """x / d element-wise (IEEE); optionally also ||x / d||."""
+    lib = _lib.load()
+    if out is None:
+        out = torch.empty_like(x)
+    if want_norm:
+        nrm = ctypes.c_double()
+        rc = lib.xmhd_divide(_h(ctx), _lib.ptr(out), _lib.ptr(x), float(d), x.numel(),
+                             ctypes.byref(nrm))
+        _lib.check(rc, "xmhd_divide")
+        return out, float(nrm.value)
+    rc = lib.xmhd_divide(_h(ctx), _lib.ptr(out), _lib.ptr(x), float(d), x.numel(), None)
+    _lib.check(rc, "xmhd_divide")
+    return out
+
+
+def diff_norms(a, b, ctx=None):
+    """(||a - b||, ||b||) of two device vectors."""
+    lib = _lib.load()
+    out = (ctypes.c_double * 2)()
+    rc = lib.xmhd_diff_norms(_h(ctx), _lib.ptr(a), _lib.ptr(b), a.numel(), out)
+    _lib.check(rc, "xmhd_diff_norms")
+    return float(out[0]), float(out[1])

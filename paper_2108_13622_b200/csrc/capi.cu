@@ -1,0 +1,539 @@
+// C-ABI of the B200 hot path (declared in include/xmhd_b200.h).
+//
+// Host-side control: context lifetime, scratch ownership, the device-resident
+// Leja loop driver (leja.py:103-150) and the scalar glue of jvp
+// (linearize.py:56-67).  Python (paper_2108_13622_b200/_lib.py) binds these with
+// ctypes; no torch types cross this boundary.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "kernels.h"
+#include "xmhd_b200.h"
+
+using namespace xb;
+
+struct xmhd_ctx {
+  Geom g;
+  cudaStream_t stream = 0;
+  int device = 0;
+  int nsm = 148;
+  int units_x = 0, nunits = 0, seg_rows = 0, grid = 0;
+  int red_grid = 0;
+  double* partials = nullptr;  // [red_grid*8]  (also the stencil's [grid][2])
+  unsigned* tickets = nullptr; // [8]
+  double* result = nullptr;    // [16]
+  int* bad = nullptr;          // [1]
+  LejaCtl* ctl = nullptr;
+  LejaCtl* ctl_h = nullptr;    // pinned mirror
+  double* h_dbl = nullptr;     // pinned [16]
+  int* h_int = nullptr;        // pinned [4]
+  double* coeffs_d = nullptr;  // [512]
+  double* xi_d = nullptr;      // [512]
+  double* ybuf[2] = {nullptr, nullptr};
+  double* pbuf[2] = {nullptr, nullptr};
+  long long ws_n = 0;          // elements per Leja workspace vector
+  long long gen_n = 0;         // vector length of the current generic Leja call
+  const double* leja_u = nullptr;
+  const double* leja_fu = nullptr;
+  long long launches = 0;
+  int batch_max = 64;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                 \
+  do {                                                                           \
+    cudaError_t e_ = (expr);                                                     \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(XMHD_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// How a constant divisor is applied in exact_div (common.cuh).
+Divisor make_divisor(double d, bool force_ieee) {
+  Divisor v;
+  v.d = d;
+  v.r = 1.0 / d;  // RN(1/d): host IEEE division
+  int ex = 0;
+  const double m = std::frexp(d, &ex);
+  if (force_ieee) {
+    v.kind = DIV_IEEE;
+  } else if (m == 0.5 || m == -0.5) {
+    v.kind = DIV_MUL;  // power of two: a*r is a/d exactly
+  } else {
+    const double e = std::fma(-d, v.r, 1.0);  // exact: 1 - d*r
+    v.kind = (std::fabs(e) <= std::ldexp(1.0, -54)) ? DIV_MK1 : DIV_MK2;
+  }
+  return v;
+}
+
+RedBuf redbuf(xmhd_ctx* c) {
+  RedBuf rb;
+  rb.partials = c->partials;
+  rb.ticket = c->tickets;
+  rb.result = c->result;
+  rb.grid = c->red_grid;
+  return rb;
+}
+
+int ensure_ws(xmhd_ctx* c, long long n) {
+  if (c->ws_n >= n) return XMHD_OK;
+  for (int k = 0; k < 2; ++k) {
+    if (c->ybuf[k]) cudaFree(c->ybuf[k]);
+    if (c->pbuf[k]) cudaFree(c->pbuf[k]);
+    c->ybuf[k] = c->pbuf[k] = nullptr;
+  }
+  c->ws_n = 0;
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaMalloc(&c->ybuf[k], sizeof(double) * n));
+    CK(cudaMalloc(&c->pbuf[k], sizeof(double) * n));
+  }
+  c->ws_n = n;
+  return XMHD_OK;
+}
+
+StencilArgs base_args(xmhd_ctx* c) {
+  StencilArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = c->g;
+  a.partials = c->partials;
+  a.ticket = c->tickets;
+  a.result = c->result;
+  a.bad = c->bad;
+  a.units_x = c->units_x;
+  a.nunits = c->nunits;
+  a.seg_rows = c->seg_rows;
+  return a;
+}
+
+int fetch_doubles(xmhd_ctx* c, int n) {
+  CK(cudaMemcpyAsync(c->h_dbl, c->result, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return XMHD_OK;
+}
+
+int fetch_bad(xmhd_ctx* c, int* out) {
+  CK(cudaMemcpyAsync(c->h_int, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *out = c->h_int[0];
+  return XMHD_OK;
+}
+
+// Python's max(a, b) for floats: the first argument unless the second is larger.
+inline double py_max(double a, double b) { return (b > a) ? b : a; }
+
+void fill_state(const LejaCtl& h, xmhd_leja_state* st) {
+  if (!st) return;
+  st->status = h.status;
+  st->iterations = h.iters;
+  st->rhs_calls = h.rhs_calls;
+  st->m = h.m;
+  st->residual = h.residual;
+  st->eps = h.eps;
+  st->ynorm = h.ynorm;
+}
+
+int sync_ctl(xmhd_ctx* c) {
+  CK(cudaMemcpyAsync(c->ctl_h, c->ctl, sizeof(LejaCtl), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return XMHD_OK;
+}
+
+// Device-resident fused Leja loop: launch iterations in growing batches; each
+// kernel exits immediately once the control block left RUNNING, so the host
+// only synchronises once per batch.
+int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
+  StencilArgs a = base_args(c);
+  a.u = c->leja_u;
+  a.fu = c->leja_fu;
+  a.ybuf[0] = c->ybuf[0];
+  a.ybuf[1] = c->ybuf[1];
+  a.pbuf[0] = c->pbuf[0];
+  a.pbuf[1] = c->pbuf[1];
+  a.coeffs = c->coeffs_d;
+  a.xi = c->xi_d;
+  a.ctl = c->ctl;
+  int batch = 2;
+  for (;;) {
+    for (int k = 0; k < batch; ++k) {
+      CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+      c->launches++;
+    }
+    int rc = sync_ctl(c);
+    if (rc) return rc;
+    if (c->ctl_h->status != LJ_RUNNING) break;
+    batch = batch * 2 < c->batch_max ? batch * 2 : c->batch_max;
+  }
+  fill_state(*c->ctl_h, st);
+  return XMHD_OK;
+}
+
+int upload_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
+  if (ncoef < 1 || ncoef > 512) return fail(XMHD_BADARG, "ncoef out of range");
+  CK(cudaMemcpyAsync(c->coeffs_d, coeffs, sizeof(double) * ncoef, cudaMemcpyHostToDevice,
+                     c->stream));
+  return XMHD_OK;
+}
+
+int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double dt, double q,
+               double theta, double tol, const double* xi, const double* coeffs, int ncoef) {
+  int rc = ensure_ws(c, n);
+  if (rc) return rc;
+  rc = upload_coeffs(c, coeffs, ncoef);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->xi_d, xi, sizeof(double) * 500, cudaMemcpyHostToDevice, c->stream));
+  LejaCtl h;
+  std::memset(&h, 0, sizeof(h));
+  h.ncoef = ncoef;
+  h.unorm = unorm;
+  h.dt = dt;
+  h.q = q;
+  h.theta = theta;
+  h.tol = tol;
+  *c->ctl_h = h;
+  CK(cudaMemcpyAsync(c->ctl, c->ctl_h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  CK(launch_leja_init(v, n, c->ybuf[0], c->pbuf[0], c->ctl, c->coeffs_d, redbuf(c), c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* xmhd_last_error(void) { return g_err.c_str(); }
+
+int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu, double eta,
+                double kappa, double gamma, double mu0, int bc_x, int bc_y, void* stream) {
+  if (!out) return fail(XMHD_BADARG, "null out");
+  if (nx < 2 || ny < 2) return fail(XMHD_BADARG, "grid must be at least 2x2");
+  if (bc_x != XMHD_BC_PERIODIC && bc_x != XMHD_BC_REFLECTING)
+    return fail(XMHD_BADARG, "bad bc_x");
+  if (bc_y < XMHD_BC_PERIODIC || bc_y > XMHD_BC_HALO) return fail(XMHD_BADARG, "bad bc_y");
+  xmhd_ctx* c = new xmhd_ctx();
+  const bool ieee = std::getenv("XMHD_DIV_IEEE") && std::atoi(std::getenv("XMHD_DIV_IEEE"));
+  Geom& g = c->g;
+  std::memset(&g, 0, sizeof(g));
+  g.nx = nx;
+  g.ny = ny;
+  g.bcx = bc_x;
+  g.bcy = bc_y;
+  g.plane = (long long)nx * ny;
+  g.diffusive = (mu != 0.0 || eta != 0.0 || kappa != 0.0) ? 1 : 0;
+  g.mu0_one = (mu0 == 1.0) ? 1 : 0;
+  g.h2x = make_divisor(2.0 * dx, ieee);   // mhd.py:115 folds 2.0*dx on the host
+  g.h2y = make_divisor(2.0 * dy, ieee);
+  g.mu0d = make_divisor(mu0, ieee);
+  g.gm1 = gamma - 1.0;
+  g.mu = mu;
+  g.eta = eta;
+  g.cond = mu * kappa * gamma / (gamma - 1.0);   // mhd.py:197, Python's order
+  g.c23 = 2.0 / 3.0;
+  c->stream = (cudaStream_t)stream;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(XMHD_CUDA_ERROR, std::string("device query: ") + cudaGetErrorString(e));
+  }
+  stencil_plan(g, c->nsm, c->units_x, c->nunits, c->seg_rows, c->grid);
+  c->red_grid = 4 * c->nsm;
+  const int slots = (c->red_grid > c->grid ? c->red_grid : c->grid) * 8 + 64;
+  if ((e = cudaMalloc(&c->partials, sizeof(double) * slots)) != cudaSuccess ||
+      (e = cudaMalloc(&c->tickets, sizeof(unsigned) * 8)) != cudaSuccess ||
+      (e = cudaMalloc(&c->result, sizeof(double) * 16)) != cudaSuccess ||
+      (e = cudaMalloc(&c->bad, sizeof(int) * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&c->ctl, sizeof(LejaCtl))) != cudaSuccess ||
+      (e = cudaMalloc(&c->coeffs_d, sizeof(double) * 512)) != cudaSuccess ||
+      (e = cudaMalloc(&c->xi_d, sizeof(double) * 512)) != cudaSuccess ||
+      (e = cudaMallocHost(&c->ctl_h, sizeof(LejaCtl))) != cudaSuccess ||
+      (e = cudaMallocHost(&c->h_dbl, sizeof(double) * 16)) != cudaSuccess ||
+      (e = cudaMallocHost(&c->h_int, sizeof(int) * 4)) != cudaSuccess ||
+      (e = cudaMemsetAsync(c->tickets, 0, sizeof(unsigned) * 8, c->stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(c->stream)) != cudaSuccess) {
+    xmhd_destroy(c);
+    return fail(XMHD_CUDA_ERROR, std::string("context allocation: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return XMHD_OK;
+}
+
+int xmhd_destroy(xmhd_ctx* c) {
+  if (!c) return XMHD_OK;
+  cudaStreamSynchronize(c->stream);
+  cudaFree(c->partials);
+  cudaFree(c->tickets);
+  cudaFree(c->result);
+  cudaFree(c->bad);
+  cudaFree(c->ctl);
+  cudaFree(c->coeffs_d);
+  cudaFree(c->xi_d);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(c->ybuf[k]);
+    cudaFree(c->pbuf[k]);
+  }
+  cudaFreeHost(c->ctl_h);
+  cudaFreeHost(c->h_dbl);
+  cudaFreeHost(c->h_int);
+  delete c;
+  return XMHD_OK;
+}
+
+int xmhd_set_stream(xmhd_ctx* c, void* stream) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  c->stream = (cudaStream_t)stream;
+  return XMHD_OK;
+}
+
+int xmhd_plan_info(xmhd_ctx* c, int* out4) {
+  if (!c || !out4) return fail(XMHD_BADARG, "null arg");
+  out4[0] = c->units_x;
+  out4[1] = c->nunits;
+  out4[2] = c->seg_rows;
+  out4[3] = c->grid;
+  return XMHD_OK;
+}
+
+long long xmhd_launch_count(xmhd_ctx* c) { return c ? c->launches : -1; }
+
+int xmhd_set_halo(xmhd_ctx* c, const double* lo, const double* hi, const double* lo_dir,
+                  const double* hi_dir) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  if (c->g.bcy != BC_HALO) return fail(XMHD_BADARG, "context is not a y-strip (bc_y != HALO)");
+  c->g.halo_lo = lo;
+  c->g.halo_hi = hi;
+  c->g.halo_lo_dir = lo_dir;
+  c->g.halo_hi_dir = hi_dir;
+  return XMHD_OK;
+}
+
+int xmhd_rhs(xmhd_ctx* c, const double* u, double* f) {
+  if (!c || !u || !f) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO && !c->g.halo_lo) return fail(XMHD_BADARG, "halo rows not set");
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.out = f;
+  CK(launch_stencil(MODE_RHS, a, c->grid, c->stream));
+  c->launches++;
+  int bad = 0;
+  int rc = fetch_bad(c, &bad);
+  if (rc) return rc;
+  return bad ? XMHD_NONFINITE : XMHD_OK;
+}
+
+int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w,
+             double* out, int* called, double* out_norm) {
+  if (!c || !u || !fu || !w || !out) return fail(XMHD_BADARG, "null arg");
+  const long long n = NF * c->g.plane;
+  CK(launch_norm(w, n, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  const double wn = c->h_dbl[0];
+  if (called) *called = 0;
+  if (wn == 0.0) {  // linearize.py:63-64: zero vector, no RHS evaluation
+    CK(cudaMemsetAsync(out, 0, sizeof(double) * n, c->stream));
+    if (out_norm) *out_norm = 0.0;
+    return XMHD_OK;
+  }
+  // linearize.py:65: eps = _SQRT_EPS * max(1.0, ||u||) / max(||w||, 1e-300)
+  const double eps = (1.4901161193847656e-08 * py_max(1.0, unorm)) / py_max(wn, 1e-300);
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.dir = w;
+  a.fu = fu;
+  a.out = out;
+  a.eps = eps;
+  CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
+  c->launches++;
+  if (called) *called = 1;
+  rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  if (out_norm) *out_norm = c->h_dbl[0];
+  int bad = 0;
+  rc = fetch_bad(c, &bad);
+  if (rc) return rc;
+  return bad ? XMHD_NONFINITE : XMHD_OK;
+}
+
+int xmhd_norm(xmhd_ctx* c, const double* x, long long n, double* out) {
+  if (!c || !x || !out) return fail(XMHD_BADARG, "null arg");
+  CK(launch_norm(x, n, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  *out = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+int xmhd_lincomb(xmhd_ctx* c, double* out, long long n, const double* const* v, const double* cf,
+                 int nterms, double* norm_out, int* nonfinite_out) {
+  if (!c || !out || !v || !cf || nterms < 1 || nterms > 4) return fail(XMHD_BADARG, "bad lincomb");
+  const int want = (norm_out || nonfinite_out) ? 1 : 0;
+  CK(launch_lincomb(out, n, v, cf, nterms, want, redbuf(c), c->stream));
+  c->launches++;
+  if (!want) return XMHD_OK;
+  int rc = fetch_doubles(c, 2);
+  if (rc) return rc;
+  if (norm_out) *norm_out = c->h_dbl[0];
+  if (nonfinite_out) *nonfinite_out = c->h_dbl[1] != 0.0;
+  return XMHD_OK;
+}
+
+int xmhd_divide(xmhd_ctx* c, double* out, const double* x, double d, long long n,
+                double* norm_out) {
+  if (!c || !out || !x) return fail(XMHD_BADARG, "null arg");
+  CK(launch_divide(out, x, d, n, norm_out ? 1 : 0, redbuf(c), c->stream));
+  c->launches++;
+  if (!norm_out) return XMHD_OK;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  *norm_out = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+int xmhd_diff_norms(xmhd_ctx* c, const double* a, const double* b, long long n, double* out) {
+  if (!c || !a || !b || !out) return fail(XMHD_BADARG, "null arg");
+  CK(launch_diffnorm(a, b, n, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 2);
+  if (rc) return rc;
+  out[0] = c->h_dbl[0];
+  out[1] = c->h_dbl[1];
+  return XMHD_OK;
+}
+
+int xmhd_divb(xmhd_ctx* c, const double* u, double* field, double* out) {
+  if (!c || !u || !out) return fail(XMHD_BADARG, "null arg");
+  CK(launch_divb_max(c->g, u, field, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  *out = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+int xmhd_field_sums(xmhd_ctx* c, const double* u, double* out8) {
+  if (!c || !u || !out8) return fail(XMHD_BADARG, "null arg");
+  CK(launch_field_sums(u, c->g.plane, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 8);
+  if (rc) return rc;
+  for (int k = 0; k < 8; ++k) out8[k] = c->h_dbl[k];
+  return XMHD_OK;
+}
+
+int xmhd_cfl_speeds(xmhd_ctx* c, const double* u, double* out2) {
+  if (!c || !u || !out2) return fail(XMHD_BADARG, "null arg");
+  const double gamma = c->g.gm1 + 1.0;
+  CK(launch_cfl(u, c->g.plane, gamma, c->g.mu0d.d, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 2);
+  if (rc) return rc;
+  out2[0] = c->h_dbl[0];
+  out2[1] = c->h_dbl[1];
+  return XMHD_OK;
+}
+
+int xmhd_leja_start(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                    const double* v, double dt, double q, double theta, double tol,
+                    const double* xi, const double* coeffs, int ncoef, xmhd_leja_state* st) {
+  if (!c || !u || !fu || !v || !xi || !coeffs) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "use the strip driver for BC_HALO");
+  const long long n = NF * c->g.plane;
+  c->leja_u = u;
+  c->leja_fu = fu;
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+  if (rc) return rc;
+  return leja_run(c, st);
+}
+
+int xmhd_leja_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_state* st) {
+  if (!c || !coeffs) return fail(XMHD_BADARG, "null arg");
+  int rc = upload_coeffs(c, coeffs, ncoef);
+  if (rc) return rc;
+  c->ctl_h->ncoef = ncoef;
+  c->ctl_h->status = LJ_RUNNING;
+  CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  return leja_run(c, st);
+}
+
+int xmhd_leja_result(xmhd_ctx* c, double* p_out) {
+  if (!c || !p_out) return fail(XMHD_BADARG, "null arg");
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
+  CK(cudaMemcpyAsync(p_out, c->pbuf[c->ctl_h->cur], sizeof(double) * n,
+                     cudaMemcpyDeviceToDevice, c->stream));
+  return XMHD_OK;
+}
+
+int xmhd_leja_current_y(xmhd_ctx* c, double* dst) {
+  if (!c || !dst) return fail(XMHD_BADARG, "null arg");
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
+  CK(cudaMemcpyAsync(dst, c->ybuf[c->ctl_h->cur], sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                     c->stream));
+  return XMHD_OK;
+}
+
+int xmhd_leja_generic_start(xmhd_ctx* c, const double* v, long long n, double dt, double q,
+                            double theta, double tol, const double* xi, const double* coeffs,
+                            int ncoef, xmhd_leja_state* st) {
+  if (!c || !v || !xi || !coeffs || n < 1) return fail(XMHD_BADARG, "bad arg");
+  int rc = leja_setup(c, v, n, 1.0, dt, q, theta, tol, xi, coeffs, ncoef);
+  if (rc) return rc;
+  c->gen_n = n;
+  rc = sync_ctl(c);
+  if (rc) return rc;
+  fill_state(*c->ctl_h, st);
+  return XMHD_OK;
+}
+
+int xmhd_leja_generic_step(xmhd_ctx* c, const double* w, xmhd_leja_state* st) {
+  if (!c || !c->gen_n) return fail(XMHD_BADARG, "no generic Leja call in progress");
+  CK(launch_leja_update(w, c->gen_n, c->ctl, c->ybuf, c->pbuf, c->coeffs_d, c->xi_d, redbuf(c),
+                        c->stream));
+  c->launches++;
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  fill_state(*c->ctl_h, st);
+  return XMHD_OK;
+}
+
+int xmhd_leja_generic_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_state* st) {
+  if (!c || !coeffs) return fail(XMHD_BADARG, "null arg");
+  int rc = upload_coeffs(c, coeffs, ncoef);
+  if (rc) return rc;
+  c->ctl_h->ncoef = ncoef;
+  c->ctl_h->status = LJ_RUNNING;
+  CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  rc = sync_ctl(c);
+  if (rc) return rc;
+  fill_state(*c->ctl_h, st);
+  return XMHD_OK;
+}
+
+int xmhd_leja_generic_result(xmhd_ctx* c, double* p_out) {
+  int rc = xmhd_leja_result(c, p_out);
+  c->gen_n = 0;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+// Host C++ port of the phi_l divided-difference routine (phi.py:99-144) that
+// feeds the Leja Newton coefficients (leja.py:84-100).
+//
+// Bitwise contract with the NumPy routine: every element-wise step is one IEEE
+// operation in the same order (compiled with -ffp-contract=off, no fast-math),
+// the substep count uses the same libm log2/ceil, and the bidiagonal matvec
+// computes out[i] = RN(RN(d[i]*w[i]) + RN(e*w[i-1])) exactly like
+// `out = diag*w; out[1:] += sub*w[:-1]`.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "xmhd_b200.h"
+
+extern "C" int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double subdiag,
+                                      double* out) {
+  if (l < 0 || n < 1 || !nodes || !out) return XMHD_BADARG;
+  const int dim = l + n;
+  std::vector<double> ext(dim, 0.0);
+  for (int i = 0; i < n; ++i) ext[l + i] = nodes[i];
+  const int terms = 60;
+  // scale = max(np.max(np.abs(ext)), abs(subdiag), 1e-30)   (Python max order)
+  double amax = std::fabs(ext[0]);
+  for (int i = 1; i < dim; ++i) {
+    const double a = std::fabs(ext[i]);
+    if (a > amax || a != a) amax = a;
+  }
+  double scale = amax;
+  if (std::fabs(subdiag) > scale) scale = std::fabs(subdiag);
+  if (1e-30 > scale) scale = 1e-30;
+  int s = 0;
+  const int s1 = (int)std::ceil(std::log2(scale));
+  const int s2 = (int)std::ceil(std::log2((double)(dim + terms) / (double)terms));
+  if (s1 > s) s = s1;
+  if (s2 > s) s = s2;
+  const double p2 = std::ldexp(1.0, s);  // 2.0 ** s
+  std::vector<double> diag(dim);
+  for (int i = 0; i < dim; ++i) diag[i] = ext[i] / p2;
+  const double sub = subdiag / p2;
+
+  std::vector<double> col(dim, 0.0), term(dim), acc(dim), tmp(dim);
+  col[0] = 1.0;
+  const long long nsub = 1LL << s;
+  for (long long it = 0; it < nsub; ++it) {
+    std::memcpy(term.data(), col.data(), sizeof(double) * dim);
+    std::memcpy(acc.data(), col.data(), sizeof(double) * dim);
+    for (int k = 1; k < terms; ++k) {
+      const double dk = (double)k;
+      // term = matvec(term) / k
+      tmp[0] = (diag[0] * term[0]) / dk;
+      for (int i = 1; i < dim; ++i) {
+        const double a = diag[i] * term[i];
+        const double b = sub * term[i - 1];
+        tmp[i] = (a + b) / dk;
+      }
+      term.swap(tmp);
+      for (int i = 0; i < dim; ++i) acc[i] = acc[i] + term[i];
+    }
+    col.swap(acc);
+  }
+  for (int i = 0; i < n; ++i) out[i] = col[l + i];
+  return XMHD_OK;
+}

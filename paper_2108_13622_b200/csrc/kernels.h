@@ -1,0 +1,152 @@
+// Internal (C++) interface between the C-ABI layer and the CUDA kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include "common.cuh"
+
+namespace xb {
+
+// Device-resident control block of one Leja phi-action (leja.py:103-150).
+// Written only by the last block of each fused iteration kernel.
+struct LejaCtl {
+  int m;            // next Newton index to compute (1 .. 499)
+  int status;       // LejaStatus
+  int small_prev;   // previous residual <= tol
+  int ncoef;        // valid coefficients on the device
+  int cur;          // index of the current y / p buffer
+  int rhs_calls;    // RHS evaluations performed (zero directions excluded)
+  int iters;        // matvecs performed
+  int zero_dir;     // current y has norm 0 (jvp short-circuit, linearize.py:63-64)
+  int fbad;         // an RHS evaluation produced non-finite cells
+  int pad_;
+  double eps;       // FD step for the next JVP (linearize.py:65)
+  double ynorm;     // ||y|| of the current y
+  double pnorm;
+  double residual;
+  double blowup;    // 1e120 * max(1, ||v||)   (leja.py:122)
+  double unorm;     // ||u|| of the frozen linearization
+  double dt, q, theta, tol;
+};
+
+enum LejaStatus {
+  LJ_RUNNING = 0,
+  LJ_CONVERGED = 1,
+  LJ_BLOWUP = 2,       // Newton basis blew up: non-converged result (leja.py:135-139)
+  LJ_RHS_BAD = 3,      // non-finite RHS: the reference raises RhsBlowupError
+  LJ_NEED_COEFFS = 4,  // m reached the coefficient chunk size (leja.py:128-130)
+  LJ_EXHAUSTED = 5,    // 499 terms without convergence (leja.py:149-150)
+};
+
+enum StencilMode { MODE_RHS = 0, MODE_JVP = 1, MODE_LEJA = 2 };
+
+struct StencilArgs {
+  Geom g;
+  const double* u;     // base state, 8 planes of nx*ny
+  const double* dir;   // JVP direction (MODE_JVP)
+  const double* fu;    // cached F(u)
+  double* out;         // MODE_RHS: F(u); MODE_JVP: J w
+  double eps;          // MODE_JVP
+  // MODE_LEJA
+  double* ybuf[2];
+  double* pbuf[2];
+  const double* coeffs;
+  const double* xi;
+  LejaCtl* ctl;
+  // reductions / flags
+  double* partials;    // [grid][2]
+  unsigned* ticket;
+  double* result;      // MODE_JVP: ||J w||
+  int* bad;            // |= 1 when a non-finite F cell is produced
+  int units_x, nunits, seg_rows;
+};
+
+constexpr int SW = 128;          // threads per block = ghost-extended columns per strip
+constexpr int SOUT = SW - 4;     // output columns per strip
+size_t stencil_smem_bytes();
+void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows, int& grid);
+cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s);
+
+// Vector kernels (vec.cu).
+struct RedBuf {
+  double* partials;    // [max_grid][4]
+  unsigned* ticket;
+  double* result;      // [8]
+  int grid;
+};
+// result[0] = ||x||
+cudaError_t launch_norm(const double* x, long long n, RedBuf rb, cudaStream_t s);
+// out = c0*v0 + c1*v1 + c2*v2 + c3*v3 (left to right; null v ends the sum);
+// result[0] = ||out|| when want_norm, result[1] = 1 if any non-finite entry.
+cudaError_t launch_lincomb(double* out, long long n, const double* const* v,
+                           const double* c, int nterms, int want_norm, RedBuf rb,
+                           cudaStream_t s);
+// out = x / d (IEEE), result[0] = ||out|| when want_norm.
+cudaError_t launch_divide(double* out, const double* x, double d, long long n,
+                          int want_norm, RedBuf rb, cudaStream_t s);
+// result[0] = ||a - b||, result[1] = ||b||.
+cudaError_t launch_diffnorm(const double* a, const double* b, long long n, RedBuf rb,
+                            cudaStream_t s);
+// result[0] = max |div B| (mhd.py:235-240 with the geometry's boundaries);
+// the div B field itself is written to `field` when non-null.
+cudaError_t launch_divb_max(const Geom& g, const double* u, double* field, RedBuf rb,
+                            cudaStream_t s);
+// result[0..7] = per-field plain sums (conserved_totals before the area factor).
+cudaError_t launch_field_sums(const double* u, long long plane, RedBuf rb, cudaStream_t s);
+// result[0] = max over cells of |vx| + cf, result[1] of |vy| + cf (harness.py:105-116).
+cudaError_t launch_cfl(const double* u, long long plane, double gamma, double mu0,
+                       RedBuf rb, cudaStream_t s);
+// Leja start: y0 = v, p0 = c0*v, ctl init (norm of v, blowup, eps).
+cudaError_t launch_leja_init(const double* v, long long n, double* y0, double* p0,
+                             LejaCtl* ctl, const double* coeffs, RedBuf rb, cudaStream_t s);
+// Generic Leja update for an arbitrary (host-supplied) matvec result w.
+cudaError_t launch_leja_update(const double* w, long long n, LejaCtl* ctl, double* const* ybuf,
+                               double* const* pbuf, const double* coeffs, const double* xi,
+                               RedBuf rb, cudaStream_t s);
+
+#ifdef __CUDACC__
+// Control update after one Newton term (leja.py:134-148); run by one thread
+// of the last CTA of the iteration kernel, after the deterministic reduction.
+__device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp, int bad,
+                                              int counted, double cm) {
+  const double kSqrtEps = 1.4901161193847656e-08;  // linearize.py:15
+  ctl->iters += 1;
+  if (counted) ctl->rhs_calls += 1;
+  if (bad) {  // mhd.py:225-231 raised inside the matvec
+    ctl->fbad = 1;
+    ctl->status = LJ_RHS_BAD;
+    return;
+  }
+  const double ny = sqrt(sy);
+  if (!isfinite(ny) || ny > ctl->blowup) {
+    ctl->residual = CUDART_INF;
+    ctl->status = LJ_BLOWUP;
+    return;
+  }
+  const double np = sqrt(sp);
+  const double res = __ddiv_rn(__dmul_rn(fabs(cm), ny), fmax(1.0, np));
+  ctl->cur ^= 1;
+  ctl->residual = res;
+  ctl->ynorm = ny;
+  ctl->pnorm = np;
+  if (res <= ctl->tol) {
+    if (ctl->small_prev) {
+      ctl->status = LJ_CONVERGED;
+      return;
+    }
+    ctl->small_prev = 1;
+  } else {
+    ctl->small_prev = 0;
+  }
+  ctl->m += 1;
+  if (ctl->m >= 500) {
+    ctl->status = LJ_EXHAUSTED;
+    return;
+  }
+  if (ctl->m >= ctl->ncoef) ctl->status = LJ_NEED_COEFFS;
+  ctl->zero_dir = (ny == 0.0);
+  ctl->eps = __ddiv_rn(__dmul_rn(kSqrtEps, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
+                       ny < 1e-300 ? 1e-300 : ny);
+}
+#endif
+
+}  // namespace xb

@@ -1,0 +1,227 @@
+"""Real Leja points and phi-function actions by Newton interpolation on the B200.
+
+Host mirror of the reference module ``pkg/src/xmhd/leja.py`` (same names,
+signatures, result type and non-convergence-as-a-flag behaviour).
+
+When the matvec is the frozen MHD Jacobian (``JacobianAction`` over a device
+``RhsOperator(MhdRhs)``), the whole Newton recurrence runs device-side: every
+term is one fused stencil launch that forms F(u + eps*y), the FD Jacobian
+action, the next basis vector, the interpolant update and both norms, and the
+last CTA updates the convergence control in device memory (csrc/stencil.cu).
+The host only intervenes when the coefficient chunk must grow
+(leja.py:128-130), keeping the reference's coefficient cache semantics.
+
+Any other matvec callable runs the same recurrence with the vector update in
+a device kernel around the caller's matvec.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from paper_2108_13622_b200 import _lib
+from paper_2108_13622_b200 import _ops
+from paper_2108_13622_b200.phi import _check_order, _phi_divided_diffs
+
+LEJA_MAX = 500       # leja.py:15
+_GRID_SIZE = 10001   # leja.py:18
+
+_sequence_cache = None
+_coeff_cache = {}
+
+
+def _greedy_leja(count):
+    """Sequential argmax of the log-distance product over a uniform grid (leja.py:24-37)."""
+    cand = np.linspace(-2.0, 2.0, _GRID_SIZE)
+    out = np.empty(count)
+    out[0] = 2.0
+    with np.errstate(divide="ignore"):
+        score = np.log(np.abs(cand - out[0]))
+        for k in range(1, count):
+            top = score.max()
+            # symmetric ties resolve toward the positive candidate
+            near = np.nonzero(score >= top - 1e-12 * max(1.0, abs(top)))[0]
+            out[k] = cand[near[np.argmax(cand[near])]]
+            score += np.log(np.abs(cand - out[k]))
+    return out
+
+
+def leja_points(count=LEJA_MAX):
+    """The first `count` Leja points of [-2, 2], starting from 2 (leja.py:40-53)."""
+    global _sequence_cache
+    if not 1 <= count <= LEJA_MAX:
+        raise ValueError(f"count must lie in [1, {LEJA_MAX}], got {count}")
+    if _sequence_cache is None:
+        seq = _greedy_leja(LEJA_MAX)
+        seq.setflags(write=False)
+        _sequence_cache = seq
+    return _sequence_cache[:count]
+
+
+@dataclass(frozen=True)
+class ShiftScale:
+    """Affine map placing the spectral interval [-alpha, 0] onto [-2, 2] (leja.py:56-60)."""
+    q: float
+    theta: float
+
+
+def shift_and_scale(alpha):
+    """q = -alpha/2, theta = alpha/4 (leja.py:63-72)."""
+    if alpha <= 0:
+        raise ValueError("spectral magnitude must be positive; "
+                         "callers handle the degenerate spectrum separately")
+    return ShiftScale(q=-0.5 * alpha, theta=0.25 * alpha)
+
+
+@dataclass
+class PhiApplyResult:
+    """Outcome of one iterative phi-function action (leja.py:75-81)."""
+    vector: object
+    iterations: int
+    converged: bool
+    residual: float
+
+
+def _newton_coeffs(l, q, theta, count):
+    """Divided differences of xi -> phi_l(q + theta*xi) at the Leja points, / theta**l.
+
+    Cached per exact (l, q, theta) with the reference's FIFO policy
+    (leja.py:84-100); the heavy part runs in the native C++ port.
+    """
+    key = (l, q, theta)
+    hit = _coeff_cache.get(key)
+    if hit is not None and hit.size >= count:
+        return hit
+    xi = leja_points(LEJA_MAX)[:count]
+    coeffs = _phi_divided_diffs(l, q + theta * xi, subdiag=theta) / theta ** l
+    if len(_coeff_cache) > 64:
+        _coeff_cache.pop(next(iter(_coeff_cache)))
+    _coeff_cache[key] = coeffs
+    return coeffs
+
+
+class JacobianAction:
+    """The matvec w -> jvp(lin, w) of a frozen linearization.
+
+    ``_PhiBroker`` hands this object to ``apply_phi_leja``; when the
+    linearization wraps the device MHD operator the Leja loop is fused.
+    """
+
+    def __init__(self, lin):
+        self.lin = lin
+
+    @property
+    def fused(self):
+        return self.lin.mhd is not None
+
+    def __call__(self, w):
+        from paper_2108_13622_b200.linearize import jvp
+        return jvp(self.lin, w)
+
+
+def _grow(l, q, theta, chunk, coeffs, m):
+    """Coefficient growth at m >= coeffs.size exactly as leja.py:128-130."""
+    chunk = min(2 * chunk, LEJA_MAX)
+    coeffs = _newton_coeffs(l, q, theta, chunk)
+    if m >= coeffs.size:
+        # the reference indexes coeffs[m] next and fails the same way
+        raise IndexError(f"index {m} is out of bounds for axis 0 with size {coeffs.size}")
+    return chunk, coeffs
+
+
+def _ptr_d(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def apply_phi_leja(l, matvec, v, dt, shift, tol):
+    """Approximate phi_l(J dt) v with J available only through `matvec` (leja.py:103-150).
+
+    Newton terms are added one at a time (one matvec each); converged after two
+    consecutive increments below tol * max(1, ||result||); non-convergence
+    (500-term cap, basis overflow) is reported in the result, not raised.
+    """
+    _check_order(l)
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    xi = np.ascontiguousarray(leja_points(LEJA_MAX))
+    if isinstance(matvec, JacobianAction) and matvec.fused:
+        return _apply_fused(l, matvec.lin, v, dt, shift, tol, xi)
+    return _apply_generic(l, matvec, v, dt, shift, tol, xi)
+
+
+def _apply_fused(l, lin, v, dt, shift, tol, xi):
+    from paper_2108_13622_b200.linearize import RhsBlowupError
+    q, theta = shift.q, shift.theta
+    mhd = lin.mhd
+    lib = _lib.load()
+    vd = _ops.as_device(v).reshape(-1)
+    chunk = 64
+    coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, chunk))
+    st = _lib.LejaState()
+    h = mhd.ctx.bind_stream()
+    rc = lib.xmhd_leja_start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
+                             float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
+                             float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
+                             int(coeffs.size), ctypes.byref(st))
+    _lib.check(rc, "xmhd_leja_start")
+    while st.status == _lib.LEJA_NEED_COEFFS:
+        chunk, grown = _grow(l, q, theta, chunk, coeffs, st.m)
+        coeffs = np.ascontiguousarray(grown)
+        rc = lib.xmhd_leja_resume(h, _ptr_d(coeffs), int(coeffs.size), ctypes.byref(st))
+        _lib.check(rc, "xmhd_leja_resume")
+    lin.rhs.calls += st.rhs_calls
+    if st.status == _lib.LEJA_RHS_NONFINITE:
+        # the reference raises from inside the matvec (mhd.py:225-231); rebuild
+        # the failing state u + eps*y to report the same cells
+        y = torch.empty_like(vd)
+        _lib.check(lib.xmhd_leja_current_y(h, _lib.ptr(y)), "xmhd_leja_current_y")
+        x = _ops.lincomb((1.0, st.eps), (lin.base_state, y))
+        try:
+            mhd(x)
+        except RhsBlowupError as err:
+            raise err
+        raise RhsBlowupError("non-finite rhs inside the fused Leja iteration")
+    p = torch.empty_like(vd)
+    _lib.check(lib.xmhd_leja_result(h, _lib.ptr(p)), "xmhd_leja_result")
+    return PhiApplyResult(vector=_ops.like(p, v), iterations=int(st.iterations),
+                          converged=st.status == _lib.LEJA_CONVERGED,
+                          residual=float(st.residual))
+
+
+def _apply_generic(l, matvec, v, dt, shift, tol, xi):
+    q, theta = shift.q, shift.theta
+    lib = _lib.load()
+    host_io = _ops.is_host(v)
+    vd = _ops.as_device(v, copy=True).reshape(-1)
+    ctx = _ops.util_ctx()
+    h = ctx.bind_stream()
+    chunk = 64
+    coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, chunk))
+    st = _lib.LejaState()
+    rc = lib.xmhd_leja_generic_start(h, _lib.ptr(vd), vd.numel(), float(dt), float(q),
+                                     float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
+                                     int(coeffs.size), ctypes.byref(st))
+    _lib.check(rc, "xmhd_leja_generic_start")
+    y = torch.empty_like(vd)
+    try:
+        while st.status in (_lib.LEJA_RUNNING, _lib.LEJA_NEED_COEFFS):
+            if st.status == _lib.LEJA_NEED_COEFFS:
+                chunk, grown = _grow(l, q, theta, chunk, coeffs, st.m)
+                coeffs = np.ascontiguousarray(grown)
+                rc = lib.xmhd_leja_generic_resume(h, _ptr_d(coeffs), int(coeffs.size),
+                                                  ctypes.byref(st))
+                _lib.check(rc, "xmhd_leja_generic_resume")
+                continue
+            _lib.check(lib.xmhd_leja_current_y(h, _lib.ptr(y)), "xmhd_leja_current_y")
+            w = matvec(_ops.to_host(y) if host_io else y)
+            wd = _ops.as_device(w).reshape(-1)
+            rc = lib.xmhd_leja_generic_step(h, _lib.ptr(wd), ctypes.byref(st))
+            _lib.check(rc, "xmhd_leja_generic_step")
+    finally:
+        p = torch.empty_like(vd)
+        _lib.check(lib.xmhd_leja_generic_result(h, _lib.ptr(p)), "xmhd_leja_generic_result")
+    return PhiApplyResult(vector=_ops.like(p, v), iterations=int(st.iterations),
+                          converged=st.status == _lib.LEJA_CONVERGED,
+                          residual=float(st.residual))

@@ -1,7 +1,18 @@
 import os
 import sys
 
-import pytest
+# The golden vectors were produced with single-threaded OpenBLAS (np.linalg.norm
+# = ddot, whose summation order depends on the thread count).
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import pytest  # noqa: E402
+
+try:
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+except Exception:  # pragma: no cover
+    pass
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:

@@ -1,0 +1,124 @@
+"""CPU-side checks: the C-ABI library builds, loads and exports every declared
+symbol; the host logic around the kernels (coefficients, Leja points,
+controllers) matches the reference's golden vectors.  No device compute here."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2108_13622_b200 import _lib
+    return _lib.load()
+
+
+def header_functions():
+    text = open(os.path.join(REPO, "include", "xmhd_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(xmhd_\w+)\s*\(",
+                                 text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2108_13622_b200 import _lib
+    names = header_functions()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.EXPORTED)
+
+
+def test_library_is_sm100a(lib):
+    import subprocess
+    from paper_2108_13622_b200 import _lib
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.library_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_native_divided_differences_bitwise(lib):
+    from paper_2108_13622_b200 import leja, phi
+    g = golden_io.arrays("coeff_cases")
+    nodes = leja.leja_points(64)
+    for l in (0, 1, 3):
+        assert np.array_equal(phi.divided_differences(l, nodes).coeffs, g[f"divdiff_l{l}"])
+
+
+def test_newton_coefficients_bitwise(lib):
+    from paper_2108_13622_b200 import leja
+    g = golden_io.arrays("coeff_cases")
+    for m in golden_io.meta()["coeff"]:
+        leja._coeff_cache.clear()
+        c = leja._newton_coeffs(m["l"], m["q"], m["theta"], m["count"])
+        assert np.array_equal(c, g[m["key"]]), m["key"]
+
+
+def test_coefficient_cache_contract(lib):
+    from paper_2108_13622_b200 import leja
+    leja._coeff_cache.clear()
+    big = leja._newton_coeffs(1, -5.0, 2.5, 256)
+    assert leja._newton_coeffs(1, -5.0, 2.5, 64) is big
+    for k in range(70):
+        leja._newton_coeffs(0, -1.0 - k, 0.5 + k, 64)
+    assert len(leja._coeff_cache) == 65
+    assert (1, -5.0, 2.5) not in leja._coeff_cache
+
+
+def test_leja_points_bitwise():
+    from paper_2108_13622_b200 import leja
+    g = golden_io.arrays("coeff_cases")
+    assert np.array_equal(leja.leja_points(500), g["leja_points"])
+    assert leja.leja_points(1)[0] == 2.0
+    with pytest.raises(ValueError):
+        leja.leja_points(0)
+    with pytest.raises(ValueError):
+        leja.leja_points(501)
+
+
+def test_shift_and_scale():
+    from paper_2108_13622_b200 import shift_and_scale
+    s = shift_and_scale(4.0)
+    assert s.q == -2.0 and s.theta == 1.0
+    with pytest.raises(ValueError):
+        shift_and_scale(0.0)
+
+
+def test_controllers_worked_examples():
+    import math
+    from paper_2108_13622_b200 import controllers as c
+    k = c.ControllerConstants()
+    assert abs(c.cost_next(0.1, 0.05, 100.0, 100.0, k) - 0.1 * 1.37412002) <= 1e-12
+    assert abs(c.cost_next(0.1, 0.05, 200.0, 100.0, k) - 0.1 * 0.64446017) <= 1e-12
+    delta = (math.log(1e6) - math.log(1.0)) / (math.log(0.1) - math.log(0.2))
+    s = math.exp(-0.65241444 * math.tanh(0.26862269 * delta))
+    assert abs(c.cost_next(0.1, 0.2, 1e6, 1.0, k) - 0.1 * s) <= 1e-12
+    assert c.traditional_next(0.1, 0.0, 1e-4, 3) == 0.2
+    assert c.combine(1.0, 2.0) == 1.0 and c.accept(1e-4, 1e-4)
+
+
+def test_controllers_match_oracle():
+    from oracle import steppers_np as st
+    from paper_2108_13622_b200 import controllers as c
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        dt, dtp = rng.uniform(1e-4, 1e-1, 2)
+        cost, costp = rng.uniform(1.0, 1e4, 2)
+        err, tol = 10.0 ** rng.uniform(-9, -2), 10.0 ** rng.uniform(-8, -3)
+        p = int(rng.integers(1, 5))
+        assert c.cost_next(dt, dtp, cost, costp) == st.cost_next(dt, dtp, cost, costp)
+        assert c.traditional_next(dt, err, tol, p) == st.trad_next(dt, err, tol, p)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_compute_without_gpu_fails_loudly():
+    import paper_2108_13622_b200 as xb
+    st = xb.StateGrid.zeros(4, 4, 0.1, 0.1)
+    with pytest.raises(xb.NativeUnavailable):
+        xb.mhd_rhs(st, xb.MHDParams(0.0, 0.0, 0.0))
