@@ -128,6 +128,14 @@ int xmhd_leja_generic_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef,
                              xmhd_leja_state* st);
 int xmhd_leja_generic_result(xmhd_ctx* ctx, double* p_out);
 
+/* Benchmark hook: average duration (CUDA events on the context stream) of
+ * n_iter back-to-back fused Leja iteration kernels with the convergence test
+ * disabled (tol = 0); coeffs500 holds 500 Newton coefficients. */
+int xmhd_time_leja_iterations(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                              const double* v, double dt, double q, double theta,
+                              const double* xi, const double* coeffs500, int n_iter,
+                              double* ms_per_iter);
+
 /* Host C++ port of _phi_divided_diffs (phi.py:99-144): first column of
  * phi_l of the bidiagonal node matrix, bitwise equal to the NumPy routine.
  * out has n entries. */

@@ -68,6 +68,7 @@ _SIGS = {
     "xmhd_leja_generic_step": (_I, [_P, _P, ctypes.POINTER(LejaState)]),
     "xmhd_leja_generic_resume": (_I, [_P, _PD, _I, ctypes.POINTER(LejaState)]),
     "xmhd_leja_generic_result": (_I, [_P, _P]),
+    "xmhd_time_leja_iterations": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _PD, _PD, _I, _PD]),
     "xmhd_phi_divided_diffs": (_I, [_I, _PD, _I, _D, _PD]),
 }
 

@@ -530,6 +530,50 @@ int xmhd_leja_generic_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_
   return XMHD_OK;
 }
 
+int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                              const double* v, double dt, double q, double theta,
+                              const double* xi, const double* coeffs500, int n_iter,
+                              double* ms_per_iter) {
+  if (!c || !u || !fu || !v || !xi || !coeffs500 || !ms_per_iter) return fail(XMHD_BADARG, "null arg");
+  if (n_iter < 1 || n_iter > 400) return fail(XMHD_BADARG, "n_iter must be in [1, 400]");
+  const long long n = NF * c->g.plane;
+  c->leja_u = u;
+  c->leja_fu = fu;
+  // tol = 0: the convergence test never fires, every launch does a full term
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, 0.0, xi, coeffs500, 500);
+  if (rc) return rc;
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.fu = fu;
+  a.ybuf[0] = c->ybuf[0];
+  a.ybuf[1] = c->ybuf[1];
+  a.pbuf[0] = c->pbuf[0];
+  a.pbuf[1] = c->pbuf[1];
+  a.coeffs = c->coeffs_d;
+  a.xi = c->xi_d;
+  a.ctl = c->ctl;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));  // warm-up term
+  CK(cudaEventRecord(e0, c->stream));
+  for (int k = 0; k < n_iter; ++k) CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaEventSynchronize(e1));
+  c->launches += n_iter + 2;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  rc = sync_ctl(c);
+  if (rc) return rc;
+  if (c->ctl_h->status != LJ_RUNNING)
+    return fail(XMHD_BADARG, "timing run left RUNNING early (status " +
+                                 std::to_string(c->ctl_h->status) + ")");
+  *ms_per_iter = (double)ms / n_iter;
+  return XMHD_OK;
+}
+
 int xmhd_leja_generic_result(xmhd_ctx* c, double* p_out) {
   int rc = xmhd_leja_result(c, p_out);
   c->gen_n = 0;
