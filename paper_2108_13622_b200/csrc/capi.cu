@@ -40,6 +40,7 @@ struct xmhd_ctx {
   const double* leja_fu = nullptr;
   long long launches = 0;
   int batch_max = 64;
+  bool force_ieee = false;
 };
 
 namespace {
@@ -199,6 +200,8 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.q = q;
   h.theta = theta;
   h.tol = tol;
+  h.thetad = make_divisor(theta, c->force_ieee);
+  h.force_ieee = c->force_ieee ? 1 : 0;
   *c->ctl_h = h;
   CK(cudaMemcpyAsync(c->ctl, c->ctl_h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
@@ -222,6 +225,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
   if (bc_y < XMHD_BC_PERIODIC || bc_y > XMHD_BC_HALO) return fail(XMHD_BADARG, "bad bc_y");
   xmhd_ctx* c = new xmhd_ctx();
   const bool ieee = std::getenv("XMHD_DIV_IEEE") && std::atoi(std::getenv("XMHD_DIV_IEEE"));
+  c->force_ieee = ieee;
   Geom& g = c->g;
   std::memset(&g, 0, sizeof(g));
   g.nx = nx;
@@ -357,6 +361,7 @@ int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const
   a.fu = fu;
   a.out = out;
   a.eps = eps;
+  a.epsd = make_divisor(eps, c->force_ieee);
   CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
   c->launches++;
   if (called) *called = 1;

@@ -80,8 +80,47 @@ struct Geom {
   const double* halo_hi_dir;
 };
 
+// Compile-time variant of exact_div (the kind is a template parameter).
+template <int K>
+__device__ __forceinline__ double qdiv(double a, const Divisor& v) {
+  if (K == DIV_MUL) return __dmul_rn(a, v.r);
+  if (K == DIV_IEEE) return __ddiv_rn(a, v.d);
+  double q = __dmul_rn(a, v.r);
+  double e = __fma_rn(-q, v.d, a);
+  q = __fma_rn(e, v.r, q);
+  if (K == DIV_MK2) {
+    e = __fma_rn(-q, v.d, a);
+    q = __fma_rn(e, v.r, q);
+  }
+  return q;
+}
+
+// Runtime divisor for per-launch scalars (eps, theta): one or two corrections.
+__device__ __forceinline__ double rdiv(double a, const Divisor& v) {
+  double q = __dmul_rn(a, v.r);
+  double e = __fma_rn(-q, v.d, a);
+  q = __fma_rn(e, v.r, q);
+  if (v.kind == DIV_MK2) {
+    e = __fma_rn(-q, v.d, a);
+    q = __fma_rn(e, v.r, q);
+  } else if (v.kind == DIV_IEEE) {
+    q = __ddiv_rn(a, v.d);
+  }
+  return q;
+}
+
+// Divisor for a value known only on the device (RN reciprocal + exactness class).
+__device__ __forceinline__ Divisor make_divisor_dev(double d) {
+  Divisor v;
+  v.d = d;
+  v.r = __drcp_rn(d);
+  const double e = __fma_rn(-d, v.r, 1.0);   // exact: 1 - d*r
+  v.kind = (fabs(e) <= 5.551115123125783e-17) ? DIV_MK1 : DIV_MK2;   // 2^-54
+  return v;
+}
+
 __device__ __forceinline__ double over_mu0(double a, const Geom& g) {
-  return g.mu0_one ? a : exact_div(a, g.mu0d);
+  return g.mu0_one ? a : rdiv(a, g.mu0d);
 }
 
 // Primitive variables at one (ghost-extended) cell, mhd.py:144-155.
@@ -159,12 +198,13 @@ constexpr int NG = 6;
 
 // d/dx inputs: xl, xr = PD at (j, i-1), (j, i+1); d/dy inputs: yd, yu = PD at
 // (j-1, i), (j+1, i); own = PD at (j, i).
+template <int KX, int KY>
 __device__ __forceinline__ void diffusive_fluxes(const double xl[NPD], const double xr[NPD],
                                                  const double yd[NPD], const double yu[NPD],
                                                  const double own[NPD], const Geom& g,
                                                  double gx[NG], double gy[NG]) {
-#define DX(k) exact_div(__dsub_rn(xr[k], xl[k]), g.h2x)
-#define DY(k) exact_div(__dsub_rn(yu[k], yd[k]), g.h2y)
+#define DX(k) qdiv<KX>(__dsub_rn(xr[k], xl[k]), g.h2x)
+#define DY(k) qdiv<KY>(__dsub_rn(yu[k], yd[k]), g.h2y)
   double dvx_dx = DX(PD_VX), dvy_dx = DX(PD_VY), dvz_dx = DX(PD_VZ);
   double dvx_dy = DY(PD_VX), dvy_dy = DY(PD_VY), dvz_dy = DY(PD_VZ);
   double divv = __dadd_rn(dvx_dx, dvy_dy);

@@ -26,6 +26,10 @@ struct LejaCtl {
   double blowup;    // 1e120 * max(1, ||v||)   (leja.py:122)
   double unorm;     // ||u|| of the frozen linearization
   double dt, q, theta, tol;
+  Divisor epsd;     // eps with its RN reciprocal (exact division in the epilogue)
+  Divisor thetad;   // theta, likewise (host-computed)
+  int force_ieee;   // testing: plain IEEE division for eps as well
+  int pad2_;
 };
 
 enum LejaStatus {
@@ -46,6 +50,7 @@ struct StencilArgs {
   const double* fu;    // cached F(u)
   double* out;         // MODE_RHS: F(u); MODE_JVP: J w
   double eps;          // MODE_JVP
+  Divisor epsd;        // MODE_JVP: eps with its reciprocal
   // MODE_LEJA
   double* ybuf[2];
   double* pbuf[2];
@@ -146,6 +151,8 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
   ctl->zero_dir = (ny == 0.0);
   ctl->eps = __ddiv_rn(__dmul_rn(kSqrtEps, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
                        ny < 1e-300 ? 1e-300 : ny);
+  ctl->epsd = make_divisor_dev(ctl->eps);
+  if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
 }
 #endif
 

@@ -2,28 +2,36 @@
 // Leja/Newton iteration in one pass over HBM.
 //
 // Reference path (arxiv/paper_2108_13622, pkg/src/xmhd):
-//   mhd_rhs            mhd.py:127-232   (MODE_RHS)
+//   mhd_rhs            mhd.py:127-232     (MODE_RHS)
 //   jvp                linearize.py:56-67 (MODE_JVP: x = u + eps*w, (F(x) - F(u))/eps)
-//   apply_phi_leja     leja.py:133-148  (MODE_LEJA: the JVP above plus
+//   apply_phi_leja     leja.py:133-148    (MODE_LEJA: the JVP above plus
 //                      y' = ((dt*w) - (q*y))/theta - xi*y, p' = p + c*y',
 //                      ||y'||, ||p'|| and the convergence control, on device)
 //
 // Data layout: the reference's flat field-major (8, ny, nx) fp64 vector.
 //
 // Dataflow (one CTA = one y-segment of one column strip, sliding window):
-//   CTA of SW=128 threads owns ghost-extended columns [X0-2, X0+126) and marches
-//   the rows r = Y0-2 .. Y1+1.  Per row step:
+//   a CTA of SW=128 threads owns ghost-extended columns [X0-2, X0+126) and
+//   marches the rows r = Y0-2 .. Y1+1.  Per row step:
 //     P1  thread t forms x(r, c_t) (= u or u + eps*y, with boundary mirror /
-//         wrap), computes the primitives once, stores the 8 differentiated
-//         primitives (PD) and the 7 ideal x-fluxes (FX) in shared-memory rings
-//         and keeps its 7 ideal y-fluxes (FY) in registers;
+//         wrap) from registers loaded one step earlier, immediately issues the
+//         loads of row r+1, computes the primitives once and stores the 8
+//         differentiated primitives (PD), the 7 ideal x-fluxes (FX) and its 7
+//         ideal y-fluxes (FY) in shared-memory rings;
 //     P2  level-1 derivatives at row r-1 (PD of rows r-2, r-1, r) -> diffusive
-//         fluxes GX (shared ring) and GY (registers);
+//         fluxes GX (shared ring, x-neighbours read it) and GY (registers);
 //     P3  output row r-2: centred differences of FX, FY, GX, GY in the
-//         reference's association order, then the mode epilogue.
+//         reference's association order, then the mode epilogue whose
+//         operands (F(u), y, p at row r-2) were loaded at the start of the step.
 //   Every primitive / flux is evaluated once per cell (plus the 4-column and
 //   4-row halo of each CTA), so the kernel streams u, y, F(u), p once and
 //   writes y', p' once: 384 B per cell per Leja iteration.
+//   Two barriers per row step; the rings are sized so no other hazard exists.
+//
+// Divisions: constant divisors (2dx, 2dy, eps, theta, mu0) use a precomputed
+// RN reciprocal with Markstein correction (common.cuh), which is the correctly
+// rounded quotient; 2dx / 2dy kinds are template parameters.  Divisions by the
+// per-cell density stay IEEE divisions.
 #include <cfloat>
 #include <climits>
 #include "kernels.h"
@@ -33,8 +41,10 @@ namespace xb {
 namespace {
 
 // Slot -> field maps for the non-zero flux rows (compile-time in unrolled loops).
-__host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; }          // skip BX
-__host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }          // skip BY
+__host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; }   // skip BX
+__host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }   // skip BY
+
+constexpr int RING_PD = 3, RING_FX = 4, RING_FY = 4, RING_GX = 2;
 
 struct RowSrc {
   const double* u;     // row base of field 0 in the base state
@@ -114,12 +124,15 @@ __device__ __forceinline__ double sum_partials(const double* p, int nblk, int st
 
 }  // namespace
 
-template <int MODE>
+template <int MODE, int KX, int KY>
 __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
   extern __shared__ double smem[];
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
-  double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + 3 * NPD * SW);
-  double (*gxs)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(smem + 3 * NPD * SW + 3 * NFX * SW);
+  double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
+  double (*fys)[NFY][SW] =
+      reinterpret_cast<double (*)[NFY][SW]>(smem + (RING_PD * NPD + RING_FX * NFX) * SW);
+  double (*gxs)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(
+      smem + (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY) * SW);
   __shared__ double red[SW / 32];
   __shared__ int am_last;
 
@@ -128,17 +141,21 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
   // Per-launch scalars.
   double eps = a.eps;
+  Divisor epsd = a.epsd;
+  Divisor thd = epsd;
   const double* dir = a.dir;
   double* yout = nullptr;
   const double* pin = nullptr;
   double* pout = nullptr;
-  double dt = 0.0, q = 0.0, theta = 1.0, xim = 0.0, cm = 0.0;
+  double dt = 0.0, q = 0.0, xim = 0.0, cm = 0.0;
   int zero_dir = 0;
   if (MODE == MODE_LEJA) {
     const LejaCtl* c = a.ctl;
     if (c->status != LJ_RUNNING) return;
     const int cur = c->cur, m = c->m;
     eps = c->eps;
+    epsd = c->epsd;
+    thd = c->thetad;
     zero_dir = c->zero_dir;
     dir = a.ybuf[cur];
     yout = a.ybuf[cur ^ 1];
@@ -146,7 +163,6 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
     pout = a.pbuf[cur ^ 1];
     dt = c->dt;
     q = c->q;
-    theta = c->theta;
     xim = __ldg(a.xi + (m - 1));
     cm = __ldg(a.coeffs + m);
   }
@@ -159,7 +175,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
     const long long n = (long long)NF * g.plane;
     for (long long i = (long long)blockIdx.x * SW + t; i < n; i += (long long)gridDim.x * SW) {
       const double y = dir[i];
-      const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), theta),
+      const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
       const double pn = __dadd_rn(pin[i], __dmul_rn(cm, yn));
       yout[i] = yn;
@@ -179,33 +195,63 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       const int c_out = X0 + t - 2;
       const bool col_ok = (t >= 2) && (t < SW - 2) && (c_out < g.nx);
       const int tl = max(t - 1, 0), tr = min(t + 1, SW - 1);
+      const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
 
-      double fy1[NFY], fy2[NFY], fy3[NFY], gy1[NG], gy2[NG];
-#pragma unroll
-      for (int k = 0; k < NFY; ++k) fy1[k] = fy2[k] = fy3[k] = 0.0;
+      double gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
 
+      // prefetch registers: state (and direction) of the next row to consume
+      double nu[NF], nd[NF];
+      {
+        const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc);
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          nu[f] = __ldg(rs.u + f * rs.fs + cs);
+          if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
+        }
+      }
+
       const int nsteps = (Y1 - Y0) + 4;
-      int s3 = 0;  // s % 3
+      int s3 = 0, s4 = 0;  // s % 3, s % 4
       for (int s = 0; s < nsteps; ++s) {
         const int r = Y0 - 2 + s;
-        const int m1 = (s3 + 2) % 3;  // ring slot of row r-1
-        const int m2 = (s3 + 1) % 3;  // ring slot of row r-2
+        const int m1 = (s3 == 0) ? 2 : s3 - 1;  // PD slot of row r-1
+        const int m2 = (s3 == 2) ? 0 : s3 + 1;  // PD slot of row r-2
+        const bool out_row = (s >= 4) && col_ok;
+        const long long obase = (long long)(r - 2) * g.nx + c_out;
 
-        // ---- P1: state at (r, cg), primitives, PD + FX to smem, FY to regs
-        double fyn[NFY];
-        {
-          const RowSrc rs = row_source(r, g, a.u, MODE == MODE_RHS ? nullptr : dir);
-          double x[NF];
+        // epilogue operands of output row r-2: issue now, consume in P3
+        double efu[NF], ey[NF], ep[NF];
+        if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            double v = __ldg(rs.u + f * rs.fs + cs);
-            if (MODE != MODE_RHS) v = __dadd_rn(v, __dmul_rn(eps, __ldg(rs.d + f * rs.fs + cs)));
-            x[f] = v;
+            const long long i = obase + f * g.plane;
+            efu[f] = __ldg(a.fu + i);
+            if (MODE == MODE_LEJA) {
+              ey[f] = __ldg(dir + i);
+              ep[f] = __ldg(pin + i);
+            }
           }
+        }
+
+        // ---- P1: state at (r, cg) from the prefetch registers
+        {
+          double x[NF];
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
+          const RowSrc rcur = row_source(r, g, a.u, dsrc);
           if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-          if (rs.flip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+          if (rcur.flip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+          if (s + 1 < nsteps) {
+            const RowSrc rs = row_source(r + 1, g, a.u, dsrc);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              nu[f] = __ldg(rs.u + f * rs.fs + cs);
+              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
+            }
+          }
           Prim p;
           primitives(x, g, p);
           pd[s3][PD_VX][t] = p.vx;
@@ -216,11 +262,13 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           pd[s3][PD_BZ][t] = p.bz;
           pd[s3][PD_T][t] = p.temp;
           pd[s3][PD_B2][t] = p.b2;
-          double fxv[NFX];
-          flux_x(p, g, fxv);
+          double fv[NFX];
+          flux_x(p, g, fv);
 #pragma unroll
-          for (int k = 0; k < NFX; ++k) fxs[s3][k][t] = fxv[k];
-          flux_y(p, g, fyn);
+          for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
+          flux_y(p, g, fv);
+#pragma unroll
+          for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
         }
         __syncthreads();
 
@@ -239,67 +287,66 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             own[k] = pd[m1][k][t];
           }
           double gxv[NG];
-          diffusive_fluxes(xl, xr, yd, yu, own, g, gxv, gyn);
+          diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyn);
 #pragma unroll
           for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
         }
         __syncthreads();
 
         // ---- P3: output row o = r-2
-        if (s >= 4 && col_ok) {
-          const int o = r - 2;
-          const int gs = s & 1;  // GX ring slot of row r-2
+        if (out_row) {
+          const int fx2 = (s4 + 2) & 3;   // FX / FY slot of row r-2 (s-2 mod 4)
+          const int fy1 = (s4 + 3) & 3;   // FY slot of row r-1
+          const int fy3 = (s4 + 1) & 3;   // FY slot of row r-3
+          const int gs = s & 1;           // GX slot of row r-2
           double F[NF];
           // ideal part: out = -(dFX/2dx); out -= dFY/2dy       (mhd.py:177-178)
 #pragma unroll
-          for (int k = 0; k < NFX; ++k) {
-            const int f = fx_field(k);
-            F[f] = -exact_div(__dsub_rn(fxs[m2][k][tr], fxs[m2][k][tl]), g.h2x);
-          }
+          for (int k = 0; k < NFX; ++k)
+            F[fx_field(k)] = -qdiv<KX>(__dsub_rn(fxs[fx2][k][tr], fxs[fx2][k][tl]), g.h2x);
           F[BX] = -0.0;
 #pragma unroll
           for (int k = 0; k < NFY; ++k) {
             const int f = fy_field(k);
-            F[f] = __dsub_rn(F[f], exact_div(__dsub_rn(fy1[k], fy3[k]), g.h2y));
+            F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(fys[fy1][k][t], fys[fy3][k][t]), g.h2y));
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
           if (g.diffusive) {
             // out += dGX/2dx; out += dGY/2dy                 (mhd.py:222-223)
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BX] = __dadd_rn(F[BX], 0.0);
-            F[MX] = __dadd_rn(F[MX], exact_div(__dsub_rn(gxs[gs][0][tr], gxs[gs][0][tl]), g.h2x));
-            F[MY] = __dadd_rn(F[MY], exact_div(__dsub_rn(gxs[gs][1][tr], gxs[gs][1][tl]), g.h2x));
-            F[MZ] = __dadd_rn(F[MZ], exact_div(__dsub_rn(gxs[gs][2][tr], gxs[gs][2][tl]), g.h2x));
-            F[BY] = __dadd_rn(F[BY], exact_div(__dsub_rn(gxs[gs][3][tr], gxs[gs][3][tl]), g.h2x));
-            F[BZ] = __dadd_rn(F[BZ], exact_div(__dsub_rn(gxs[gs][4][tr], gxs[gs][4][tl]), g.h2x));
-            F[EN] = __dadd_rn(F[EN], exact_div(__dsub_rn(gxs[gs][5][tr], gxs[gs][5][tl]), g.h2x));
+            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gxs[gs][0][tr], gxs[gs][0][tl]), g.h2x));
+            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gxs[gs][1][tr], gxs[gs][1][tl]), g.h2x));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gxs[gs][2][tr], gxs[gs][2][tl]), g.h2x));
+            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gxs[gs][3][tr], gxs[gs][3][tl]), g.h2x));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gxs[gs][4][tr], gxs[gs][4][tl]), g.h2x));
+            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gxs[gs][5][tr], gxs[gs][5][tl]), g.h2x));
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BY] = __dadd_rn(F[BY], 0.0);
-            F[MX] = __dadd_rn(F[MX], exact_div(__dsub_rn(gyn[0], gy2[0]), g.h2y));
-            F[MY] = __dadd_rn(F[MY], exact_div(__dsub_rn(gyn[1], gy2[1]), g.h2y));
-            F[MZ] = __dadd_rn(F[MZ], exact_div(__dsub_rn(gyn[2], gy2[2]), g.h2y));
-            F[BX] = __dadd_rn(F[BX], exact_div(__dsub_rn(gyn[3], gy2[3]), g.h2y));
-            F[BZ] = __dadd_rn(F[BZ], exact_div(__dsub_rn(gyn[4], gy2[4]), g.h2y));
-            F[EN] = __dadd_rn(F[EN], exact_div(__dsub_rn(gyn[5], gy2[5]), g.h2y));
+            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gyn[0], gy2[0]), g.h2y));
+            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gyn[1], gy2[1]), g.h2y));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gyn[2], gy2[2]), g.h2y));
+            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gyn[3], gy2[3]), g.h2y));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gyn[4], gy2[4]), g.h2y));
+            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gyn[5], gy2[5]), g.h2y));
           }
-          const long long base = (long long)o * g.nx + c_out;
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            const long long i = base + f * g.plane;
+            const long long i = obase + f * g.plane;
             if (!isfinite(F[f])) bad = 1;
             if (MODE == MODE_RHS) {
               a.out[i] = F[f];
             } else if (MODE == MODE_JVP) {
-              const double jv = __ddiv_rn(__dsub_rn(F[f], __ldg(a.fu + i)), eps);
+              const double jv = rdiv(__dsub_rn(F[f], efu[f]), epsd);
               a.out[i] = jv;
               acc0 = __fma_rn(jv, jv, acc0);
             } else {
-              const double w = __ddiv_rn(__dsub_rn(F[f], __ldg(a.fu + i)), eps);
-              const double y = dir[i];
+              const double w = rdiv(__dsub_rn(F[f], efu[f]), epsd);
+              const double y = ey[f];
               const double yn = __dsub_rn(
-                  __ddiv_rn(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), theta),
+                  rdiv(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                   __dmul_rn(xim, y));
-              const double pn = __dadd_rn(pin[i], __dmul_rn(cm, yn));
+              const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
               yout[i] = yn;
               pout[i] = pn;
               acc0 = __fma_rn(yn, yn, acc0);
@@ -307,14 +354,13 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             }
           }
         }
-        __syncthreads();
 
-#pragma unroll
-        for (int k = 0; k < NFY; ++k) { fy3[k] = fy2[k]; fy2[k] = fy1[k]; fy1[k] = fyn[k]; }
 #pragma unroll
         for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
         s3 = (s3 == 2) ? 0 : s3 + 1;
+        s4 = (s4 + 1) & 3;
       }
+      __syncthreads();   // rings are reused by the next unit
     }
   }
 
@@ -349,7 +395,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 }
 
 size_t stencil_smem_bytes() {
-  return sizeof(double) * (size_t)SW * (3 * NPD + 3 * NFX + 2 * NG);
+  return sizeof(double) * (size_t)SW *
+         (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG);
 }
 
 // Work decomposition: column strips of SOUT outputs x y-segments; the
@@ -374,40 +421,44 @@ void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_ro
   grid = nunits < slots ? nunits : slots;
 }
 
-cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s) {
-  static bool attr_done[3] = {false, false, false};
+namespace {
+
+template <int MODE, int KX, int KY>
+cudaError_t launch_one(const StencilArgs& a, int grid, cudaStream_t s) {
+  static bool attr_done = false;
   const size_t smem = stencil_smem_bytes();
-  cudaError_t err = cudaSuccess;
-  switch (mode) {
-    case MODE_RHS:
-      if (!attr_done[0]) {
-        err = cudaFuncSetAttribute(stencil_kernel<MODE_RHS>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        attr_done[0] = true;
-      }
-      stencil_kernel<MODE_RHS><<<grid, SW, smem, s>>>(a);
-      break;
-    case MODE_JVP:
-      if (!attr_done[1]) {
-        err = cudaFuncSetAttribute(stencil_kernel<MODE_JVP>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        attr_done[1] = true;
-      }
-      stencil_kernel<MODE_JVP><<<grid, SW, smem, s>>>(a);
-      break;
-    default:
-      if (!attr_done[2]) {
-        err = cudaFuncSetAttribute(stencil_kernel<MODE_LEJA>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (err != cudaSuccess) return err;
-        attr_done[2] = true;
-      }
-      stencil_kernel<MODE_LEJA><<<grid, SW, smem, s>>>(a);
-      break;
+  if (!attr_done) {
+    cudaError_t err = cudaFuncSetAttribute(stencil_kernel<MODE, KX, KY>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) return err;
+    attr_done = true;
   }
+  stencil_kernel<MODE, KX, KY><<<grid, SW, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_mode(const StencilArgs& a, int grid, cudaStream_t s) {
+  const int kx = a.g.h2x.kind, ky = a.g.h2y.kind;
+  if (kx == DIV_IEEE || ky == DIV_IEEE) return launch_one<MODE, DIV_IEEE, DIV_IEEE>(a, grid, s);
+  if (kx == DIV_MUL && ky == DIV_MUL) return launch_one<MODE, DIV_MUL, DIV_MUL>(a, grid, s);
+  // a power-of-two divisor is also exact on the one-correction path
+  const int x2 = (kx == DIV_MK2), y2 = (ky == DIV_MK2);
+  if (x2 && y2) return launch_one<MODE, DIV_MK2, DIV_MK2>(a, grid, s);
+  if (x2) return launch_one<MODE, DIV_MK2, DIV_MK1>(a, grid, s);
+  if (y2) return launch_one<MODE, DIV_MK1, DIV_MK2>(a, grid, s);
+  return launch_one<MODE, DIV_MK1, DIV_MK1>(a, grid, s);
+}
+
+}  // namespace
+
+cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s) {
+  switch (mode) {
+    case MODE_RHS: return launch_mode<MODE_RHS>(a, grid, s);
+    case MODE_JVP: return launch_mode<MODE_JVP>(a, grid, s);
+    default: return launch_mode<MODE_LEJA>(a, grid, s);
+  }
 }
 
 }  // namespace xb

@@ -265,6 +265,8 @@ __global__ void __launch_bounds__(VT) leja_init_kernel(const double* __restrict_
     ctl->zero_dir = (ny == 0.0);
     ctl->eps = __ddiv_rn(__dmul_rn(SQRT_EPS, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
                          ny < 1e-300 ? 1e-300 : ny);
+    ctl->epsd = make_divisor_dev(ctl->eps);
+    if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
     ctl->m = 1;
     ctl->cur = 0;
     ctl->iters = 0;
