@@ -60,8 +60,8 @@ __device__ __forceinline__ RowSrc row_source(int r, const Geom& g, const double*
   s.fs = g.plane;
   int rr = r;
   if (g.bcy == BC_PERIODIC) {
-    rr = r % g.ny;
-    if (rr < 0) rr += g.ny;
+    // r lies in [-2, ny+2) and ny >= 2: one conditional wrap, no integer division
+    rr = r < 0 ? r + g.ny : (r >= g.ny ? r - g.ny : r);
   } else if (g.bcy == BC_REFLECT) {
     if (r < 0) { rr = -1 - r; s.flip = 1; }
     else if (r >= g.ny) { rr = 2 * g.ny - 1 - r; s.flip = 1; }
@@ -330,10 +330,17 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gyn[4], gy2[4]), g.h2y));
             F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gyn[5], gy2[5]), g.h2y));
           }
+          // non-finite detection (mhd.py:225-231): exponent field all ones
+          {
+            unsigned ex = 0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+              ex = max(ex, (unsigned)__double2hiint(F[f]) & 0x7ff00000u);
+            bad |= (ex == 0x7ff00000u);
+          }
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
             const long long i = obase + f * g.plane;
-            if (!isfinite(F[f])) bad = 1;
             if (MODE == MODE_RHS) {
               a.out[i] = F[f];
             } else if (MODE == MODE_JVP) {
