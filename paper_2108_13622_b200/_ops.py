@@ -52,7 +52,18 @@ def as_device(x, copy=False):
 
 
 def to_host(t):
-    return t.detach().cpu().numpy()
+    """D2H into page-locked memory (torch's caching host allocator) -> NumPy view.
+
+    The returned array keeps its pinned block alive; the block returns to the
+    pool when the array is released, so repeated calls do not re-pin memory.
+    """
+    t = t.detach()
+    if not t.is_cuda:
+        return t.numpy()
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return host.numpy()
 
 
 def like(result, template):

@@ -24,7 +24,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     # the bitwise contract: no FMA contraction in device or host code
     "-fmad=false",
-    "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
     "-shared",
     "-cudart", "static",
 ]

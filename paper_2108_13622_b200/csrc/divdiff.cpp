@@ -5,12 +5,35 @@
 // operation in the same order (compiled with -ffp-contract=off, no fast-math),
 // the substep count uses the same libm log2/ceil, and the bidiagonal matvec
 // computes out[i] = RN(RN(d[i]*w[i]) + RN(e*w[i-1])) exactly like
-// `out = diag*w; out[1:] += sub*w[:-1]`.
+// `out = diag*w; out[1:] += sub*w[:-1]`, then `/ k` and `new += term`.
+// The element loop is SIMD-vectorised (per-element IEEE ops, no reassociation);
+// target_clones picks AVX-512 / AVX2 / baseline at load time.
 #include <cmath>
 #include <cstring>
 #include <vector>
 
 #include "xmhd_b200.h"
+
+namespace {
+
+// One Taylor term of one substep: term <- (diag*term + sub*shift(term)) / k,
+// acc <- acc + term.  `prev` holds the previous term (read-only here).
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void taylor_term(int dim, const double* __restrict diag, double sub, double dk,
+                 const double* __restrict prev, double* __restrict next,
+                 double* __restrict acc) {
+  next[0] = (diag[0] * prev[0]) / dk;
+  acc[0] = acc[0] + next[0];
+  for (int i = 1; i < dim; ++i) {
+    const double a = diag[i] * prev[i];
+    const double b = sub * prev[i - 1];
+    const double t = (a + b) / dk;
+    next[i] = t;
+    acc[i] = acc[i] + t;
+  }
+}
+
+}  // namespace
 
 extern "C" int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double subdiag,
                                       double* out) {
@@ -38,23 +61,19 @@ extern "C" int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double 
   for (int i = 0; i < dim; ++i) diag[i] = ext[i] / p2;
   const double sub = subdiag / p2;
 
-  std::vector<double> col(dim, 0.0), term(dim), acc(dim), tmp(dim);
+  std::vector<double> col(dim, 0.0), t0(dim), t1(dim), acc(dim);
   col[0] = 1.0;
   const long long nsub = 1LL << s;
   for (long long it = 0; it < nsub; ++it) {
-    std::memcpy(term.data(), col.data(), sizeof(double) * dim);
+    std::memcpy(t0.data(), col.data(), sizeof(double) * dim);
     std::memcpy(acc.data(), col.data(), sizeof(double) * dim);
+    double* prev = t0.data();
+    double* next = t1.data();
     for (int k = 1; k < terms; ++k) {
-      const double dk = (double)k;
-      // term = matvec(term) / k
-      tmp[0] = (diag[0] * term[0]) / dk;
-      for (int i = 1; i < dim; ++i) {
-        const double a = diag[i] * term[i];
-        const double b = sub * term[i - 1];
-        tmp[i] = (a + b) / dk;
-      }
-      term.swap(tmp);
-      for (int i = 0; i < dim; ++i) acc[i] = acc[i] + term[i];
+      taylor_term(dim, diag.data(), sub, (double)k, prev, next, acc.data());
+      double* sw = prev;
+      prev = next;
+      next = sw;
     }
     col.swap(acc);
   }

@@ -16,6 +16,7 @@ a device kernel around the caller's matvec.
 """
 
 import ctypes
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -84,6 +85,31 @@ class PhiApplyResult:
     residual: float
 
 
+def _compute_coeffs(l, q, theta, count):
+    xi = leja_points(LEJA_MAX)[:count]
+    return _phi_divided_diffs(l, q + theta * xi, subdiag=theta) / theta ** l
+
+
+# Speculative chunk growth: while the device runs the Newton terms of the
+# current chunk, a host thread computes the next chunk (a pure function of
+# (l, q, theta, count), so the values are the ones an on-demand computation
+# would produce).  The cache below still follows the reference's policy.
+_spec_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="leja-coeffs")
+_spec = {}
+
+
+def _speculate(l, q, theta, count):
+    hit = _coeff_cache.get((l, q, theta))
+    if (hit is not None and hit.size >= count) or (l, q, theta, count) in _spec:
+        return
+    _spec[(l, q, theta, count)] = _spec_pool.submit(_compute_coeffs, l, q, theta, count)
+
+
+def _drop_speculation(l, q, theta):
+    for key in [k for k in _spec if k[:3] == (l, q, theta)]:
+        _spec.pop(key).cancel()
+
+
 def _newton_coeffs(l, q, theta, count):
     """Divided differences of xi -> phi_l(q + theta*xi) at the Leja points, / theta**l.
 
@@ -94,8 +120,13 @@ def _newton_coeffs(l, q, theta, count):
     hit = _coeff_cache.get(key)
     if hit is not None and hit.size >= count:
         return hit
-    xi = leja_points(LEJA_MAX)[:count]
-    coeffs = _phi_divided_diffs(l, q + theta * xi, subdiag=theta) / theta ** l
+    fut = _spec.pop((l, q, theta, count), None)
+    if fut is not None and (fut.running() or fut.done()):
+        coeffs = fut.result()
+    else:
+        if fut is not None:
+            fut.cancel()
+        coeffs = _compute_coeffs(l, q, theta, count)
     if len(_coeff_cache) > 64:
         _coeff_cache.pop(next(iter(_coeff_cache)))
     _coeff_cache[key] = coeffs
@@ -159,6 +190,7 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
     vd = _ops.as_device(v).reshape(-1)
     chunk = 64
     coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, chunk))
+    _speculate(l, q, theta, min(2 * chunk, LEJA_MAX))
     st = _lib.LejaState()
     h = mhd.ctx.bind_stream()
     rc = lib.xmhd_leja_start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
@@ -169,8 +201,10 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
     while st.status == _lib.LEJA_NEED_COEFFS:
         chunk, grown = _grow(l, q, theta, chunk, coeffs, st.m)
         coeffs = np.ascontiguousarray(grown)
+        _speculate(l, q, theta, min(2 * chunk, LEJA_MAX))
         rc = lib.xmhd_leja_resume(h, _ptr_d(coeffs), int(coeffs.size), ctypes.byref(st))
         _lib.check(rc, "xmhd_leja_resume")
+    _drop_speculation(l, q, theta)
     lin.rhs.calls += st.rhs_calls
     if st.status == _lib.LEJA_RHS_NONFINITE:
         # the reference raises from inside the matvec (mhd.py:225-231); rebuild
