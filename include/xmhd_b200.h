@@ -128,6 +128,34 @@ int xmhd_leja_generic_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef,
                              xmhd_leja_state* st);
 int xmhd_leja_generic_result(xmhd_ctx* ctx, double* p_out);
 
+/* ---- y-strip decomposition (bc_y == XMHD_BC_HALO) ----------------
+ * Each rank owns rows [y0, y0+ny) of every field.  Every norm is a cross-rank
+ * sum, so these entry points expose local partial sums and the control updates
+ * that run after the caller's allreduce; all ranks then take identical
+ * decisions.  Sequence per Leja term (stream-ordered, no host sync):
+ *   strip_pack -> halo exchange of y (caller, NCCL P2P) -> strip_iterate(sums)
+ *   -> allreduce(sums[0..2], SUM) (caller) -> strip_finalize(sums). */
+int xmhd_sumsq(xmhd_ctx* ctx, const double* x, long long n, double* out);
+/* jvp with the FD step eps given by the caller (from the global ||w||);
+ * *out_sumsq = local sum of squares of the result (may be NULL). */
+int xmhd_jvp_eps(xmhd_ctx* ctx, const double* u, const double* fu, const double* w, double eps,
+                 double* out, double* out_sumsq);
+/* y = v, p = c0*v; sums[0] (device) = local sum of v^2; then strip_start_finalize. */
+int xmhd_leja_strip_start(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                          const double* v, double dt, double q, double theta, double tol,
+                          const double* xi, const double* coeffs, int ncoef, double* sums);
+int xmhd_leja_strip_start_finalize(xmhd_ctx* ctx, const double* sums);
+/* Boundary rows of the current y into send buffers / mirrored ghost rows ([field][2][nx]). */
+int xmhd_leja_strip_pack(xmhd_ctx* ctx, double* send_lo, double* send_hi, double* halo_lo_dir,
+                         double* halo_hi_dir, int mirror_lo, int mirror_hi);
+/* One fused Newton term on the strip; sums[0..2] (device) = local [sum y'^2, sum p'^2, bad]. */
+int xmhd_leja_strip_iterate(xmhd_ctx* ctx, double* sums);
+/* Control update from the allreduced sums (no-op once the call has finished). */
+int xmhd_leja_strip_finalize(xmhd_ctx* ctx, const double* sums);
+int xmhd_leja_query(xmhd_ctx* ctx, xmhd_leja_state* st);
+/* Upload a grown coefficient chunk and clear NEED_COEFFS without running. */
+int xmhd_leja_set_coeffs(xmhd_ctx* ctx, const double* coeffs, int ncoef);
+
 /* Benchmark hook: average duration (CUDA events on the context stream) of
  * n_iter back-to-back fused Leja iteration kernels with the convergence test
  * disabled (tol = 0); coeffs500 holds 500 Newton coefficients. */

@@ -68,6 +68,15 @@ _SIGS = {
     "xmhd_leja_generic_step": (_I, [_P, _P, ctypes.POINTER(LejaState)]),
     "xmhd_leja_generic_resume": (_I, [_P, _PD, _I, ctypes.POINTER(LejaState)]),
     "xmhd_leja_generic_result": (_I, [_P, _P]),
+    "xmhd_sumsq": (_I, [_P, _P, _L, _PD]),
+    "xmhd_jvp_eps": (_I, [_P, _P, _P, _P, _D, _P, _PD]),
+    "xmhd_leja_strip_start": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I, _P]),
+    "xmhd_leja_strip_start_finalize": (_I, [_P, _P]),
+    "xmhd_leja_strip_pack": (_I, [_P, _P, _P, _P, _P, _I, _I]),
+    "xmhd_leja_strip_iterate": (_I, [_P, _P]),
+    "xmhd_leja_strip_finalize": (_I, [_P, _P]),
+    "xmhd_leja_query": (_I, [_P, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_set_coeffs": (_I, [_P, _PD, _I]),
     "xmhd_time_leja_iterations": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _PD, _PD, _I, _PD]),
     "xmhd_phi_divided_diffs": (_I, [_I, _PD, _I, _D, _PD]),
 }

@@ -6,6 +6,7 @@ reductions.
 """
 
 import ctypes
+import math
 import threading
 
 import numpy as np
@@ -18,14 +19,18 @@ _util_lock = threading.Lock()
 
 
 def util_ctx():
-    """A geometry-free context used for reductions on arbitrary vectors."""
-    dev = torch.cuda.current_device()
+    """A geometry-free context used for reductions on arbitrary vectors.
+
+    One per (device, host thread): its reduction scratch must not be shared by
+    concurrently enqueued work.
+    """
+    key = (torch.cuda.current_device(), threading.get_ident())
     with _util_lock:
-        c = _util.get(dev)
+        c = _util.get(key)
         if c is None:
             c = _lib.Context(2, 2, 1.0, 1.0, 0.0, 0.0, 0.0, 5.0 / 3.0, 1.0,
                              _lib.BC_PERIODIC, _lib.BC_PERIODIC)
-            _util[dev] = c
+            _util[key] = c
     return c
 
 
@@ -75,12 +80,49 @@ def _h(ctx):
     return (ctx or util_ctx()).bind_stream()
 
 
+# Cross-rank reducer of the y-strip decomposition (strips.Reducer); None = one
+# domain.  Host-thread local, so ranks emulated by threads stay independent.
+_tls = threading.local()
+
+
+def set_reducer(reducer):
+    """Install (or clear with None) the cross-rank reduction used by every norm."""
+    prev = getattr(_tls, "reducer", None)
+    _tls.reducer = reducer
+    return prev
+
+
+def reducer():
+    return getattr(_tls, "reducer", None)
+
+
+def sumsq(x, ctx=None):
+    """Local sum of squares of a device vector (deterministic)."""
+    lib = _lib.load()
+    out = ctypes.c_double()
+    _lib.check(lib.xmhd_sumsq(_h(ctx), _lib.ptr(x), x.numel(), ctypes.byref(out)), "xmhd_sumsq")
+    return float(out.value)
+
+
 def norm(x, ctx=None):
-    """np.linalg.norm(x) of a device vector."""
+    """np.linalg.norm(x) of a device vector (global over ranks on y-strips)."""
+    red = reducer()
+    if red is not None:
+        return math.sqrt(red.sum([sumsq(x, ctx)])[0])
     lib = _lib.load()
     out = ctypes.c_double()
     _lib.check(lib.xmhd_norm(_h(ctx), _lib.ptr(x), x.numel(), ctypes.byref(out)), "xmhd_norm")
     return float(out.value)
+
+
+def global_max(values):
+    red = reducer()
+    return red.max(list(values)) if red is not None else list(values)
+
+
+def global_sum(values):
+    red = reducer()
+    return red.sum(list(values)) if red is not None else list(values)
 
 
 def lincomb(coeffs, vecs, out=None, want_norm=False, ctx=None):
@@ -101,6 +143,10 @@ def lincomb(coeffs, vecs, out=None, want_norm=False, ctx=None):
         rc = lib.xmhd_lincomb(_h(ctx), _lib.ptr(out), n, arr, cs, len(vecs), ctypes.byref(nrm),
                               ctypes.byref(bad))
         _lib.check(rc, "xmhd_lincomb")
+        red = reducer()
+        if red is not None:
+            s, b = red.sum([nrm.value * nrm.value, float(bad.value)])
+            return out, math.sqrt(s), b > 0.0
         return out, float(nrm.value), bool(bad.value)
     rc = lib.xmhd_lincomb(_h(ctx), _lib.ptr(out), n, arr, cs, len(vecs), None, None)
     _lib.check(rc, "xmhd_lincomb")
@@ -124,7 +170,12 @@ def divide(x, d, out=None, want_norm=False, ctx=None):
 
 
 def diff_norms(a, b, ctx=None):
-    """(||a - b||, ||b||) of two device vectors."""
+    """(||a - b||, ||b||) of two device vectors (global over ranks on y-strips)."""
+    red = reducer()
+    if red is not None:
+        d = lincomb((1.0, -1.0), (a, b), ctx=ctx)
+        s_d, s_b = red.sum([sumsq(d, ctx), sumsq(b, ctx)])
+        return math.sqrt(s_d), math.sqrt(s_b)
     lib = _lib.load()
     out = (ctypes.c_double * 2)()
     rc = lib.xmhd_diff_norms(_h(ctx), _lib.ptr(a), _lib.ptr(b), a.numel(), out)

@@ -186,7 +186,8 @@ int upload_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
 }
 
 int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double dt, double q,
-               double theta, double tol, const double* xi, const double* coeffs, int ncoef) {
+               double theta, double tol, const double* xi, const double* coeffs, int ncoef,
+               double* ext_sums = nullptr) {
   int rc = ensure_ws(c, n);
   if (rc) return rc;
   rc = upload_coeffs(c, coeffs, ncoef);
@@ -205,9 +206,24 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   *c->ctl_h = h;
   CK(cudaMemcpyAsync(c->ctl, c->ctl_h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
-  CK(launch_leja_init(v, n, c->ybuf[0], c->pbuf[0], c->ctl, c->coeffs_d, redbuf(c), c->stream));
+  CK(launch_leja_init(v, n, c->ybuf[0], c->pbuf[0], c->ctl, c->coeffs_d, redbuf(c), c->stream,
+                      ext_sums));
   c->launches++;
   return XMHD_OK;
+}
+
+StencilArgs leja_args(xmhd_ctx* c) {
+  StencilArgs a = base_args(c);
+  a.u = c->leja_u;
+  a.fu = c->leja_fu;
+  a.ybuf[0] = c->ybuf[0];
+  a.ybuf[1] = c->ybuf[1];
+  a.pbuf[0] = c->pbuf[0];
+  a.pbuf[1] = c->pbuf[1];
+  a.coeffs = c->coeffs_d;
+  a.xi = c->xi_d;
+  a.ctl = c->ctl;
+  return a;
 }
 
 }  // namespace
@@ -576,6 +592,107 @@ int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, do
     return fail(XMHD_BADARG, "timing run left RUNNING early (status " +
                                  std::to_string(c->ctl_h->status) + ")");
   *ms_per_iter = (double)ms / n_iter;
+  return XMHD_OK;
+}
+
+// ---------------------------------------------------------------- y-strips
+// Every norm on a strip is a cross-rank sum: these entry points expose the
+// local partial sums (device or host) and the control updates that run after
+// the caller's allreduce, so all ranks take identical decisions.
+
+int xmhd_sumsq(xmhd_ctx* c, const double* x, long long n, double* out) {
+  if (!c || !x || !out) return fail(XMHD_BADARG, "null arg");
+  CK(launch_sumsq(x, n, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  *out = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+int xmhd_jvp_eps(xmhd_ctx* c, const double* u, const double* fu, const double* w, double eps,
+                 double* out, double* out_sumsq) {
+  if (!c || !u || !fu || !w || !out) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO && !(c->g.halo_lo && c->g.halo_lo_dir))
+    return fail(XMHD_BADARG, "halo rows (state and direction) not set");
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.dir = w;
+  a.fu = fu;
+  a.out = out;
+  a.eps = eps;
+  a.epsd = make_divisor(eps, c->force_ieee);
+  CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 2);
+  if (rc) return rc;
+  if (out_sumsq) *out_sumsq = c->h_dbl[1];
+  int bad = 0;
+  rc = fetch_bad(c, &bad);
+  if (rc) return rc;
+  return bad ? XMHD_NONFINITE : XMHD_OK;
+}
+
+int xmhd_leja_strip_start(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                          const double* v, double dt, double q, double theta, double tol,
+                          const double* xi, const double* coeffs, int ncoef, double* sums) {
+  if (!c || !u || !fu || !v || !xi || !coeffs || !sums) return fail(XMHD_BADARG, "null arg");
+  c->leja_u = u;
+  c->leja_fu = fu;
+  return leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef, sums);
+}
+
+int xmhd_leja_strip_start_finalize(xmhd_ctx* c, const double* sums) {
+  if (!c || !sums) return fail(XMHD_BADARG, "null arg");
+  CK(launch_leja_init_finalize(c->ctl, sums, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_strip_pack(xmhd_ctx* c, double* send_lo, double* send_hi, double* halo_lo_dir,
+                         double* halo_hi_dir, int mirror_lo, int mirror_hi) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  CK(launch_leja_pack_halo(c->ctl, c->ybuf[0], c->ybuf[1], c->g.nx, c->g.ny, send_lo, send_hi,
+                           halo_lo_dir, halo_hi_dir, mirror_lo, mirror_hi, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_strip_iterate(xmhd_ctx* c, double* sums) {
+  if (!c || !sums) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO && !(c->g.halo_lo && c->g.halo_lo_dir))
+    return fail(XMHD_BADARG, "halo rows (state and direction) not set");
+  StencilArgs a = leja_args(c);
+  a.ext_sums = sums;
+  CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_strip_finalize(xmhd_ctx* c, const double* sums) {
+  if (!c || !sums) return fail(XMHD_BADARG, "null arg");
+  CK(launch_leja_finalize(c->ctl, sums, c->coeffs_d, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_query(xmhd_ctx* c, xmhd_leja_state* st) {
+  if (!c || !st) return fail(XMHD_BADARG, "null arg");
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  fill_state(*c->ctl_h, st);
+  return XMHD_OK;
+}
+
+int xmhd_leja_set_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
+  if (!c || !coeffs) return fail(XMHD_BADARG, "null arg");
+  int rc = upload_coeffs(c, coeffs, ncoef);
+  if (rc) return rc;
+  c->ctl_h->ncoef = ncoef;
+  c->ctl_h->status = LJ_RUNNING;
+  CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   return XMHD_OK;
 }
 

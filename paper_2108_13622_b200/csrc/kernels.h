@@ -62,6 +62,7 @@ struct StencilArgs {
   unsigned* ticket;
   double* result;      // MODE_JVP: ||J w||
   int* bad;            // |= 1 when a non-finite F cell is produced
+  double* ext_sums;    // MODE_LEJA y-strips: [sum y'^2, sum p'^2, bad] of this rank
   int units_x, nunits, seg_rows;
 };
 
@@ -100,9 +101,22 @@ cudaError_t launch_field_sums(const double* u, long long plane, RedBuf rb, cudaS
 // result[0] = max over cells of |vx| + cf, result[1] of |vy| + cf (harness.py:105-116).
 cudaError_t launch_cfl(const double* u, long long plane, double gamma, double mu0,
                        RedBuf rb, cudaStream_t s);
-// Leja start: y0 = v, p0 = c0*v, ctl init (norm of v, blowup, eps).
+// Leja start: y0 = v, p0 = c0*v, ctl init (norm of v, blowup, eps).  With
+// ext_sums the local sum of squares goes there instead (y-strips: allreduce,
+// then launch_leja_init_finalize).
 cudaError_t launch_leja_init(const double* v, long long n, double* y0, double* p0,
-                             LejaCtl* ctl, const double* coeffs, RedBuf rb, cudaStream_t s);
+                             LejaCtl* ctl, const double* coeffs, RedBuf rb, cudaStream_t s,
+                             double* ext_sums = nullptr);
+cudaError_t launch_leja_init_finalize(LejaCtl* ctl, const double* sums, cudaStream_t s);
+// Control update from globally reduced [sum y'^2, sum p'^2, bad] (y-strips).
+cudaError_t launch_leja_finalize(LejaCtl* ctl, const double* sums, const double* coeffs,
+                                 cudaStream_t s);
+// Halo rows of the current y (send buffers and/or mirrored ghost rows).
+cudaError_t launch_leja_pack_halo(const LejaCtl* ctl, const double* y0, const double* y1, int nx,
+                                  int ny, double* send_lo, double* send_hi, double* halo_lo,
+                                  double* halo_hi, int mirror_lo, int mirror_hi, cudaStream_t s);
+// result[0] = sum of squares (no sqrt; y-strip partial norms).
+cudaError_t launch_sumsq(const double* x, long long n, RedBuf rb, cudaStream_t s);
 // Generic Leja update for an arbitrary (host-supplied) matvec result w.
 cudaError_t launch_leja_update(const double* w, long long n, LejaCtl* ctl, double* const* ybuf,
                                double* const* pbuf, const double* coeffs, const double* xi,
@@ -153,6 +167,27 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
                        ny < 1e-300 ? 1e-300 : ny);
   ctl->epsd = make_divisor_dev(ctl->eps);
   if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
+}
+
+// Control-block start from sum(v^2) (leja.py:121-123): y = v, p = c0*v done by the caller.
+__device__ __forceinline__ void leja_init_ctl(LejaCtl* ctl, double sumsq) {
+  const double kSqrtEps = 1.4901161193847656e-08;
+  const double ny = sqrt(sumsq);
+  ctl->ynorm = ny;
+  ctl->blowup = __dmul_rn(1e120, fmax(1.0, ny));
+  ctl->zero_dir = (ny == 0.0);
+  ctl->eps = __ddiv_rn(__dmul_rn(kSqrtEps, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
+                       ny < 1e-300 ? 1e-300 : ny);
+  ctl->epsd = make_divisor_dev(ctl->eps);
+  if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
+  ctl->m = 1;
+  ctl->cur = 0;
+  ctl->iters = 0;
+  ctl->rhs_calls = 0;
+  ctl->small_prev = 0;
+  ctl->fbad = 0;
+  ctl->residual = CUDART_INF;
+  ctl->status = (ctl->ncoef <= 1) ? LJ_NEED_COEFFS : LJ_RUNNING;
 }
 #endif
 

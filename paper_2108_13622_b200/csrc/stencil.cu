@@ -392,10 +392,17 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
     if (t == 0) {
       if (MODE == MODE_JVP) {
         a.result[0] = sqrt(sy);
+      } else if (a.ext_sums) {
+        // y-strips: publish this rank's partial sums; the control update runs
+        // after the cross-rank allreduce (leja_finalize_kernel)
+        a.ext_sums[0] = sy;
+        a.ext_sums[1] = sp;
+        a.ext_sums[2] = *((volatile int*)a.bad) ? 1.0 : 0.0;
       } else {
         const int flag = *((volatile int*)a.bad);
         leja_finalize(a.ctl, sy, sp, flag, !zero_dir, cm);
       }
+      if (MODE == MODE_JVP) a.result[1] = sy;   // local sum of squares (y-strips)
       *a.ticket = 0u;
     }
   }

@@ -14,7 +14,6 @@ namespace xb {
 namespace {
 
 constexpr int VT = 256;  // threads per block
-constexpr double SQRT_EPS = 1.4901161193847656e-08;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -247,7 +246,7 @@ __global__ void __launch_bounds__(VT) leja_init_kernel(const double* __restrict_
                                                        double* __restrict__ y0,
                                                        double* __restrict__ p0, LejaCtl* ctl,
                                                        const double* __restrict__ coeffs,
-                                                       RedBuf rb) {
+                                                       RedBuf rb, double* ext_sums) {
   const double c0 = coeffs[0];
   double acc[1] = {0.0};
   for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
@@ -259,23 +258,56 @@ __global__ void __launch_bounds__(VT) leja_init_kernel(const double* __restrict_
   }
   double tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) {
-    const double ny = sqrt(tot[0]);
-    ctl->ynorm = ny;
-    ctl->blowup = __dmul_rn(1e120, fmax(1.0, ny));
-    ctl->zero_dir = (ny == 0.0);
-    ctl->eps = __ddiv_rn(__dmul_rn(SQRT_EPS, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
-                         ny < 1e-300 ? 1e-300 : ny);
-    ctl->epsd = make_divisor_dev(ctl->eps);
-    if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
-    ctl->m = 1;
-    ctl->cur = 0;
-    ctl->iters = 0;
-    ctl->rhs_calls = 0;
-    ctl->small_prev = 0;
-    ctl->fbad = 0;
-    ctl->residual = CUDART_INF;
-    ctl->status = (ctl->ncoef <= 1) ? LJ_NEED_COEFFS : LJ_RUNNING;
+    if (ext_sums) ext_sums[0] = tot[0];   // y-strips: global sum first (allreduce)
+    else leja_init_ctl(ctl, tot[0]);
   }
+}
+
+// One-thread control kernels of the y-strip driver: run after the allreduce of
+// the per-rank partial sums, so every rank takes identical decisions.
+__global__ void leja_init_finalize_kernel(LejaCtl* ctl, const double* sums) {
+  leja_init_ctl(ctl, sums[0]);
+}
+
+__global__ void leja_finalize_kernel(LejaCtl* ctl, const double* sums,
+                                     const double* __restrict__ coeffs) {
+  if (ctl->status != LJ_RUNNING) return;
+  leja_finalize(ctl, sums[0], sums[1], sums[2] > 0.0, !ctl->zero_dir, coeffs[ctl->m]);
+}
+
+// Halo rows of the current Newton basis vector (y-strips): rows 0,1 go to the
+// rank below, rows ny-2, ny-1 to the rank above; a mirror edge builds its own
+// ghost rows (mhd.py:77-105: MY, BY odd).  Layout of every buffer: [field][2][nx].
+__global__ void leja_pack_halo_kernel(const LejaCtl* ctl, const double* y0, const double* y1,
+                                      int nx, int ny, double* send_lo, double* send_hi,
+                                      double* halo_lo, double* halo_hi, int mirror_lo,
+                                      int mirror_hi) {
+  const double* y = ctl->cur ? y1 : y0;
+  const long long plane = (long long)nx * ny;
+  const int total = NF * 2 * nx;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    const int f = k / (2 * nx), rr = (k / nx) % 2, i = k % nx;
+    const double lo = y[f * plane + (long long)rr * nx + i];               // row rr
+    const double hi = y[f * plane + (long long)(ny - 2 + rr) * nx + i];    // row ny-2+rr
+    if (send_lo) send_lo[k] = lo;
+    if (send_hi) send_hi[k] = hi;
+    const double s = (f == MY || f == BY) ? -1.0 : 1.0;
+    // ghost row -2 = s*row 1, -1 = s*row 0; ny = s*row ny-1, ny+1 = s*row ny-2
+    if (mirror_lo) halo_lo[k] = __dmul_rn(s, y[f * plane + (long long)(1 - rr) * nx + i]);
+    if (mirror_hi) halo_hi[k] = __dmul_rn(s, y[f * plane + (long long)(ny - 1 - rr) * nx + i]);
+  }
+}
+
+__global__ void __launch_bounds__(VT) sumsq_kernel(const double* __restrict__ x, long long n,
+                                                   RedBuf rb) {
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    const double v = __ldg(x + i);
+    acc[0] = __fma_rn(v, v, acc[0]);
+  }
+  double tot[1];
+  if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = tot[0];
 }
 
 // Newton-term update for an externally supplied w = matvec(y) (leja.py:133-148).
@@ -367,8 +399,34 @@ cudaError_t launch_cfl(const double* u, long long plane, double gamma, double mu
 }
 
 cudaError_t launch_leja_init(const double* v, long long n, double* y0, double* p0, LejaCtl* ctl,
-                             const double* coeffs, RedBuf rb, cudaStream_t s) {
-  leja_init_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(v, n, y0, p0, ctl, coeffs, rb);
+                             const double* coeffs, RedBuf rb, cudaStream_t s, double* ext_sums) {
+  leja_init_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(v, n, y0, p0, ctl, coeffs, rb, ext_sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leja_init_finalize(LejaCtl* ctl, const double* sums, cudaStream_t s) {
+  leja_init_finalize_kernel<<<1, 1, 0, s>>>(ctl, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leja_finalize(LejaCtl* ctl, const double* sums, const double* coeffs,
+                                 cudaStream_t s) {
+  leja_finalize_kernel<<<1, 1, 0, s>>>(ctl, sums, coeffs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leja_pack_halo(const LejaCtl* ctl, const double* y0, const double* y1, int nx,
+                                  int ny, double* send_lo, double* send_hi, double* halo_lo,
+                                  double* halo_hi, int mirror_lo, int mirror_hi, cudaStream_t s) {
+  const int total = NF * 2 * nx;
+  const int grid = (total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024;
+  leja_pack_halo_kernel<<<grid, 256, 0, s>>>(ctl, y0, y1, nx, ny, send_lo, send_hi, halo_lo,
+                                             halo_hi, mirror_lo, mirror_hi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sumsq(const double* x, long long n, RedBuf rb, cudaStream_t s) {
+  sumsq_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(x, n, rb);
   return cudaGetLastError();
 }
 

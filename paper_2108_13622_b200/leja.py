@@ -16,6 +16,7 @@ a device kernel around the caller's matvec.
 """
 
 import ctypes
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -31,6 +32,21 @@ _GRID_SIZE = 10001   # leja.py:18
 
 _sequence_cache = None
 _coeff_cache = {}
+_tls = threading.local()
+
+
+def _cache():
+    """The coefficient cache of this host thread (the main thread's is _coeff_cache).
+
+    One process per GPU uses only the main thread's cache; ranks emulated by
+    threads (tests) get independent caches like independent processes would.
+    """
+    if threading.current_thread() is threading.main_thread():
+        return _coeff_cache
+    c = getattr(_tls, "cache", None)
+    if c is None:
+        c = _tls.cache = {}
+    return c
 
 
 def _greedy_leja(count):
@@ -99,7 +115,7 @@ _spec = {}
 
 
 def _speculate(l, q, theta, count):
-    hit = _coeff_cache.get((l, q, theta))
+    hit = _cache().get((l, q, theta))
     if (hit is not None and hit.size >= count) or (l, q, theta, count) in _spec:
         return
     _spec[(l, q, theta, count)] = _spec_pool.submit(_compute_coeffs, l, q, theta, count)
@@ -117,7 +133,8 @@ def _newton_coeffs(l, q, theta, count):
     (leja.py:84-100); the heavy part runs in the native C++ port.
     """
     key = (l, q, theta)
-    hit = _coeff_cache.get(key)
+    cache = _cache()
+    hit = cache.get(key)
     if hit is not None and hit.size >= count:
         return hit
     fut = _spec.pop((l, q, theta, count), None)
@@ -127,9 +144,9 @@ def _newton_coeffs(l, q, theta, count):
         if fut is not None:
             fut.cancel()
         coeffs = _compute_coeffs(l, q, theta, count)
-    if len(_coeff_cache) > 64:
-        _coeff_cache.pop(next(iter(_coeff_cache)))
-    _coeff_cache[key] = coeffs
+    if len(cache) > 64:
+        cache.pop(next(iter(cache)))
+    cache[key] = coeffs
     return coeffs
 
 
@@ -178,6 +195,9 @@ def apply_phi_leja(l, matvec, v, dt, shift, tol):
         raise ValueError("tolerance must be positive")
     xi = np.ascontiguousarray(leja_points(LEJA_MAX))
     if isinstance(matvec, JacobianAction) and matvec.fused:
+        from paper_2108_13622_b200.strips import StripMhd, apply_phi_leja_strips
+        if isinstance(matvec.lin.mhd, StripMhd):
+            return apply_phi_leja_strips(l, matvec.lin, v, dt, shift, tol, xi)
         return _apply_fused(l, matvec.lin, v, dt, shift, tol, xi)
     return _apply_generic(l, matvec, v, dt, shift, tol, xi)
 

@@ -1,0 +1,420 @@
+"""y-strip domain decomposition of the hot path over ranks.
+
+Partitioning: contiguous y-strips — rank r owns rows [y0, y0+ny_r) of every
+field with the full x extent, so x-periodicity stays rank-local ("row bands",
+SPEC.md:486).  Per stencil evaluation a rank needs 2 ghost rows of the state
+from each y-neighbour (the ±2 footprint of mhd.py:143,222-223); the periodic
+wrap connects rank 0 and rank P-1, a reflecting wall makes the edge rank build
+its own mirrored ghost rows (mhd.py:77-105).
+
+Per Leja term (leja.py:133-148) the driver below enqueues, without any host
+synchronisation:
+
+    pack the boundary rows of the current y          (device kernel)
+    2-row halo exchange with both y-neighbours        (torch.distributed P2P: NCCL/NVLink)
+    fused FD-JVP + Newton term on the strip           (stencil kernel, BC_HALO rows)
+    allreduce of [sum y'^2, sum p'^2, non-finite]     (one 24-byte NCCL allreduce)
+    control update from the global sums               (1-thread kernel, identical on all ranks)
+
+and synchronises once per batch of terms.  u's halo rows are exchanged once per
+phi-call (u is frozen).  Every other norm of the host layer (FD step, error
+norm, power iteration, totals) becomes a cross-rank reduction through
+``_ops.set_reducer``.
+
+The orchestration (layout, neighbour order, halo ordering, reductions, the
+control flow of the Newton loop) is backend-agnostic: ``CudaStripBackend`` runs
+the sm_100a kernels; the CPU tests drive the same ``leja_strips`` loop with a
+NumPy oracle backend over the gloo transport (tests/test_strips_cpu.py).
+"""
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from paper_2108_13622_b200 import _lib
+from paper_2108_13622_b200 import _ops
+
+NF = 8
+MY, BY = 2, 5
+
+
+class StripLayout:
+    """Balanced contiguous row partition of ny rows over `size` ranks."""
+
+    def __init__(self, ny, size, rank):
+        if ny < 2 * size:
+            raise ValueError(f"{ny} rows cannot give every one of {size} ranks >= 2 rows")
+        base, rem = divmod(ny, size)
+        self.counts = [base + (1 if r < rem else 0) for r in range(size)]
+        self.starts = [sum(self.counts[:r]) for r in range(size)]
+        self.size, self.rank = size, rank
+        self.ny_global = ny
+        self.y0 = self.starts[rank]
+        self.ny = self.counts[rank]
+
+    def local_rows(self, global_fields):
+        """(8, ny_global, nx) -> this rank's (8, ny, nx) rows."""
+        return global_fields[:, self.y0:self.y0 + self.ny, :]
+
+
+class Comm:
+    """The transport of the decomposition: torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.size = dist.get_world_size(group)
+        else:
+            self.rank, self.size = 0, 1
+
+    def allreduce_sum(self, t):
+        if self.size > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def allreduce_max(self, t):
+        if self.size > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def neighbours(self, periodic):
+        below = self.rank - 1 if self.rank > 0 else (self.size - 1 if periodic else None)
+        above = self.rank + 1 if self.rank < self.size - 1 else (0 if periodic else None)
+        return below, above
+
+    def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
+        """Send my rows 0,1 down and rows ny-2,ny-1 up; receive the neighbours' rows.
+
+        Posting order is fixed (send up, send down, receive from below, receive
+        from above) so that with two ranks on a periodic ring the two messages
+        between the same pair are matched in order.
+        """
+        below, above = self.neighbours(periodic)
+        if self.size == 1:
+            if periodic:
+                recv_lo.copy_(send_hi)
+                recv_hi.copy_(send_lo)
+            return
+        ops = []
+        if above is not None:
+            ops.append(dist.P2POp(dist.isend, send_hi, above, self.group))
+        if below is not None:
+            ops.append(dist.P2POp(dist.isend, send_lo, below, self.group))
+        if below is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_lo, below, self.group))
+        if above is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_hi, above, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class Reducer:
+    """Cross-rank reductions for the host layer's norms (installed with _ops.set_reducer)."""
+
+    def __init__(self, comm, device):
+        self.comm = comm
+        self.device = device
+
+    def sum(self, values):
+        t = torch.tensor(values, dtype=torch.float64, device=self.device)
+        return self.comm.allreduce_sum(t).tolist()
+
+    def max(self, values):
+        t = torch.tensor(values, dtype=torch.float64, device=self.device)
+        return self.comm.allreduce_max(t).tolist()
+
+
+def mirror_rows(rows, lo_side):
+    """Ghost rows of a reflecting wall from the 2 boundary rows (MY, BY odd).
+
+    rows: (8, 2, nx) boundary rows in grid order.  Returns (8, 2, nx) ghost rows in
+    grid order: below the wall [-2, -1] = s*[row 1, row 0]; above it
+    [ny, ny+1] = s*[row ny-1, row ny-2].
+    """
+    ghost = rows.flip(1).clone()
+    ghost[MY] *= -1.0
+    ghost[BY] *= -1.0
+    return ghost
+
+
+def global_normal_slice(rng, layout, nx):
+    """This rank's slice of rng.standard_normal(8*ny*nx) in the global field-major order.
+
+    The reference draws the power-iteration start vector for the whole state
+    (linearize.py:113, harness.py:130); drawing the stream in row chunks
+    reproduces it exactly, and each rank keeps its own rows.
+    """
+    out = np.empty((NF, layout.ny, nx))
+    row_chunk = max(1, (1 << 22) // nx)
+    for f in range(NF):
+        r = 0
+        while r < layout.ny_global:
+            k = min(row_chunk, layout.ny_global - r)
+            lo, hi = max(r, layout.y0), min(r + k, layout.y0 + layout.ny)
+            if lo < hi:
+                draw = rng.standard_normal(k * nx).reshape(k, nx)
+                out[f, lo - layout.y0:hi - layout.y0] = draw[lo - r:hi - r]
+            else:
+                rng.standard_normal(k * nx)
+            r += k
+    return out.reshape(-1)
+
+
+class HaloSet:
+    """Send / receive row buffers of one vector, layout [field][2][nx]."""
+
+    def __init__(self, nx, device, dtype=torch.float64):
+        z = lambda: torch.empty((NF, 2, nx), dtype=dtype, device=device)
+        self.send_lo, self.send_hi, self.lo, self.hi = z(), z(), z(), z()
+
+    def exchange(self, vec3d, comm, periodic):
+        """Fill lo/hi with the neighbours' rows of vec3d (8, ny, nx) (or mirrored rows)."""
+        self.send_lo.copy_(vec3d[:, :2, :])
+        self.send_hi.copy_(vec3d[:, -2:, :])
+        below, above = comm.neighbours(periodic)
+        if below is None:
+            self.lo.copy_(mirror_rows(self.send_lo, True))
+        if above is None:
+            self.hi.copy_(mirror_rows(self.send_hi, False))
+        comm.exchange_rows(self.send_lo, self.send_hi, self.lo, self.hi, periodic)
+        return self.lo, self.hi
+
+
+class StripMhd:
+    """Device MHD right-hand side of one y-strip (the strip counterpart of MhdRhs)."""
+
+    def __init__(self, geometry, params, comm=None):
+        from paper_2108_13622_b200.mhd import Boundary
+        self.comm = comm or Comm()
+        self.layout = StripLayout(geometry.ny, self.comm.size, self.comm.rank)
+        self.nx, self.ny = geometry.nx, self.layout.ny
+        self.ny_global = geometry.ny
+        self.dx, self.dy = geometry.dx, geometry.dy
+        self.params = params
+        self.n = NF * self.nx * self.ny
+        self.periodic_y = params.bc_y is Boundary.PERIODIC
+        bcx = _lib.BC_PERIODIC if params.bc_x is Boundary.PERIODIC else _lib.BC_REFLECTING
+        self.ctx = _lib.Context(self.nx, self.ny, self.dx, self.dy, params.mu, params.eta,
+                                params.kappa, params.gamma, params.mu0, bcx, _lib.BC_HALO)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.state_halo = HaloSet(self.nx, dev)
+        self.dir_halo = HaloSet(self.nx, dev)
+
+    def _set_halo(self, u_halo, d_halo=None):
+        lib = _lib.load()
+        rc = lib.xmhd_set_halo(self.ctx.h, _lib.ptr(u_halo.lo), _lib.ptr(u_halo.hi),
+                               _lib.ptr(d_halo.lo) if d_halo else None,
+                               _lib.ptr(d_halo.hi) if d_halo else None)
+        _lib.check(rc, "xmhd_set_halo")
+
+    def exchange(self, flat, halo):
+        return halo.exchange(flat.reshape(NF, self.ny, self.nx), self.comm, self.periodic_y)
+
+    def __call__(self, flat, out=None):
+        from paper_2108_13622_b200.mhd import _blowup
+        u = _ops.as_device(flat).reshape(-1)
+        if u.numel() != self.n:
+            raise ValueError(f"strip state has {u.numel()} entries, needs {self.n}")
+        out = torch.empty_like(u) if out is None else out
+        self.exchange(u, self.state_halo)
+        self._set_halo(self.state_halo)
+        rc = _lib.load().xmhd_rhs(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(out))
+        _lib.check(rc, "xmhd_rhs (strip)")
+        if rc == _lib.NONFINITE:
+            err = _blowup(out, self.nx, self.ny)
+            err.cells = [(f, i, j + self.layout.y0) for f, i, j in (err.cells or [])]
+            raise err
+        return out
+
+    # -- per-step diagnostics over all strips (harness.py:105-116, 137-138, 209-211, 243)
+    def divb_max(self, u):
+        self.exchange(u, self.state_halo)
+        self._set_halo(self.state_halo)
+        out = ctypes.c_double()
+        _lib.check(_lib.load().xmhd_divb(self.ctx.bind_stream(), _lib.ptr(u), None,
+                                         ctypes.byref(out)), "xmhd_divb (strip)")
+        return _ops.global_max([out.value])[0]
+
+    def field_sums(self, u):
+        out = (ctypes.c_double * 8)()
+        _lib.check(_lib.load().xmhd_field_sums(self.ctx.bind_stream(), _lib.ptr(u), out),
+                   "xmhd_field_sums (strip)")
+        return _ops.global_sum(list(out))
+
+    def cfl_speeds(self, u):
+        out = (ctypes.c_double * 2)()
+        _lib.check(_lib.load().xmhd_cfl_speeds(self.ctx.bind_stream(), _lib.ptr(u), out),
+                   "xmhd_cfl_speeds (strip)")
+        return _ops.global_max(list(out))
+
+    def jvp(self, u, fu, w, eps):
+        """(F(u + eps*w) - F(u))/eps on the strip with the caller's (global) eps."""
+        self.exchange(u, self.state_halo)
+        self.exchange(w, self.dir_halo)
+        self._set_halo(self.state_halo, self.dir_halo)
+        out = torch.empty_like(w)
+        rc = _lib.load().xmhd_jvp_eps(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(fu),
+                                      _lib.ptr(w), float(eps), _lib.ptr(out), None)
+        _lib.check(rc, "xmhd_jvp_eps")
+        return out, rc == _lib.NONFINITE
+
+
+class CudaStripBackend:
+    """The per-term device operations of the strip Leja loop (C-ABI calls)."""
+
+    def __init__(self, mhd, lin):
+        self.mhd = mhd
+        self.lin = lin
+        self.lib = _lib.load()
+        self.h = mhd.ctx.bind_stream()
+        dev = lin.base_state.device
+        self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+
+    def start(self, v, dt, q, theta, tol, xi, coeffs):
+        mhd = self.mhd
+        mhd.exchange(self.lin.base_state, mhd.state_halo)
+        mhd._set_halo(mhd.state_halo, mhd.dir_halo)
+        rc = self.lib.xmhd_leja_strip_start(
+            self.h, _lib.ptr(self.lin.base_state), _lib.ptr(self.lin.base_rhs),
+            float(self.lin._base_norm), _lib.ptr(v), float(dt), float(q), float(theta),
+            float(tol), _ptr_d(xi), _ptr_d(coeffs), int(coeffs.size), _lib.ptr(self.sums))
+        _lib.check(rc, "xmhd_leja_strip_start")
+        return self.sums[:1]
+
+    def start_finalize(self, sums):
+        _lib.check(self.lib.xmhd_leja_strip_start_finalize(self.h, _lib.ptr(self.sums)),
+                   "xmhd_leja_strip_start_finalize")
+
+    def pack(self, mirror_lo, mirror_hi):
+        hs = self.mhd.dir_halo
+        rc = self.lib.xmhd_leja_strip_pack(self.h, _lib.ptr(hs.send_lo), _lib.ptr(hs.send_hi),
+                                           _lib.ptr(hs.lo), _lib.ptr(hs.hi), int(mirror_lo),
+                                           int(mirror_hi))
+        _lib.check(rc, "xmhd_leja_strip_pack")
+        return hs
+
+    def iterate(self):
+        _lib.check(self.lib.xmhd_leja_strip_iterate(self.h, _lib.ptr(self.sums)),
+                   "xmhd_leja_strip_iterate")
+        return self.sums
+
+    def finalize(self, sums):
+        _lib.check(self.lib.xmhd_leja_strip_finalize(self.h, _lib.ptr(self.sums)),
+                   "xmhd_leja_strip_finalize")
+
+    def state(self):
+        st = _lib.LejaState()
+        _lib.check(self.lib.xmhd_leja_query(self.h, ctypes.byref(st)), "xmhd_leja_query")
+        return st
+
+    def set_coeffs(self, coeffs):
+        _lib.check(self.lib.xmhd_leja_set_coeffs(self.h, _ptr_d(coeffs), int(coeffs.size)),
+                   "xmhd_leja_set_coeffs")
+
+    def result(self, like):
+        p = torch.empty_like(like)
+        _lib.check(self.lib.xmhd_leja_result(self.h, _lib.ptr(p)), "xmhd_leja_result")
+        return p
+
+    def current_y(self, like):
+        y = torch.empty_like(like)
+        _lib.check(self.lib.xmhd_leja_current_y(self.h, _lib.ptr(y)), "xmhd_leja_current_y")
+        return y
+
+
+def _ptr_d(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def leja_strips(backend, comm, periodic, l, v, dt, q, theta, tol, xi, coeff_fn, grow_fn,
+                batch0=2, batch_max=32):
+    """The Newton/Leja loop of leja.py:103-150 on y-strips (backend-agnostic).
+
+    coeff_fn(chunk) -> the initial coefficient array; grow_fn(chunk, coeffs, m)
+    -> (chunk, coeffs) on NEED_COEFFS (leja.py:128-130).  Returns the backend's
+    final state.  All ranks run the same sequence of collectives.
+    """
+    below, above = comm.neighbours(periodic)
+    chunk = 64
+    coeffs = coeff_fn(chunk)
+    part = backend.start(v, dt, q, theta, tol, xi, coeffs)
+    comm.allreduce_sum(part)
+    backend.start_finalize(part)
+    batch = batch0
+    while True:
+        for _ in range(batch):
+            hs = backend.pack(below is None, above is None)
+            comm.exchange_rows(hs.send_lo, hs.send_hi, hs.lo, hs.hi, periodic)
+            sums = backend.iterate()
+            comm.allreduce_sum(sums)
+            backend.finalize(sums)
+        st = backend.state()
+        if st.status == _lib.LEJA_NEED_COEFFS:
+            chunk, coeffs = grow_fn(chunk, coeffs, st.m)
+            backend.set_coeffs(coeffs)
+            batch = batch0
+            continue
+        if st.status != _lib.LEJA_RUNNING:
+            return st
+        batch = min(2 * batch, batch_max)
+
+
+def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
+    """apply_phi_leja for a linearization whose RHS is a StripMhd (called by leja.py)."""
+    from paper_2108_13622_b200 import leja
+    from paper_2108_13622_b200.linearize import RhsBlowupError
+    mhd = lin.mhd
+    q, theta = shift.q, shift.theta
+    vd = _ops.as_device(v).reshape(-1)
+    backend = CudaStripBackend(mhd, lin)
+
+    def coeff_fn(chunk):
+        c = np.ascontiguousarray(leja._newton_coeffs(l, q, theta, chunk))
+        leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
+        return c
+
+    def grow_fn(chunk, coeffs, m):
+        chunk, grown = leja._grow(l, q, theta, chunk, coeffs, m)
+        leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
+        return chunk, np.ascontiguousarray(grown)
+
+    st = leja_strips(backend, mhd.comm, mhd.periodic_y, l, vd, dt, q, theta, tol, xi,
+                     coeff_fn, grow_fn)
+    leja._drop_speculation(l, q, theta)
+    lin.rhs.calls += st.rhs_calls
+    if st.status == _lib.LEJA_RHS_NONFINITE:
+        y = backend.current_y(vd)
+        x = _ops.lincomb((1.0, st.eps), (lin.base_state, y))
+        try:
+            mhd(x)
+        except RhsBlowupError as err:
+            raise err
+        raise RhsBlowupError("non-finite rhs inside the fused Leja iteration (another strip)")
+    p = backend.result(vd)
+    return leja.PhiApplyResult(vector=_ops.like(p, v), iterations=int(st.iterations),
+                               converged=st.status == _lib.LEJA_CONVERGED,
+                               residual=float(st.residual))
+
+
+def gather_strips(local_flat, layout, nx, comm, root=0):
+    """Full (8, ny, nx) host array on `root` (None elsewhere) from every rank's strip."""
+    host = np.asarray(_ops.to_host(local_flat) if torch.is_tensor(local_flat) else local_flat)
+    host = host.reshape(NF, layout.ny, nx)
+    if comm.size == 1:
+        return host.copy()
+    objs = [None] * comm.size
+    dist.all_gather_object(objs, host, group=comm.group)
+    if comm.rank != root:
+        return None
+    return np.concatenate(objs, axis=1)
+
+
+def strip_norm_check(x_local, comm):
+    """||x|| of a distributed vector (diagnostics helper)."""
+    s = _ops.sumsq(x_local)
+    return math.sqrt(comm.allreduce_sum(torch.tensor([s], dtype=torch.float64,
+                                                     device=x_local.device)).item())
