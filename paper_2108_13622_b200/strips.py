@@ -86,6 +86,14 @@ class Comm:
         above = self.rank + 1 if self.rank < self.size - 1 else (0 if periodic else None)
         return below, above
 
+    def gather_host(self, obj):
+        """Every rank's host object, in rank order (final-state assembly only)."""
+        if self.size == 1:
+            return [obj]
+        objs = [None] * self.size
+        dist.all_gather_object(objs, obj, group=self.group)
+        return objs
+
     def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
         """Send my rows 0,1 down and rows ny-2,ny-1 up; receive the neighbours' rows.
 
@@ -406,8 +414,7 @@ def gather_strips(local_flat, layout, nx, comm, root=0):
     host = host.reshape(NF, layout.ny, nx)
     if comm.size == 1:
         return host.copy()
-    objs = [None] * comm.size
-    dist.all_gather_object(objs, host, group=comm.group)
+    objs = comm.gather_host(host)
     if comm.rank != root:
         return None
     return np.concatenate(objs, axis=1)

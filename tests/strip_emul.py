@@ -54,6 +54,14 @@ class ThreadComm:
         t.copy_(tot)
         return t
 
+    def gather_host(self, obj):
+        self.sh.barrier.wait()
+        self.sh.slots[self.rank] = obj
+        self.sh.barrier.wait()
+        objs = list(self.sh.slots)
+        self.sh.barrier.wait()
+        return objs
+
     def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
         torch.cuda.current_stream().synchronize()
         self.sh.slots[self.rank] = (send_lo.clone(), send_hi.clone())
