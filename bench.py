@@ -15,8 +15,10 @@ coefficient cache cleared per step so the host coefficient work is included.
           bounded sample of the same workload on this host.
 
 ``--impl reference`` times that CPU implementation alone (rank 0; other ranks
-exit 0).  N>1 under torchrun: one process per GPU; each rank runs the full
-workload (replicas, "scaling": "weak") until the y-strip path is benchmarked.
+exit 0).  N>1 under torchrun: one process per GPU, the 2048^2 grid split into
+y-strips (2-row NCCL halo exchange + one 3-scalar allreduce per Leja term,
+paper_2108_13622_b200/strips.py); the total work is fixed ("scaling": "strong")
+and `value` is whole-job cell-updates/s over the max-over-ranks device time.
 """
 
 import argparse
@@ -191,12 +193,12 @@ def reference_arm(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def total_launches():
+def total_launches(op=None):
     from paper_2108_13622_b200 import _ops, mhd
-    n = 0
-    for c in list(mhd._ctx_cache.values()) + list(_ops._util.values()):
-        n += c.launches()
-    return n
+    ctxs = list(mhd._ctx_cache.values()) + list(_ops._util.values())
+    if op is not None and op.ctx not in ctxs:
+        ctxs.append(op.ctx)
+    return sum(c.launches() for c in ctxs)
 
 
 def main():
@@ -218,12 +220,25 @@ def main():
     s.nx = s.ny = args.n
     q = sc.initial_fields(s)
     n_cells = s.nx * s.ny
-    v_host = sc.unit_gaussian(q.size, s.extra["v_seed"])
+    v_host = sc.unit_gaussian(q.size, s.extra["v_seed"]).reshape(q.shape)
     params = xb.MHDParams(mu=s.mu, eta=s.eta, kappa=s.kappa)
-    u_dev = torch.from_numpy(q).cuda().reshape(-1)
-    v_dev = torch.from_numpy(v_host).cuda()
-    st = xb.StateGrid(s.nx, s.ny, s.dx, s.dy, u_dev.reshape(8, s.ny, s.nx))
-    mhd = xb.MhdRhs(st, params)
+    if world > 1:
+        # y-strips: rank r owns rows [y0, y0+ny_r) of the 2048^2 problem (strong scaling)
+        from paper_2108_13622_b200 import strips
+        comm = strips.Comm()
+        mhd = strips.StripMhd(xb.StateGrid(s.nx, s.ny, s.dx, s.dy, None), params, comm)
+        _ops_mod = xb.linearize._ops
+        _ops_mod.set_reducer(strips.Reducer(comm, torch.device("cuda", local)))
+        q_loc = np.ascontiguousarray(mhd.layout.local_rows(q))
+        v_loc = np.ascontiguousarray(mhd.layout.local_rows(v_host))
+    else:
+        mhd = None
+        q_loc, v_loc = q, v_host
+    u_dev = torch.from_numpy(q_loc).cuda().reshape(-1)
+    v_dev = torch.from_numpy(v_loc).cuda().reshape(-1)
+    if mhd is None:
+        st = xb.StateGrid(s.nx, s.ny, s.dx, s.dy, u_dev.reshape(8, s.ny, s.nx))
+        mhd = xb.MhdRhs(st, params)
     op = xb.RhsOperator(mhd)
     lin = xb.FrozenLinearization(op, u_dev)
     est = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0))
@@ -259,7 +274,7 @@ def main():
     stream = torch.cuda.current_stream()
     iters_total = 0
     degrees = None
-    launches0 = total_launches()
+    launches0 = total_launches(mhd)
     with ClockSampler(local) as clocks:
         barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -272,18 +287,20 @@ def main():
             degrees = [r.iterations for r in outs]
         ev1.record(stream)
         barrier()
-    launches = total_launches() - launches0
+    launches = total_launches(mhd) - launches0
     ms = maxed(ev0.elapsed_time(ev1))
-    value = world * iters_total * n_cells / (ms * 1e-3)
+    # every rank processes its strip of the same iterations: whole-job cell-updates
+    value = iters_total * n_cells / (ms * 1e-3)
 
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
     kern_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
-    achieved = BYTES_PER_CELL_ITER * n_cells / (kern_ms * 1e-3) / 1e9
+    local_cells = u_dev.numel() // 8
+    achieved = BYTES_PER_CELL_ITER * local_cells / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
 
     # ---- end to end through the public API with pinned host buffers
-    u_pin = torch.from_numpy(q.reshape(-1)).pin_memory()
-    v_pin = torch.from_numpy(v_host).pin_memory()
+    u_pin = torch.from_numpy(q_loc.reshape(-1)).pin_memory()
+    v_pin = torch.from_numpy(v_loc.reshape(-1)).pin_memory()
     e2e_iters = 0
     barrier()
     t0 = time.perf_counter()
@@ -303,13 +320,13 @@ def main():
     e1.record(stream)
     barrier()
     e2e_ms = maxed(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)))
-    vec_bytes = 8 * q.size
-    e2e = {"value": world * e2e_iters * n_cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
+    vec_bytes = 8 * q.size   # whole job: every rank moves its strip
+    e2e = {"value": e2e_iters * n_cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
            "h2d_bytes_per_step": vec_bytes * (1 + len(SWEEP)),
            "d2h_bytes_per_step": vec_bytes * len(SWEEP)}
 
     exprb = None
-    if not args.no_exprb and rank == 0:
+    if not args.no_exprb and rank == 0 and world == 1:
         exprb = exprb_step_time(xb)
 
     cpu = None
@@ -321,14 +338,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes "
                     "per field; v seeded unit Gaussian)",
             "config": {"workload": f"config1: phi_1(dt J)v at {args.n}^2, alpha*dt sweep "
                                    f"{list(SWEEP)}, Leja tol {LEJA_TOL:g}",
                        "grid": args.n, "alpha": alpha, "leja_degrees": degrees,
                        "l2_policy": "inputs larger than L2 (268 MB per vector)",
-                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "parallelism": f"y-strips x{world} (NCCL halo + allreduce)"
+                                      if world > 1 else "single-gpu",
                        "stencil_plan": plan},
             "gbs_algorithmic": value * BYTES_PER_CELL_ITER / 1e9,
             "jv_per_s": value / n_cells,
