@@ -203,8 +203,10 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
       // prefetch registers: state (and direction) of the next row to consume
       double nu[NF], nd[NF];
+      int nflip;   // mirror flag of the prefetched row
       {
         const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc);
+        nflip = rs.flip;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           nu[f] = __ldg(rs.u + f * rs.fs + cs);
@@ -241,11 +243,11 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 #pragma unroll
           for (int f = 0; f < NF; ++f)
             x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
-          const RowSrc rcur = row_source(r, g, a.u, dsrc);
           if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-          if (rcur.flip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+          if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
           if (s + 1 < nsteps) {
             const RowSrc rs = row_source(r + 1, g, a.u, dsrc);
+            nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
               nu[f] = __ldg(rs.u + f * rs.fs + cs);
@@ -344,14 +346,16 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             if (MODE == MODE_RHS) {
               a.out[i] = F[f];
             } else if (MODE == MODE_JVP) {
-              const double jv = rdiv(__dsub_rn(F[f], efu[f]), epsd);
+              const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
               a.out[i] = jv;
               acc0 = __fma_rn(jv, jv, acc0);
             } else {
-              const double w = rdiv(__dsub_rn(F[f], efu[f]), epsd);
+              // per-launch divisors (eps, theta): the general two-correction path,
+              // branch-free (exact for every divisor)
+              const double w = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
               const double y = ey[f];
               const double yn = __dsub_rn(
-                  rdiv(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
+                  qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                   __dmul_rn(xim, y));
               const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
               yout[i] = yn;
