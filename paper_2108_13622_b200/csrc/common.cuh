@@ -131,9 +131,14 @@ struct Prim {
 
 __device__ __forceinline__ void primitives(const double x[NF], const Geom& g, Prim& p) {
   p.rho = x[RHO];
-  p.vx = __ddiv_rn(x[MX], p.rho);
-  p.vy = __ddiv_rn(x[MY], p.rho);
-  p.vz = __ddiv_rn(x[MZ], p.rho);
+  // the four divisions by the density share one correctly rounded reciprocal;
+  // each quotient is then exact by the two-correction Markstein sequence
+  Divisor rd;
+  rd.d = p.rho;
+  rd.r = __drcp_rn(p.rho);
+  p.vx = qdiv<DIV_MK2>(x[MX], rd);
+  p.vy = qdiv<DIV_MK2>(x[MY], rd);
+  p.vz = qdiv<DIV_MK2>(x[MZ], rd);
   p.bx = x[BX];
   p.by = x[BY];
   p.bz = x[BZ];
@@ -156,7 +161,7 @@ __device__ __forceinline__ void primitives(const double x[NF], const Geom& g, Pr
   // emf_z = vy*bx - by*vx
   p.emf = __dsub_rn(__dmul_rn(p.vy, p.bx), __dmul_rn(p.by, p.vx));
   // temp = pres/rho  (mhd.py:198)
-  p.temp = __ddiv_rn(p.pres, p.rho);
+  p.temp = qdiv<DIV_MK2>(p.pres, rd);
 }
 
 // Non-zero ideal x-flux rows, mhd.py:161-175.  Slot order:
