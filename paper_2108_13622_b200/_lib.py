@@ -88,7 +88,8 @@ _lock = threading.Lock()
 
 
 def library_path():
-    return _build.SO_PATH
+    """The in-tree library; XMHD_SO points at an alternative build (A/B benchmarks)."""
+    return os.environ.get("XMHD_SO") or _build.SO_PATH
 
 
 def load(build_if_missing=True):
@@ -98,7 +99,7 @@ def load(build_if_missing=True):
         if _lib is not None:
             return _lib
         path = library_path()
-        if build_if_missing:
+        if build_if_missing and not os.environ.get("XMHD_SO"):
             try:
                 _build.build_so()
             except (OSError, RuntimeError) as exc:

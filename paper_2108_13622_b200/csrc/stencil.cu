@@ -197,10 +197,9 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       const int tl = max(t - 1, 0), tr = min(t + 1, SW - 1);
       const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
 
-      // own-column diffusive y-fluxes of rows r-2, r-3, r-4 (registers)
-      double gy1[NG], gy2[NG], gy3[NG];
+      double gy1[NG], gy2[NG];
 #pragma unroll
-      for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = gy3[k] = 0.0;
+      for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
 
       // prefetch registers: state (and direction) of the next row to consume
       double nu[NF], nd[NF];
@@ -215,21 +214,16 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         }
       }
 
-      // Row step s handles new input row r = Y0-2+s.  Phase A runs the output
-      // row r-3 (P3) and the primitives of row r (P1) back to back: the two are
-      // independent, so their dependency chains interleave in one basic block.
-      // Phase B computes the diffusive fluxes of row r-1 (P2).
-      const int nsteps = (Y1 - Y0) + 5;
+      const int nsteps = (Y1 - Y0) + 4;
       int s3 = 0, s4 = 0;  // s % 3, s % 4
       for (int s = 0; s < nsteps; ++s) {
         const int r = Y0 - 2 + s;
         const int m1 = (s3 == 0) ? 2 : s3 - 1;  // PD slot of row r-1
         const int m2 = (s3 == 2) ? 0 : s3 + 1;  // PD slot of row r-2
-        const bool out_row = (s >= 5) && col_ok;
-        const bool in_row = (r <= Y1 + 1);
-        const long long obase = (long long)(r - 3) * g.nx + c_out;
+        const bool out_row = (s >= 4) && col_ok;
+        const long long obase = (long long)(r - 2) * g.nx + c_out;
 
-        // epilogue operands of output row r-3, issued ahead of the P1 work
+        // epilogue operands of output row r-2: issue now, consume in P3
         double efu[NF], ey[NF], ep[NF];
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
@@ -243,22 +237,80 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           }
         }
 
-        // ---- P3: output row o = r-3
+        // ---- P1: state at (r, cg) from the prefetch registers
+        {
+          double x[NF];
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
+          if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
+          if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+          if (s + 1 < nsteps) {
+            const RowSrc rs = row_source(r + 1, g, a.u, dsrc);
+            nflip = rs.flip;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              nu[f] = __ldg(rs.u + f * rs.fs + cs);
+              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
+            }
+          }
+          Prim p;
+          primitives(x, g, p);
+          pd[s3][PD_VX][t] = p.vx;
+          pd[s3][PD_VY][t] = p.vy;
+          pd[s3][PD_VZ][t] = p.vz;
+          pd[s3][PD_BX][t] = p.bx;
+          pd[s3][PD_BY][t] = p.by;
+          pd[s3][PD_BZ][t] = p.bz;
+          pd[s3][PD_T][t] = p.temp;
+          pd[s3][PD_B2][t] = p.b2;
+          double fv[NFX];
+          flux_x(p, g, fv);
+#pragma unroll
+          for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
+          flux_y(p, g, fv);
+#pragma unroll
+          for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
+        }
+        __syncthreads();
+
+        // ---- P2: diffusive fluxes at row r-1
+        double gyn[NG];
+#pragma unroll
+        for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
+        if (g.diffusive && s >= 2) {
+          double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
+#pragma unroll
+          for (int k = 0; k < NPD; ++k) {
+            xl[k] = pd[m1][k][tl];
+            xr[k] = pd[m1][k][tr];
+            yd[k] = pd[m2][k][t];
+            yu[k] = pd[s3][k][t];
+            own[k] = pd[m1][k][t];
+          }
+          double gxv[NG];
+          diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyn);
+#pragma unroll
+          for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
+        }
+        __syncthreads();
+
+        // ---- P3: output row o = r-2
         if (out_row) {
-          const int fx3 = (s4 + 1) & 3;   // FX slot of row r-3
-          const int fy2 = (s4 + 2) & 3;   // FY slot of row r-2
-          const int fy4 = s4;             // FY slot of row r-4 (read before P1 reuses it)
-          const int gs = (s + 1) & 1;     // GX slot of row r-3
+          const int fx2 = (s4 + 2) & 3;   // FX / FY slot of row r-2 (s-2 mod 4)
+          const int fy1 = (s4 + 3) & 3;   // FY slot of row r-1
+          const int fy3 = (s4 + 1) & 3;   // FY slot of row r-3
+          const int gs = s & 1;           // GX slot of row r-2
           double F[NF];
           // ideal part: out = -(dFX/2dx); out -= dFY/2dy       (mhd.py:177-178)
 #pragma unroll
           for (int k = 0; k < NFX; ++k)
-            F[fx_field(k)] = -qdiv<KX>(__dsub_rn(fxs[fx3][k][tr], fxs[fx3][k][tl]), g.h2x);
+            F[fx_field(k)] = -qdiv<KX>(__dsub_rn(fxs[fx2][k][tr], fxs[fx2][k][tl]), g.h2x);
           F[BX] = -0.0;
 #pragma unroll
           for (int k = 0; k < NFY; ++k) {
             const int f = fy_field(k);
-            F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(fys[fy2][k][t], fys[fy4][k][t]), g.h2y));
+            F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(fys[fy1][k][t], fys[fy3][k][t]), g.h2y));
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
           if (g.diffusive) {
@@ -273,12 +325,12 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gxs[gs][5][tr], gxs[gs][5][tl]), g.h2x));
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BY] = __dadd_rn(F[BY], 0.0);
-            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gy1[0], gy3[0]), g.h2y));
-            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gy1[1], gy3[1]), g.h2y));
-            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gy1[2], gy3[2]), g.h2y));
-            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gy1[3], gy3[3]), g.h2y));
-            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gy1[4], gy3[4]), g.h2y));
-            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gy1[5], gy3[5]), g.h2y));
+            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gyn[0], gy2[0]), g.h2y));
+            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gyn[1], gy2[1]), g.h2y));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gyn[2], gy2[2]), g.h2y));
+            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gyn[3], gy2[3]), g.h2y));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gyn[4], gy2[4]), g.h2y));
+            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gyn[5], gy2[5]), g.h2y));
           }
           // non-finite detection (mhd.py:225-231): exponent field all ones
           {
@@ -314,66 +366,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           }
         }
 
-        // ---- P1: state at (r, cg) from the prefetch registers
-        if (in_row) {
-          double x[NF];
 #pragma unroll
-          for (int f = 0; f < NF; ++f)
-            x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
-          if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-          if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
-          if (r + 1 <= Y1 + 1) {
-            const RowSrc rs = row_source(r + 1, g, a.u, dsrc);
-            nflip = rs.flip;
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              nu[f] = __ldg(rs.u + f * rs.fs + cs);
-              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
-            }
-          }
-          Prim p;
-          primitives(x, g, p);
-          pd[s3][PD_VX][t] = p.vx;
-          pd[s3][PD_VY][t] = p.vy;
-          pd[s3][PD_VZ][t] = p.vz;
-          pd[s3][PD_BX][t] = p.bx;
-          pd[s3][PD_BY][t] = p.by;
-          pd[s3][PD_BZ][t] = p.bz;
-          pd[s3][PD_T][t] = p.temp;
-          pd[s3][PD_B2][t] = p.b2;
-          double fv[NFX];
-          flux_x(p, g, fv);
-#pragma unroll
-          for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
-          flux_y(p, g, fv);
-#pragma unroll
-          for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
-        }
-        __syncthreads();
-
-        // ---- P2: diffusive fluxes at row r-1
-        double gyn[NG];
-#pragma unroll
-        for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
-        if (g.diffusive && s >= 2 && r - 1 <= Y1) {
-          double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
-#pragma unroll
-          for (int k = 0; k < NPD; ++k) {
-            xl[k] = pd[m1][k][tl];
-            xr[k] = pd[m1][k][tr];
-            yd[k] = pd[m2][k][t];
-            yu[k] = pd[s3][k][t];
-            own[k] = pd[m1][k][t];
-          }
-          double gxv[NG];
-          diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyn);
-#pragma unroll
-          for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
-        }
-        __syncthreads();
-
-#pragma unroll
-        for (int k = 0; k < NG; ++k) { gy3[k] = gy2[k]; gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
+        for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
         s3 = (s3 == 2) ? 0 : s3 + 1;
         s4 = (s4 + 1) & 3;
       }
