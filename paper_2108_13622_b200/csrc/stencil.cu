@@ -44,7 +44,7 @@ namespace {
 __host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; }   // skip BX
 __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }   // skip BY
 
-constexpr int RING_PD = 3, RING_FX = 4, RING_FY = 4, RING_GX = 2;
+constexpr int RING_PD = 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
 
 struct RowSrc {
   const double* u;     // row base of field 0 in the base state
@@ -200,6 +200,11 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       double gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
+      // own-column differentiated primitives of rows r-1 and r-2 (registers);
+      // shared memory holds only the row x-neighbours read (PD of row r-1)
+      double pr1[NPD], pr2[NPD];
+#pragma unroll
+      for (int k = 0; k < NPD; ++k) pr1[k] = pr2[k] = 0.0;
 
       // prefetch registers: state (and direction) of the next row to consume
       double nu[NF], nd[NF];
@@ -215,11 +220,9 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       }
 
       const int nsteps = (Y1 - Y0) + 4;
-      int s3 = 0, s4 = 0;  // s % 3, s % 4
+      int s4 = 0;  // s % 4
       for (int s = 0; s < nsteps; ++s) {
         const int r = Y0 - 2 + s;
-        const int m1 = (s3 == 0) ? 2 : s3 - 1;  // PD slot of row r-1
-        const int m2 = (s3 == 2) ? 0 : s3 + 1;  // PD slot of row r-2
         const bool out_row = (s >= 4) && col_ok;
         const long long obase = (long long)(r - 2) * g.nx + c_out;
 
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         }
 
         // ---- P1: state at (r, cg) from the prefetch registers
+        double pn[NPD];
         {
           double x[NF];
 #pragma unroll
@@ -256,14 +260,16 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           }
           Prim p;
           primitives(x, g, p);
-          pd[s3][PD_VX][t] = p.vx;
-          pd[s3][PD_VY][t] = p.vy;
-          pd[s3][PD_VZ][t] = p.vz;
-          pd[s3][PD_BX][t] = p.bx;
-          pd[s3][PD_BY][t] = p.by;
-          pd[s3][PD_BZ][t] = p.bz;
-          pd[s3][PD_T][t] = p.temp;
-          pd[s3][PD_B2][t] = p.b2;
+          pn[PD_VX] = p.vx;
+          pn[PD_VY] = p.vy;
+          pn[PD_VZ] = p.vz;
+          pn[PD_BX] = p.bx;
+          pn[PD_BY] = p.by;
+          pn[PD_BZ] = p.bz;
+          pn[PD_T] = p.temp;
+          pn[PD_B2] = p.b2;
+#pragma unroll
+          for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
           double fv[NFX];
           flux_x(p, g, fv);
 #pragma unroll
@@ -279,20 +285,19 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 #pragma unroll
         for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
         if (g.diffusive && s >= 2) {
-          double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
+          double xl[NPD], xr[NPD];
 #pragma unroll
           for (int k = 0; k < NPD; ++k) {
-            xl[k] = pd[m1][k][tl];
-            xr[k] = pd[m1][k][tr];
-            yd[k] = pd[m2][k][t];
-            yu[k] = pd[s3][k][t];
-            own[k] = pd[m1][k][t];
+            xl[k] = pd[(s + 1) & 1][k][tl];   // PD of row r-1 at t-1, t+1
+            xr[k] = pd[(s + 1) & 1][k][tr];
           }
           double gxv[NG];
-          diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyn);
+          diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyn);
 #pragma unroll
           for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
         }
+#pragma unroll
+        for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
         __syncthreads();
 
         // ---- P3: output row o = r-2
@@ -368,7 +373,6 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
 #pragma unroll
         for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
-        s3 = (s3 == 2) ? 0 : s3 + 1;
         s4 = (s4 + 1) & 3;
       }
       __syncthreads();   // rings are reused by the next unit
