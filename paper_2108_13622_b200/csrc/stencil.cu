@@ -36,6 +36,10 @@
 #include <climits>
 #include "kernels.h"
 
+#ifndef XB_EPI_PREFETCH
+#define XB_EPI_PREFETCH 0
+#endif
+
 namespace xb {
 
 namespace {
@@ -228,6 +232,20 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
         // epilogue operands of output row r-2: issue now, consume in P3
         double efu[NF], ey[NF], ep[NF];
+#if XB_EPI_PREFETCH
+        // variant: only pull the lines into L2 now; load them at P3 (fewer live registers)
+        if (MODE != MODE_RHS && out_row) {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            const long long i = obase + f * g.plane;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
+            if (MODE == MODE_LEJA) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
+            }
+          }
+        }
+#else
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
@@ -239,6 +257,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             }
           }
         }
+#endif
 
         // ---- P1: state at (r, cg) from the prefetch registers
         double pn[NPD];
@@ -302,6 +321,19 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
         // ---- P3: output row o = r-2
         if (out_row) {
+#if XB_EPI_PREFETCH
+          if (MODE != MODE_RHS) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const long long i = obase + f * g.plane;
+              efu[f] = __ldg(a.fu + i);
+              if (MODE == MODE_LEJA) {
+                ey[f] = __ldg(dir + i);
+                ep[f] = __ldg(pin + i);
+              }
+            }
+          }
+#endif
           const int fx2 = (s4 + 2) & 3;   // FX / FY slot of row r-2 (s-2 mod 4)
           const int fy1 = (s4 + 3) & 3;   // FY slot of row r-1
           const int fy3 = (s4 + 1) & 3;   // FY slot of row r-3
@@ -429,14 +461,12 @@ void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_ro
   const int slots = 2 * nsm;
   double best = 1e300;
   int best_seg = g.ny;
-  for (int seg = 8; seg <= g.ny + 8; seg += (seg < 64 ? 1 : 8)) {
-    const int s = seg > g.ny ? g.ny : seg;
+  for (int s = 1; s <= g.ny; ++s) {
     const int nseg = (g.ny + s - 1) / s;
     const long long units = (long long)units_x * nseg;
     const long long waves = (units + slots - 1) / slots;
-    const double cost = (double)waves * (s + 4);
+    const double cost = (double)waves * (s + 4);   // row steps of the busiest CTA
     if (cost < best - 1e-9) { best = cost; best_seg = s; }
-    if (seg > g.ny) break;
   }
   seg_rows = best_seg;
   nunits = units_x * ((g.ny + seg_rows - 1) / seg_rows);
