@@ -109,8 +109,59 @@ def _exprb54s4(lin, br, u, dt, rhs):
     return u5, rel_err(u4, u5)
 
 
+def _epirk5p1(lin, br, u, dt, rhs):
+    """integrators.py:56-75, 202-222."""
+    a11, a21, a22 = 0.35129592695058193092, 0.84405472011657126298, 1.6905891609568963624
+    b1, b2, b3 = 1.0, 1.2727127317356892397, 2.271459926542262275
+    g11, g21, g22, g31 = a11, a21, 0.5, 1.0
+    g32, g33, g32e, g33e = 0.71111095364366870359, 0.62378111953371494809, 0.5, 1.0
+    fu = lin.fu
+    a = u + a11 * dt * br.apply(1, g11, fu)
+    da = stage_diff(lin, rhs, a, u, fu)
+    b = (u + a21 * dt * br.apply(1, g21, fu) + a22 * dt * br.apply(1, g22, da))
+    db = stage_diff(lin, rhs, b, u, fu)
+    w = db - 2.0 * da
+    p1 = br.apply(1, g31, fu)
+    u5 = (u + b1 * dt * p1 + b2 * dt * br.apply(1, g32, da) + b3 * dt * br.apply(3, g33, w))
+    u4 = (u + b1 * dt * p1 + b2 * dt * br.apply(1, g32e, da) + b3 * dt * br.apply(3, g33e, w))
+    return u5, rel_err(u4, u5)
+
+
 SCHEMES = {"exp-euler": _euler, "ros-euler": _euler,
-           "exprb43": _exprb43, "exprb54s4": _exprb54s4}
+           "exprb43": _exprb43, "exprb54s4": _exprb54s4, "epirk5p1": _epirk5p1}
+
+# explicit embedded pairs, integrators.py:225-281 (Zonneveld 4(3), Dormand-Prince 5(4))
+_TAB = {
+    "rk43": ([[], [0.5], [0.0, 0.5], [0.0, 0.0, 1.0],
+              [5.0 / 32.0, 7.0 / 32.0, 13.0 / 32.0, -1.0 / 32.0]],
+             [1.0 / 6.0, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 6.0, 0.0],
+             [-0.5, 7.0 / 3.0, 7.0 / 3.0, 13.0 / 6.0, -16.0 / 3.0]),
+    "dopri54": ([[], [0.2], [3.0 / 40.0, 9.0 / 40.0], [44.0 / 45.0, -56.0 / 15.0, 32.0 / 9.0],
+                 [19372.0 / 6561.0, -25360.0 / 2187.0, 64448.0 / 6561.0, -212.0 / 729.0],
+                 [9017.0 / 3168.0, -355.0 / 33.0, 46732.0 / 5247.0, 49.0 / 176.0,
+                  -5103.0 / 18656.0],
+                 [35.0 / 384.0, 0.0, 500.0 / 1113.0, 125.0 / 192.0, -2187.0 / 6784.0,
+                  11.0 / 84.0]],
+                [35.0 / 384.0, 0.0, 500.0 / 1113.0, 125.0 / 192.0, -2187.0 / 6784.0,
+                 11.0 / 84.0, 0.0],
+                [5179.0 / 57600.0, 0.0, 7571.0 / 16695.0, 393.0 / 640.0, -92097.0 / 339200.0,
+                 187.0 / 2100.0, 1.0 / 40.0]),
+}
+ORDERS.update({"epirk5p1": (5, 4), "rk43": (4, 3), "dopri54": (5, 4)})
+
+
+def _explicit(scheme, rhs, u, dt):
+    a, b, bhat = _TAB[scheme]
+    ks = []
+    for row in a:
+        x = u
+        for cf, kj in zip(row, ks):
+            if cf != 0.0:
+                x = x + dt * cf * kj
+        ks.append(np.asarray(rhs(x), dtype=float))
+    hi = u + dt * sum(bi * ki for bi, ki in zip(b, ks) if bi != 0.0)
+    lo = u + dt * sum(bi * ki for bi, ki in zip(bhat, ks) if bi != 0.0)
+    return hi, rel_err(lo, hi)
 
 
 @dataclass
@@ -128,6 +179,13 @@ def one_step(scheme, rhs, u, dt, alpha, tol, lin=None, cache=None):
         raise ValueError("dt")
     u = np.asarray(u, dtype=float)
     before = rhs.calls
+    if scheme in _TAB:
+        try:
+            un, err = _explicit(scheme, rhs, u, dt)
+            ok = np.all(np.isfinite(un)) and np.isfinite(err)
+        except (mhd_np.NonFiniteRhs, FloatingPointError):
+            un, err, ok = u, np.inf, False
+        return StepOut(un, err, rhs.calls - before, 0, 0, bool(ok))
     mag = alpha.alpha if isinstance(alpha, lj.Spectrum) else float(alpha)
     if lin is None:
         lin = lj.Frozen(rhs, u)

@@ -184,7 +184,12 @@ def step_cases():
     meta = []
     for tag, setup, scheme, dt in (("kh32_exprb43", sc.kh_setup(32), Scheme.EXPRB43, 2e-3),
                                    ("harris32_exprb54s4", sc.harris_setup(32),
-                                    Scheme.EXPRB54S4, 0.05)):
+                                    Scheme.EXPRB54S4, 0.05),
+                                   ("kh32_epirk5p1", sc.kh_setup(32), Scheme.EPIRK5P1, 2e-3),
+                                   ("kh32_rosEuler", sc.kh_setup(32), Scheme.ROS_EULER, 1e-3),
+                                   ("kh32_rk43", sc.kh_setup(32), Scheme.RK43, 1e-4),
+                                   ("harris32_dopri54", sc.harris_setup(32), Scheme.DOPRI54,
+                                    0.01)):
         q = setup_state(setup)
         params = MHDParams(mu=setup.mu, eta=setup.eta, kappa=setup.kappa)
         op = mhd_op(q, setup.dx, setup.dy, params)
