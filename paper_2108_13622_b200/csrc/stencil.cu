@@ -39,6 +39,51 @@
 #ifndef XB_EPI_PREFETCH
 #define XB_EPI_PREFETCH 0
 #endif
+#ifndef XB_GY_SMEM
+#define XB_GY_SMEM 0
+#endif
+// Variants kept for A/B measurement (all measured slower on B200 at 2048^2 /
+// 4096^2, see profiles/): epilogue operands prefetched to L2 only (no change),
+// GY ring in shared memory (-35%: smaller L1), L1 cache hints (-10%).
+#ifndef XB_CACHE_HINTS
+#define XB_CACHE_HINTS 0
+#endif
+
+namespace xb {
+namespace {
+// L1 policy of the streamed operands.  u, F(u) and p are read once per
+// launch: do not let them displace the rows of y, which every thread reads
+// twice (as the JVP direction of row r, and again two rows later in the
+// Newton-update epilogue).
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if XB_CACHE_HINTS
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+#if XB_CACHE_HINTS
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_reuse(const double* p) {
+#if XB_CACHE_HINTS
+  double v;
+  asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+}  // namespace
+}  // namespace xb
 
 namespace xb {
 
@@ -49,6 +94,11 @@ __host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; } 
 __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }   // skip BY
 
 constexpr int RING_PD = 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
+#if XB_GY_SMEM
+constexpr int RING_GY = 3;   // own-column diffusive y-fluxes of rows r-1..r-3
+#else
+constexpr int RING_GY = 0;
+#endif
 
 struct RowSrc {
   const double* u;     // row base of field 0 in the base state
@@ -137,6 +187,9 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       reinterpret_cast<double (*)[NFY][SW]>(smem + (RING_PD * NPD + RING_FX * NFX) * SW);
   double (*gxs)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(
       smem + (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY) * SW);
+  double (*gys)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(
+      smem + (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG) * SW);
+  (void)gys;
   __shared__ double red[SW / 32];
   __shared__ int am_last;
 
@@ -201,9 +254,12 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       const int tl = max(t - 1, 0), tr = min(t + 1, SW - 1);
       const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
 
+#if !XB_GY_SMEM
       double gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
+#endif
+      int s3 = 0;  // s % 3 (GY ring)
       // own-column differentiated primitives of rows r-1 and r-2 (registers);
       // shared memory holds only the row x-neighbours read (PD of row r-1)
       double pr1[NPD], pr2[NPD];
@@ -218,8 +274,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         nflip = rs.flip;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          nu[f] = __ldg(rs.u + f * rs.fs + cs);
-          if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
+          nu[f] = ld_stream(rs.u + f * rs.fs + cs);
+          if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + f * rs.fs + cs);
         }
       }
 
@@ -250,10 +306,10 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
             const long long i = obase + f * g.plane;
-            efu[f] = __ldg(a.fu + i);
+            efu[f] = ld_stream(a.fu + i);
             if (MODE == MODE_LEJA) {
-              ey[f] = __ldg(dir + i);
-              ep[f] = __ldg(pin + i);
+              ey[f] = ld_reuse(dir + i);
+              ep[f] = ld_stream(pin + i);
             }
           }
         }
@@ -273,8 +329,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-              nu[f] = __ldg(rs.u + f * rs.fs + cs);
-              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + f * rs.fs + cs);
+              nu[f] = ld_stream(rs.u + f * rs.fs + cs);
+              if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + f * rs.fs + cs);
             }
           }
           Prim p;
@@ -326,10 +382,10 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
               const long long i = obase + f * g.plane;
-              efu[f] = __ldg(a.fu + i);
+              efu[f] = ld_stream(a.fu + i);
               if (MODE == MODE_LEJA) {
-                ey[f] = __ldg(dir + i);
-                ep[f] = __ldg(pin + i);
+                ey[f] = ld_reuse(dir + i);
+                ep[f] = ld_stream(pin + i);
               }
             }
           }
@@ -362,12 +418,20 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gxs[gs][5][tr], gxs[gs][5][tl]), g.h2x));
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BY] = __dadd_rn(F[BY], 0.0);
-            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gyn[0], gy2[0]), g.h2y));
-            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gyn[1], gy2[1]), g.h2y));
-            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gyn[2], gy2[2]), g.h2y));
-            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gyn[3], gy2[3]), g.h2y));
-            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gyn[4], gy2[4]), g.h2y));
-            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gyn[5], gy2[5]), g.h2y));
+#if XB_GY_SMEM
+            double gy3[NG];   // GY of row r-3: written two steps ago (slot (s+1) % 3)
+            const int g3 = (s3 == 2) ? 0 : s3 + 1;
+#pragma unroll
+            for (int k = 0; k < NG; ++k) gy3[k] = gys[g3][k][t];
+#else
+            const double* gy3 = gy2;
+#endif
+            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gyn[0], gy3[0]), g.h2y));
+            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gyn[1], gy3[1]), g.h2y));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gyn[2], gy3[2]), g.h2y));
+            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gyn[3], gy3[3]), g.h2y));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gyn[4], gy3[4]), g.h2y));
+            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gyn[5], gy3[5]), g.h2y));
           }
           // non-finite detection (mhd.py:225-231): exponent field all ones
           {
@@ -404,7 +468,12 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         }
 
 #pragma unroll
+#if XB_GY_SMEM
+        for (int k = 0; k < NG; ++k) gys[s3][k][t] = gyn[k];
+#else
         for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
+#endif
+        s3 = (s3 == 2) ? 0 : s3 + 1;
         s4 = (s4 + 1) & 3;
       }
       __syncthreads();   // rings are reused by the next unit
@@ -450,15 +519,40 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
 size_t stencil_smem_bytes() {
   return sizeof(double) * (size_t)SW *
-         (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG);
+         (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG + RING_GY * NG);
 }
 
 // Work decomposition: column strips of SOUT outputs x y-segments; the
 // persistent grid is 2 CTAs per SM.  The segment length trades warm-up rows
 // (4 per segment) against wave quantisation of the units over the grid.
+template <int MODE, int KX, int KY>
+cudaError_t set_smem_attr() {
+  return cudaFuncSetAttribute(stencil_kernel<MODE, KX, KY>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)stencil_smem_bytes());
+}
+
+// Resident CTAs per SM of the fused iteration kernel (registers + shared memory).
+int stencil_occupancy() {
+  static int occ = 0;
+  if (occ) return occ;
+  int n = 0;
+  if (set_smem_attr<MODE_LEJA, DIV_MUL, DIV_MUL>() == cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &n, stencil_kernel<MODE_LEJA, DIV_MUL, DIV_MUL>, SW, stencil_smem_bytes()) ==
+          cudaSuccess &&
+      n > 0) {
+    occ = n;
+  } else {
+    cudaGetLastError();
+    occ = 2;
+  }
+  return occ;
+}
+
 void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows, int& grid) {
   units_x = (g.nx + SOUT - 1) / SOUT;
-  const int slots = 2 * nsm;
+  const int slots = stencil_occupancy() * nsm;
   double best = 1e300;
   int best_seg = g.ny;
   for (int s = 1; s <= g.ny; ++s) {

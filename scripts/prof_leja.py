@@ -34,5 +34,6 @@ rc = _lib.load().xmhd_time_leja_iterations(mhd.ctx.bind_stream(), _lib.ptr(lin.b
                                            c.ctypes.data_as(dp), iters, ctypes.byref(out))
 assert rc == 0, _lib.err_text()
 torch.cuda.synchronize()
+print(mhd.ctx.plan())
 print(f"n={n} fused Leja iteration: {out.value:.4f} ms -> "
       f"{384 * n * n / (out.value * 1e-3) / 1e9:.1f} GB/s algorithmic")
