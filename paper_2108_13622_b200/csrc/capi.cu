@@ -40,6 +40,7 @@ struct xmhd_ctx {
   const double* leja_fu = nullptr;
   long long launches = 0;
   int batch_max = 64;
+  int last_iters = 2;          // degree of the previous fused Leja call (batch sizing)
   bool force_ieee = false;
 };
 
@@ -163,7 +164,12 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
   a.coeffs = c->coeffs_d;
   a.xi = c->xi_d;
   a.ctl = c->ctl;
-  int batch = 2;
+  // first batch: the previous call's degree on this context (steppers call
+  // phi-actions of similar degree back to back), so most calls need one sync
+  const int done = c->ctl_h->iters;
+  int batch = c->last_iters - done;
+  if (batch < 2) batch = 2;
+  if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
     for (int k = 0; k < batch; ++k) {
       CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
@@ -174,6 +180,7 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
     if (c->ctl_h->status != LJ_RUNNING) break;
     batch = batch * 2 < c->batch_max ? batch * 2 : c->batch_max;
   }
+  if (c->ctl_h->status != LJ_NEED_COEFFS) c->last_iters = c->ctl_h->iters;
   fill_state(*c->ctl_h, st);
   return XMHD_OK;
 }
