@@ -111,6 +111,9 @@ int xmhd_cfl_speeds(xmhd_ctx* ctx, const double* u, double* out2);
 int xmhd_leja_start(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
                     const double* v, double dt, double q, double theta, double tol,
                     const double* xi, const double* coeffs, int ncoef, xmhd_leja_state* st);
+/* Expected number of Newton terms of the next xmhd_leja_start (host-side
+ * launch batching only; results do not depend on it). */
+int xmhd_leja_hint(xmhd_ctx* ctx, int expected_iterations);
 /* After XMHD_LEJA_NEED_COEFFS: upload the grown chunk and continue. */
 int xmhd_leja_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef, xmhd_leja_state* st);
 /* Copy the interpolant p of the finished call into p_out (device, 8*nx*ny). */

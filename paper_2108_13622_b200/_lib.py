@@ -61,6 +61,7 @@ _SIGS = {
     "xmhd_leja_start": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I,
                              ctypes.POINTER(LejaState)]),
     "xmhd_leja_resume": (_I, [_P, _PD, _I, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_hint": (_I, [_P, _I]),
     "xmhd_leja_result": (_I, [_P, _P]),
     "xmhd_leja_current_y": (_I, [_P, _P]),
     "xmhd_leja_generic_start": (_I, [_P, _P, _L, _D, _D, _D, _D, _PD, _PD, _I,

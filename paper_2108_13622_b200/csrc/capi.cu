@@ -40,7 +40,7 @@ struct xmhd_ctx {
   const double* leja_fu = nullptr;
   long long launches = 0;
   int batch_max = 64;
-  int last_iters = 2;          // degree of the previous fused Leja call (batch sizing)
+  int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
   bool force_ieee = false;
 };
 
@@ -164,10 +164,10 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
   a.coeffs = c->coeffs_d;
   a.xi = c->xi_d;
   a.ctl = c->ctl;
-  // first batch: the previous call's degree on this context (steppers call
-  // phi-actions of similar degree back to back), so most calls need one sync
+  // first batch: the caller's degree hint (xmhd_leja_hint; the host keys it by
+  // phi order and interval scale), so most calls need a single sync
   const int done = c->ctl_h->iters;
-  int batch = c->last_iters - done;
+  int batch = c->hint_iters - done;
   if (batch < 2) batch = 2;
   if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
@@ -180,7 +180,6 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
     if (c->ctl_h->status != LJ_RUNNING) break;
     batch = batch * 2 < c->batch_max ? batch * 2 : c->batch_max;
   }
-  if (c->ctl_h->status != LJ_NEED_COEFFS) c->last_iters = c->ctl_h->iters;
   fill_state(*c->ctl_h, st);
   return XMHD_OK;
 }
@@ -498,6 +497,12 @@ int xmhd_leja_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_sta
   CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   return leja_run(c, st);
+}
+
+int xmhd_leja_hint(xmhd_ctx* c, int expected_iterations) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  c->hint_iters = expected_iterations < 2 ? 2 : expected_iterations;
+  return XMHD_OK;
 }
 
 int xmhd_leja_result(xmhd_ctx* c, double* p_out) {
