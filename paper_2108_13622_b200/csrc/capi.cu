@@ -245,6 +245,10 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
   if (bc_x != XMHD_BC_PERIODIC && bc_x != XMHD_BC_REFLECTING)
     return fail(XMHD_BADARG, "bad bc_x");
   if (bc_y < XMHD_BC_PERIODIC || bc_y > XMHD_BC_HALO) return fail(XMHD_BADARG, "bad bc_y");
+  // the kernels index a vector with 32-bit unsigned element offsets (34 GB)
+  if (8.0 * (double)nx * (double)ny >= 4294967296.0)
+    return fail(XMHD_BADARG, "8*nx*ny must stay below 2^32 elements per device (split into "
+                             "y-strips over more GPUs)");
   xmhd_ctx* c = new xmhd_ctx();
   const bool ieee = std::getenv("XMHD_DIV_IEEE") && std::atoi(std::getenv("XMHD_DIV_IEEE"));
   c->force_ieee = ieee;

@@ -100,10 +100,15 @@ constexpr int RING_GY = 3;   // own-column diffusive y-fluxes of rows r-1..r-3
 constexpr int RING_GY = 0;
 #endif
 
+// Source of one ghost-extended row.  Element offsets are 32-bit unsigned: a
+// per-GPU vector of 8*nx*ny < 2^32 doubles (34 GB) covers every grid that fits
+// a 180 GB device (checked at context creation), and unsigned offsets turn
+// each access into a single IMAD.WIDE.U32 address.
 struct RowSrc {
-  const double* u;     // row base of field 0 in the base state
-  const double* d;     // row base of field 0 in the direction vector
-  long long fs;        // stride between fields
+  const double* u;     // base of the base state (or its halo buffer)
+  const double* d;     // base of the direction vector (or its halo buffer)
+  unsigned off;        // element offset of the row's field-0 start
+  unsigned fs;         // stride between fields
   int flip;            // mirror ghost row: negate MY, BY
 };
 
@@ -111,7 +116,9 @@ __device__ __forceinline__ RowSrc row_source(int r, const Geom& g, const double*
                                              const double* d) {
   RowSrc s;
   s.flip = 0;
-  s.fs = g.plane;
+  s.fs = (unsigned)g.plane;
+  s.u = u;
+  s.d = d;
   int rr = r;
   if (g.bcy == BC_PERIODIC) {
     // r lies in [-2, ny+2) and ny >= 2: one conditional wrap, no integer division
@@ -122,20 +129,21 @@ __device__ __forceinline__ RowSrc row_source(int r, const Geom& g, const double*
     rr = min(max(rr, 0), g.ny - 1);
   } else {  // BC_HALO: rows owned by the y-neighbours, [field][2][nx]
     if (r < 0) {
-      s.u = g.halo_lo + (long long)(r + 2) * g.nx;
-      s.d = g.halo_lo_dir ? g.halo_lo_dir + (long long)(r + 2) * g.nx : nullptr;
-      s.fs = 2LL * g.nx;
+      s.u = g.halo_lo;
+      s.d = g.halo_lo_dir;
+      s.off = (unsigned)(r + 2) * (unsigned)g.nx;
+      s.fs = 2u * (unsigned)g.nx;
       return s;
     }
     if (r >= g.ny) {
-      s.u = g.halo_hi + (long long)(r - g.ny) * g.nx;
-      s.d = g.halo_hi_dir ? g.halo_hi_dir + (long long)(r - g.ny) * g.nx : nullptr;
-      s.fs = 2LL * g.nx;
+      s.u = g.halo_hi;
+      s.d = g.halo_hi_dir;
+      s.off = (unsigned)(r - g.ny) * (unsigned)g.nx;
+      s.fs = 2u * (unsigned)g.nx;
       return s;
     }
   }
-  s.u = u + (long long)rr * g.nx;
-  s.d = d ? d + (long long)rr * g.nx : nullptr;
+  s.off = (unsigned)rr * (unsigned)g.nx;
   return s;
 }
 
@@ -274,8 +282,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         nflip = rs.flip;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          nu[f] = ld_stream(rs.u + f * rs.fs + cs);
-          if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + f * rs.fs + cs);
+          nu[f] = ld_stream(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+          if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
         }
       }
 
@@ -284,7 +292,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       for (int s = 0; s < nsteps; ++s) {
         const int r = Y0 - 2 + s;
         const bool out_row = (s >= 4) && col_ok;
-        const long long obase = (long long)(r - 2) * g.nx + c_out;
+        const unsigned obase = (unsigned)(r - 2) * (unsigned)g.nx + (unsigned)c_out;
+        const unsigned plane = (unsigned)g.plane;
 
         // epilogue operands of output row r-2: issue now, consume in P3
         double efu[NF], ey[NF], ep[NF];
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            const long long i = obase + f * g.plane;
+            const unsigned i = obase + (unsigned)f * plane;
             asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
             if (MODE == MODE_LEJA) {
               asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            const long long i = obase + f * g.plane;
+            const unsigned i = obase + (unsigned)f * plane;
             efu[f] = ld_stream(a.fu + i);
             if (MODE == MODE_LEJA) {
               ey[f] = ld_reuse(dir + i);
@@ -329,8 +338,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-              nu[f] = ld_stream(rs.u + f * rs.fs + cs);
-              if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + f * rs.fs + cs);
+              nu[f] = ld_stream(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+              if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
             }
           }
           Prim p;
@@ -381,7 +390,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           if (MODE != MODE_RHS) {
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-              const long long i = obase + f * g.plane;
+              const unsigned i = obase + (unsigned)f * plane;
               efu[f] = ld_stream(a.fu + i);
               if (MODE == MODE_LEJA) {
                 ey[f] = ld_reuse(dir + i);
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           }
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
-            const long long i = obase + f * g.plane;
+            const unsigned i = obase + (unsigned)f * plane;
             if (MODE == MODE_RHS) {
               a.out[i] = F[f];
             } else if (MODE == MODE_JVP) {
