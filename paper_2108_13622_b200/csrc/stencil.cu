@@ -31,7 +31,8 @@
 // Divisions: constant divisors (2dx, 2dy, eps, theta, mu0) use a precomputed
 // RN reciprocal with Markstein correction (common.cuh), which is the correctly
 // rounded quotient; 2dx / 2dy kinds are template parameters.  Divisions by the
-// per-cell density stay IEEE divisions.
+// per-cell density share one correctly rounded reciprocal (__drcp_rn) and are
+// completed by the two-correction Markstein sequence (exact for any divisor).
 #include <cfloat>
 #include <climits>
 #include "kernels.h"
@@ -47,6 +48,15 @@
 // GY ring in shared memory (-35%: smaller L1), L1 cache hints (-10%).
 #ifndef XB_CACHE_HINTS
 #define XB_CACHE_HINTS 0
+#endif
+// Variant: shared-memory rings hold field pairs as double2 (16-byte LDS/STS,
+// half the shared-memory instructions, same bytes).  Measured neutral on B200
+// (0.3488 vs 0.3461 ms at 2048^2): shared-memory issue is not the limiter.
+#ifndef XB_SMEM_V2
+#define XB_SMEM_V2 0
+#endif
+#if XB_SMEM_V2 && XB_GY_SMEM
+#error "XB_SMEM_V2 requires XB_GY_SMEM=0"
 #endif
 
 namespace xb {
@@ -99,6 +109,24 @@ constexpr int RING_GY = 3;   // own-column diffusive y-fluxes of rows r-1..r-3
 #else
 constexpr int RING_GY = 0;
 #endif
+// double2 slots per ring row (odd counts padded)
+constexpr int NPD2 = (NPD + 1) / 2, NFX2 = (NFX + 1) / 2, NFY2 = (NFY + 1) / 2, NG2 = (NG + 1) / 2;
+
+template <int N>
+__device__ __forceinline__ void st_pairs(double2* row, const double* v) {
+#pragma unroll
+  for (int k = 0; k < (N + 1) / 2; ++k)
+    row[k * SW] = make_double2(v[2 * k], (2 * k + 1 < N) ? v[2 * k + 1] : 0.0);
+}
+template <int N>
+__device__ __forceinline__ void ld_pairs(const double2* row, double* v) {
+#pragma unroll
+  for (int k = 0; k < (N + 1) / 2; ++k) {
+    const double2 p = row[k * SW];
+    v[2 * k] = p.x;
+    if (2 * k + 1 < N) v[2 * k + 1] = p.y;
+  }
+}
 
 // Source of one ghost-extended row.  Element offsets are 32-bit unsigned: a
 // per-GPU vector of 8*nx*ny < 2^32 doubles (34 GB) covers every grid that fits
@@ -188,7 +216,16 @@ __device__ __forceinline__ double sum_partials(const double* p, int nblk, int st
 
 template <int MODE, int KX, int KY>
 __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
+#if XB_SMEM_V2
+  double2* const s2 = reinterpret_cast<double2*>(smem);
+  double2 (*pd2)[NPD2][SW] = reinterpret_cast<double2 (*)[NPD2][SW]>(s2);
+  double2 (*fx2s)[NFX2][SW] = reinterpret_cast<double2 (*)[NFX2][SW]>(s2 + RING_PD * NPD2 * SW);
+  double2 (*fy2s)[NFY2][SW] =
+      reinterpret_cast<double2 (*)[NFY2][SW]>(s2 + (RING_PD * NPD2 + RING_FX * NFX2) * SW);
+  double2 (*gx2s)[NG2][SW] = reinterpret_cast<double2 (*)[NG2][SW]>(
+      s2 + (RING_PD * NPD2 + RING_FX * NFX2 + RING_FY * NFY2) * SW);
+#endif
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
   double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
   double (*fys)[NFY][SW] =
@@ -352,15 +389,23 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           pn[PD_BZ] = p.bz;
           pn[PD_T] = p.temp;
           pn[PD_B2] = p.b2;
+          double fv[NFX];
+#if XB_SMEM_V2
+          st_pairs<NPD>(&pd2[s & 1][0][t], pn);
+          flux_x(p, g, fv);
+          st_pairs<NFX>(&fx2s[s4][0][t], fv);
+          flux_y(p, g, fv);
+          st_pairs<NFY>(&fy2s[s4][0][t], fv);
+#else
 #pragma unroll
           for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
-          double fv[NFX];
           flux_x(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
           flux_y(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
+#endif
         }
         __syncthreads();
 
@@ -369,16 +414,25 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 #pragma unroll
         for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
         if (g.diffusive && s >= 2) {
-          double xl[NPD], xr[NPD];
+          double xl[NPD], xr[NPD];   // PD of row r-1 at t-1, t+1
+#if XB_SMEM_V2
+          ld_pairs<NPD>(&pd2[(s + 1) & 1][0][tl], xl);
+          ld_pairs<NPD>(&pd2[(s + 1) & 1][0][tr], xr);
+#else
 #pragma unroll
           for (int k = 0; k < NPD; ++k) {
-            xl[k] = pd[(s + 1) & 1][k][tl];   // PD of row r-1 at t-1, t+1
+            xl[k] = pd[(s + 1) & 1][k][tl];
             xr[k] = pd[(s + 1) & 1][k][tr];
           }
+#endif
           double gxv[NG];
           diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyn);
+#if XB_SMEM_V2
+          st_pairs<NG>(&gx2s[(s + 1) & 1][0][t], gxv);
+#else
 #pragma unroll
           for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
+#endif
         }
 #pragma unroll
         for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
@@ -405,26 +459,54 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           const int gs = s & 1;           // GX slot of row r-2
           double F[NF];
           // ideal part: out = -(dFX/2dx); out -= dFY/2dy       (mhd.py:177-178)
+          {
+            double a[NFX], b[NFX];
+#if XB_SMEM_V2
+            ld_pairs<NFX>(&fx2s[fx2][0][tr], a);
+            ld_pairs<NFX>(&fx2s[fx2][0][tl], b);
+#else
 #pragma unroll
-          for (int k = 0; k < NFX; ++k)
-            F[fx_field(k)] = -qdiv<KX>(__dsub_rn(fxs[fx2][k][tr], fxs[fx2][k][tl]), g.h2x);
+            for (int k = 0; k < NFX; ++k) { a[k] = fxs[fx2][k][tr]; b[k] = fxs[fx2][k][tl]; }
+#endif
+#pragma unroll
+            for (int k = 0; k < NFX; ++k)
+              F[fx_field(k)] = -qdiv<KX>(__dsub_rn(a[k], b[k]), g.h2x);
+          }
           F[BX] = -0.0;
+          {
+            double a[NFY], b[NFY];
+#if XB_SMEM_V2
+            ld_pairs<NFY>(&fy2s[fy1][0][t], a);
+            ld_pairs<NFY>(&fy2s[fy3][0][t], b);
+#else
 #pragma unroll
-          for (int k = 0; k < NFY; ++k) {
-            const int f = fy_field(k);
-            F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(fys[fy1][k][t], fys[fy3][k][t]), g.h2y));
+            for (int k = 0; k < NFY; ++k) { a[k] = fys[fy1][k][t]; b[k] = fys[fy3][k][t]; }
+#endif
+#pragma unroll
+            for (int k = 0; k < NFY; ++k) {
+              const int f = fy_field(k);
+              F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(a[k], b[k]), g.h2y));
+            }
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
           if (g.diffusive) {
             // out += dGX/2dx; out += dGY/2dy                 (mhd.py:222-223)
+            double gr[NG], gl[NG];
+#if XB_SMEM_V2
+            ld_pairs<NG>(&gx2s[gs][0][tr], gr);
+            ld_pairs<NG>(&gx2s[gs][0][tl], gl);
+#else
+#pragma unroll
+            for (int k = 0; k < NG; ++k) { gr[k] = gxs[gs][k][tr]; gl[k] = gxs[gs][k][tl]; }
+#endif
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BX] = __dadd_rn(F[BX], 0.0);
-            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gxs[gs][0][tr], gxs[gs][0][tl]), g.h2x));
-            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gxs[gs][1][tr], gxs[gs][1][tl]), g.h2x));
-            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gxs[gs][2][tr], gxs[gs][2][tl]), g.h2x));
-            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gxs[gs][3][tr], gxs[gs][3][tl]), g.h2x));
-            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gxs[gs][4][tr], gxs[gs][4][tl]), g.h2x));
-            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gxs[gs][5][tr], gxs[gs][5][tl]), g.h2x));
+            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gr[0], gl[0]), g.h2x));
+            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gr[1], gl[1]), g.h2x));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gr[2], gl[2]), g.h2x));
+            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gr[3], gl[3]), g.h2x));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gr[4], gl[4]), g.h2x));
+            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gr[5], gl[5]), g.h2x));
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BY] = __dadd_rn(F[BY], 0.0);
 #if XB_GY_SMEM
@@ -527,6 +609,10 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 }
 
 size_t stencil_smem_bytes() {
+#if XB_SMEM_V2
+  return sizeof(double2) * (size_t)SW *
+         (RING_PD * NPD2 + RING_FX * NFX2 + RING_FY * NFY2 + RING_GX * NG2);
+#endif
   return sizeof(double) * (size_t)SW *
          (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG + RING_GY * NG);
 }
