@@ -167,6 +167,27 @@ int xmhd_time_leja_iterations(xmhd_ctx* ctx, const double* u, const double* fu, 
                               const double* xi, const double* coeffs500, int n_iter,
                               double* ms_per_iter);
 
+/* ---- Krylov baseline (replaces the NumPy Arnoldi loop of krylov.py:34-84) ----
+ * The paper's Leja-vs-Krylov comparison arm; the Hessenberg matrix and its
+ * phi_l(H)e1 stay on the host (at most 200 x 200).
+ *
+ * xmhd_krylov_mgs: both modified Gram-Schmidt passes of Arnoldi step j
+ * (krylov.py:60-67) against basis[0..nb-1] (device vectors of n doubles), w
+ * updated in place.  Stream-ordered: each update reads the previous launch's
+ * reduced dot from device memory; one host sync at the end.
+ * coef_out[0..nb) = pass-1 coefficients, coef_out[nb..2nb) = pass-2;
+ * *wsumsq_out = sum(w^2) after both passes (||w||^2 of krylov.py:68). */
+int xmhd_krylov_mgs(xmhd_ctx* ctx, const double* const* basis, int nb, double* w, long long n,
+                    double* coef_out, double* wsumsq_out);
+/* One MGS update for y-strip callers (coefficients are global, reduced by the
+ * caller between updates): w -= coef*v (v may be NULL: no update), then
+ * *sum_out = local sum(next * w) (sum(w * w) when next is NULL). */
+int xmhd_mgs_update(xmhd_ctx* ctx, double* w, long long n, const double* v, double coef,
+                    const double* next, double* sum_out);
+/* out = scale * sum_k coef[k] * basis[k], k = 0..m-1 (m <= 200; krylov.py:79-80). */
+int xmhd_krylov_combine(xmhd_ctx* ctx, const double* const* basis, const double* coef, int m,
+                        double scale, long long n, double* out);
+
 /* Host C++ port of _phi_divided_diffs (phi.py:99-144): first column of
  * phi_l of the bidiagonal node matrix, bitwise equal to the NumPy routine.
  * out has n entries. */

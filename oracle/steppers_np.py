@@ -18,6 +18,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from oracle import krylov_np as kr
 from oracle import leja_np as lj
 from oracle import mhd_np
 
@@ -44,8 +45,9 @@ def rel_err(a, b):
 
 
 class Broker:
-    def __init__(self, lin, dt, alpha, tol, cache=None):
+    def __init__(self, lin, dt, alpha, tol, cache=None, method="leja"):
         self.lin, self.dt, self.alpha, self.tol = lin, dt, alpha, tol
+        self.method = method
         self.apps = 0
         self.iters = 0
         self.failed = False
@@ -56,9 +58,12 @@ class Broker:
         if self.alpha < 1e-14:
             return vec / math.factorial(l)
         h = c * self.dt
-        q, th = lj.shift_scale(self.alpha * h)
-        r = lj.phi_leja(l, lambda w: lj.fd_jvp(self.lin, w), vec, h, q, th,
-                        self.tol, self.cache)
+        if self.method == "krylov":            # integrators.py:129-130
+            r = kr.phi_krylov(l, lambda w: lj.fd_jvp(self.lin, w), vec, h, self.tol)
+        else:
+            q, th = lj.shift_scale(self.alpha * h)
+            r = lj.phi_leja(l, lambda w: lj.fd_jvp(self.lin, w), vec, h, q, th,
+                            self.tol, self.cache)
         self.iters += r.iterations
         if not r.converged:
             self.failed = True
@@ -174,7 +179,7 @@ class StepOut:
     converged: bool
 
 
-def one_step(scheme, rhs, u, dt, alpha, tol, lin=None, cache=None):
+def one_step(scheme, rhs, u, dt, alpha, tol, lin=None, cache=None, method="leja"):
     if dt <= 0:
         raise ValueError("dt")
     u = np.asarray(u, dtype=float)
@@ -189,7 +194,7 @@ def one_step(scheme, rhs, u, dt, alpha, tol, lin=None, cache=None):
     mag = alpha.alpha if isinstance(alpha, lj.Spectrum) else float(alpha)
     if lin is None:
         lin = lj.Frozen(rhs, u)
-    br = Broker(lin, dt, mag, tol, cache)
+    br = Broker(lin, dt, mag, tol, cache, method)
     try:
         un, err = SCHEMES[scheme](lin, br, u, dt, rhs)
         ok = (not br.failed) and np.all(np.isfinite(un)) and np.isfinite(err)
@@ -246,7 +251,7 @@ class Report:
 
 def run(data0, dx, dy, mu, eta, kappa, scheme, tol, t_final, gamma=5.0 / 3.0,
         mu0=1.0, periodic_x=True, periodic_y=True, interval=50, seed=0,
-        controller="combined", max_accepted=None, cache=None):
+        controller="combined", max_accepted=None, cache=None, method="leja"):
     """Adaptive driver loop of harness.py:123-249 on an explicit initial state.
 
     ``max_accepted`` stops cleanly after that many accepted steps (the
@@ -282,7 +287,7 @@ def run(data0, dx, dy, mu, eta, kappa, scheme, tol, t_final, gamma=5.0 / 3.0,
         rep.spectrum_rhs_evals += op.calls - cs
         while True:
             cb = op.calls
-            res = one_step(scheme, op, u, dt, est, tol, lin, cache)
+            res = one_step(scheme, op, u, dt, est, tol, lin, cache, method)
             spent = op.calls - cb
             if res.converged and res.error_estimate <= tol:
                 break

@@ -11,8 +11,10 @@ raises ``NativeUnavailable``.
 from paper_2108_13622_b200._lib import NativeUnavailable
 from paper_2108_13622_b200.controllers import (ControllerConstants, ControllerMode, accept,
                                                combine, cost_next, traditional_next)
-from paper_2108_13622_b200.harness import RunConfig, RunReport, StepRecord, run
+from paper_2108_13622_b200.harness import (RunConfig, RunReport, StepRecord, divb_series,
+                                           make_reference, run, work_precision)
 from paper_2108_13622_b200.integrators import Scheme, error_norm, step
+from paper_2108_13622_b200.krylov import apply_phi_krylov
 from paper_2108_13622_b200.leja import (JacobianAction, PhiApplyResult, ShiftScale,
                                         apply_phi_leja, leja_points, shift_and_scale)
 from paper_2108_13622_b200.linearize import (FrozenLinearization, RhsBlowupError, RhsOperator,

@@ -38,6 +38,8 @@ struct xmhd_ctx {
   long long gen_n = 0;         // vector length of the current generic Leja call
   const double* leja_u = nullptr;
   const double* leja_fu = nullptr;
+  double* kry_d = nullptr;     // [512] MGS coefficient slots (Krylov baseline)
+  double* kry_h = nullptr;     // pinned [512]
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -316,6 +318,8 @@ int xmhd_destroy(xmhd_ctx* c) {
   cudaFreeHost(c->ctl_h);
   cudaFreeHost(c->h_dbl);
   cudaFreeHost(c->h_int);
+  cudaFree(c->kry_d);
+  cudaFreeHost(c->kry_h);
   delete c;
   return XMHD_OK;
 }
@@ -623,6 +627,75 @@ int xmhd_sumsq(xmhd_ctx* c, const double* x, long long n, double* out) {
   int rc = fetch_doubles(c, 1);
   if (rc) return rc;
   *out = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+// ---- Krylov baseline (krylov.py:34-84) ---------------------------------------
+
+static int ensure_krylov(xmhd_ctx* c) {
+  if (c->kry_d) return XMHD_OK;
+  CK(cudaMalloc(&c->kry_d, sizeof(double) * 512));
+  CK(cudaMallocHost(&c->kry_h, sizeof(double) * 512));
+  return XMHD_OK;
+}
+
+int xmhd_krylov_mgs(xmhd_ctx* c, const double* const* basis, int nb, double* w, long long n,
+                    double* coef_out, double* wsumsq_out) {
+  if (!c || !basis || !w || !coef_out || !wsumsq_out || nb < 1 || nb > KRYLOV_MAX + 1)
+    return fail(XMHD_BADARG, "bad krylov_mgs arguments");
+  for (int i = 0; i < nb; ++i)
+    if (!basis[i]) return fail(XMHD_BADARG, "null basis vector");
+  int rc = ensure_krylov(c);
+  if (rc) return rc;
+  // slots: [0, nb) pass-1 coefficients, [nb, 2nb) pass-2, 2nb = sum w^2
+  double* s = c->kry_d;
+  const RedBuf rb = redbuf(c);
+  CK(launch_mgs(w, n, nullptr, nullptr, 0.0, basis[0], s, rb, c->stream));
+  c->launches++;
+  for (int pass = 0; pass < 2; ++pass) {
+    double* sp = s + pass * nb;
+    for (int i = 0; i < nb; ++i) {
+      const bool last = (i + 1 == nb);
+      const double* next = !last ? basis[i + 1] : (pass == 0 ? basis[0] : nullptr);
+      double* cout = !last ? sp + i + 1 : s + (pass + 1) * nb;
+      CK(launch_mgs(w, n, basis[i], sp + i, 0.0, next, cout, rb, c->stream));
+      c->launches++;
+    }
+  }
+  CK(cudaMemcpyAsync(c->kry_h, s, sizeof(double) * (2 * nb + 1), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < 2 * nb; ++k) coef_out[k] = c->kry_h[k];
+  *wsumsq_out = c->kry_h[2 * nb];
+  return XMHD_OK;
+}
+
+int xmhd_mgs_update(xmhd_ctx* c, double* w, long long n, const double* v, double coef,
+                    const double* next, double* sum_out) {
+  if (!c || !w || !sum_out) return fail(XMHD_BADARG, "null arg");
+  int rc = ensure_krylov(c);
+  if (rc) return rc;
+  CK(launch_mgs(w, n, v, nullptr, coef, next, c->kry_d, redbuf(c), c->stream));
+  c->launches++;
+  CK(cudaMemcpyAsync(c->kry_h, c->kry_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *sum_out = c->kry_h[0];
+  return XMHD_OK;
+}
+
+int xmhd_krylov_combine(xmhd_ctx* c, const double* const* basis, const double* coef, int m,
+                        double scale, long long n, double* out) {
+  if (!c || !basis || !coef || !out || m < 1 || m > KRYLOV_MAX)
+    return fail(XMHD_BADARG, "bad krylov_combine arguments");
+  KrylovBasis B;
+  std::memset(&B, 0, sizeof(B));
+  for (int k = 0; k < m; ++k) {
+    if (!basis[k]) return fail(XMHD_BADARG, "null basis vector");
+    B.v[k] = basis[k];
+    B.c[k] = coef[k];
+  }
+  CK(launch_krylov_combine(out, n, B, m, scale, redbuf(c), c->stream));
+  c->launches++;
   return XMHD_OK;
 }
 

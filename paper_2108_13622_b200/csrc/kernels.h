@@ -122,6 +122,21 @@ cudaError_t launch_leja_update(const double* w, long long n, LejaCtl* ctl, doubl
                                double* const* pbuf, const double* coeffs, const double* xi,
                                RedBuf rb, cudaStream_t s);
 
+// Krylov baseline (krylov.py:34-84).
+constexpr int KRYLOV_MAX = 200;   // krylov.py:16 (M_CAP)
+struct KrylovBasis {
+  const double* v[KRYLOV_MAX];
+  double c[KRYLOV_MAX];
+};
+// w -= c*v (v non-null; c = *cin, or c_host when cin is null), then
+// *cout = sum(next * w) (sum(w * w) when next is null).
+cudaError_t launch_mgs(double* w, long long n, const double* v, const double* cin,
+                       double c_host, const double* next, double* cout, RedBuf rb,
+                       cudaStream_t s);
+// out = scale * sum_k c_k v_k (k = 0..m-1, left to right).
+cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B, int m,
+                                  double scale, RedBuf rb, cudaStream_t s);
+
 #ifdef __CUDACC__
 // Control update after one Newton term (leja.py:134-148); run by one thread
 // of the last CTA of the iteration kernel, after the deterministic reduction.

@@ -342,6 +342,43 @@ __global__ void __launch_bounds__(VT) leja_update_kernel(const double* __restric
   if (grid_reduce<2, false>(acc, rb, tot)) leja_finalize(ctl, tot[0], tot[1], 0, 0, cm);
 }
 
+// One modified Gram-Schmidt update of the Arnoldi loop (krylov.py:60-67):
+// w -= c*v (NumPy's rounded product, then the subtraction), then the dot of
+// the updated w with `next` (with w itself when next is null) reduced into
+// *cout.  c is read from the device slot cin (the previous launch's reduced
+// dot) or, when cin is null, taken from c_host.  v == null: dot only.
+__global__ void __launch_bounds__(VT) mgs_kernel(double* __restrict__ w, long long n,
+                                                 const double* __restrict__ v,
+                                                 const double* cin, double c_host,
+                                                 const double* __restrict__ next,
+                                                 double* cout, RedBuf rb) {
+  const double c = cin ? *cin : c_host;
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    double x = w[i];
+    if (v) {
+      x = __dsub_rn(x, __dmul_rn(c, __ldg(v + i)));
+      w[i] = x;
+    }
+    const double y = next ? __ldg(next + i) : x;
+    acc[0] = __fma_rn(y, x, acc[0]);
+  }
+  double tot[1];
+  if (grid_reduce<1, false>(acc, rb, tot)) *cout = tot[0];
+}
+
+// out = scale * (sum_k c_k v_k), k = 0..m-1 in order (krylov.py:79-80).
+__global__ void __launch_bounds__(VT) krylov_combine_kernel(double* __restrict__ out, long long n,
+                                                            KrylovBasis B, int m, double scale) {
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    double s = __dmul_rn(B.c[0], __ldg(B.v[0] + i));
+    for (int k = 1; k < m; ++k) s = __dadd_rn(s, __dmul_rn(B.c[k], __ldg(B.v[k] + i)));
+    out[i] = __dmul_rn(scale, s);
+  }
+}
+
 int grid_for(long long n, int maxg) {
   long long g = (n + VT - 1) / VT;
   if (g > maxg) g = maxg;
@@ -350,6 +387,19 @@ int grid_for(long long n, int maxg) {
 }
 
 }  // namespace
+
+cudaError_t launch_mgs(double* w, long long n, const double* v, const double* cin,
+                       double c_host, const double* next, double* cout, RedBuf rb,
+                       cudaStream_t s) {
+  mgs_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(w, n, v, cin, c_host, next, cout, rb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B, int m,
+                                  double scale, RedBuf rb, cudaStream_t s) {
+  krylov_combine_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, n, B, m, scale);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_norm(const double* x, long long n, RedBuf rb, cudaStream_t s) {
   norm_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(x, n, rb);

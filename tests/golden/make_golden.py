@@ -212,7 +212,7 @@ def step_cases():
     return meta
 
 
-def run_case(setup, scheme):
+def run_case(setup, scheme, method="leja"):
     q = setup_state(setup)
     params = MHDParams(mu=setup.mu, eta=setup.eta, kappa=setup.kappa)
     spec = Scenario(problem="custom", case_id=setup.name, nx=setup.nx, ny=setup.ny,
@@ -226,7 +226,8 @@ def run_case(setup, scheme):
     try:
         t0 = time.perf_counter()
         rep = ref_harness.run(ref_harness.RunConfig(scenario=spec, scheme=scheme,
-                                                    tol=setup.tol, rng_seed=setup.seed))
+                                                    method=method, tol=setup.tol,
+                                                    rng_seed=setup.seed))
         wall = time.perf_counter() - t0
     finally:
         ref_harness.initialize = saved
@@ -263,14 +264,113 @@ def run_cases():
     return meta
 
 
+def krylov_cases():
+    """The Krylov baseline (krylov.py) on the fused-JVP matvec, a Krylov step and run."""
+    from xmhd.krylov import apply_phi_krylov
+    out = {}
+    meta = {"phi": [], "step": [], "run": []}
+    for tag, setup in (("kh32", sc.kh_setup(32)), ("harris32", sc.harris_setup(32))):
+        q = setup_state(setup)
+        params = MHDParams(mu=setup.mu, eta=setup.eta, kappa=setup.kappa)
+        op = mhd_op(q, setup.dx, setup.dy, params)
+        u = q.reshape(-1).copy()
+        lin = ref_lin.FrozenLinearization(op, u)
+        est = ref_lin.estimate_alpha(lin, None, rng=np.random.default_rng(0))
+        v = sc.unit_gaussian(u.size, 8)
+        out[f"{tag}__u"] = q
+        out[f"{tag}__v"] = v
+        cases = [(1, 1.0, 1e-10, 100), (1, 10.0, 1e-10, 100), (0, 10.0, 1e-8, 100),
+                 (4, 10.0, 1e-8, 100), (2, 3.0, 1e-12, 100), (1, 10.0, 1e-10, 5)]
+        if tag != "kh32":
+            cases = cases[:2]
+        for l, adt, tol, m_max in cases:
+            dt = adt / est.alpha
+            before = op.calls
+            res = apply_phi_krylov(l, lambda x: ref_lin.jvp(lin, x), v, dt, tol, m_max)
+            key = f"{tag}__kry_l{l}_a{adt:g}_t{tol:g}_m{m_max}"
+            out[key] = res.vector
+            meta["phi"].append(dict(key=key, case=tag, l=l, adt=adt, dt=dt, tol=tol,
+                                    m_max=m_max, alpha=est.alpha, iterations=res.iterations,
+                                    converged=res.converged, residual=res.residual,
+                                    rhs_calls=op.calls - before, dx=setup.dx, dy=setup.dy,
+                                    mu=setup.mu, eta=setup.eta, kappa=setup.kappa))
+    for tag, setup, scheme, dt in (("kh32_exprb43_krylov", sc.kh_setup(32), Scheme.EXPRB43,
+                                    2e-3),
+                                   ("harris32_exprb54s4_krylov", sc.harris_setup(32),
+                                    Scheme.EXPRB54S4, 0.05)):
+        q = setup_state(setup)
+        params = MHDParams(mu=setup.mu, eta=setup.eta, kappa=setup.kappa)
+        op = mhd_op(q, setup.dx, setup.dy, params)
+        u = q.reshape(-1).copy()
+        lin = ref_lin.FrozenLinearization(op, u)
+        est = ref_lin.estimate_alpha(lin, None, rng=np.random.default_rng(0))
+        before = op.calls
+        res = step(scheme, op, u, dt, method="krylov", alpha=est, tol=setup.tol, lin=lin)
+        out[f"{tag}__u"] = q
+        out[f"{tag}__new"] = res.new_state
+        meta["step"].append(dict(name=tag, scheme=scheme.value, dt=dt, tol=setup.tol,
+                                 alpha=est.alpha, error=res.error_estimate,
+                                 rhs_calls=res.rhs_calls, step_calls=op.calls - before,
+                                 phi_iterations=res.phi_iterations,
+                                 phi_applications=res.phi_applications,
+                                 converged=res.converged, dx=setup.dx, dy=setup.dy,
+                                 mu=setup.mu, eta=setup.eta, kappa=setup.kappa))
+    k = sc.kh_setup(32, t_final=0.2, name="C0_32_t0.2_krylov")
+    m, fin = run_case(k, Scheme.EXPRB43, method="krylov")
+    out["C0_32_t0.2_krylov__final"] = fin
+    meta["run"].append(m)
+    np.savez_compressed(os.path.join(HERE, "krylov_cases.npz"), **out)
+    return meta
+
+
+def wp_cases():
+    """make_reference + work_precision (harness.py:255-327) on a small KH grid."""
+    import tempfile
+    from dataclasses import replace
+    setup = sc.kh_setup(32, t_final=0.1, name="wp32")
+    q = setup_state(setup)
+    params = MHDParams(mu=setup.mu, eta=setup.eta, kappa=setup.kappa)
+    spec = Scenario(problem="custom", case_id=setup.name, nx=setup.nx, ny=setup.ny,
+                    t_final=setup.t_final, x_min=setup.x_min, x_max=setup.x_max,
+                    y_min=setup.y_min, y_max=setup.y_max, params=params, tol=setup.tol)
+    state0 = StateGrid(setup.nx, setup.ny, setup.dx, setup.dy, q.copy())
+    saved = ref_harness.initialize
+    ref_harness.initialize = lambda _spec: StateGrid(state0.nx, state0.ny, state0.dx,
+                                                      state0.dy, state0.data.copy())
+    ref_leja._coeff_cache.clear()
+    out = {}
+    try:
+        base = ref_harness.RunConfig(scenario=spec, rng_seed=setup.seed)
+        with tempfile.TemporaryDirectory() as tmp:
+            ref_path = os.path.join(tmp, "ref.chk")
+            rep = ref_harness.make_reference(base, ref_path)
+            out["reference_final"] = rep.final_state.data
+            out["reference_chk"] = np.frombuffer(open(ref_path, "rb").read(), dtype=np.uint8)
+            rows = ref_harness.work_precision(base, [1e-3, 1e-5], [Scheme.EXPRB43,
+                                                                   Scheme.EXPRB54S4],
+                                              ["leja", "krylov"], ref_path,
+                                              os.path.join(tmp, "wp.csv"))
+            series, srep = ref_harness.divb_series(replace(base, tol=1e-4), 0.02)
+    finally:
+        ref_harness.initialize = saved
+    keep = [{k: v for k, v in r.items() if k not in ("wall_seconds", "timestamp")}
+            for r in rows]
+    np.savez_compressed(os.path.join(HERE, "wp_cases.npz"), **out)
+    return dict(setup=dict(nx=setup.nx, t_final=setup.t_final, seed=setup.seed),
+                reference=dict(accepted=rep.accepted, rejected=rep.rejected,
+                               rhs_evals=rep.rhs_evals, t_reached=rep.t_reached),
+                rows=keep, divb_series=[[float(t), float(v)] for t, v in series],
+                divb_accepted=srep.accepted)
+
+
 def main():
-    which = sys.argv[1:] or ["rhs", "leja", "coeff", "step", "run"]
+    which = sys.argv[1:] or ["rhs", "leja", "coeff", "step", "run", "krylov", "wp"]
     path = os.path.join(HERE, "golden_meta.json")
     meta = json.load(open(path)) if os.path.exists(path) else {}
     meta["generator"] = "tests/golden/make_golden.py (reference xmhd %s, numpy %s)" % (
         xmhd.__version__, np.__version__)
     fns = dict(rhs=rhs_cases, leja=leja_cases, coeff=coeff_cases, step=step_cases,
-               run=run_cases)
+               run=run_cases, krylov=krylov_cases, wp=wp_cases)
     for w in which:
         t0 = time.perf_counter()
         meta[w] = fns[w]()

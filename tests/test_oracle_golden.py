@@ -135,3 +135,65 @@ def test_oracle_adaptive_run(case):
     assert rep.checksum == case["checksum"]
     assert np.array_equal(rep.final, golden_io.arrays("run_cases")[f"{case['name']}__final"])
     assert rep.max_divb == case["max_divb"]
+
+
+# ---- Krylov baseline (krylov.py) -------------------------------------------------
+
+from oracle import krylov_np as kr  # noqa: E402
+
+
+@pytest.mark.parametrize("case", golden_io.meta()["krylov"]["phi"], ids=lambda m: m["key"])
+def test_oracle_krylov_phi(case):
+    g = golden_io.arrays("krylov_cases")
+    tag = case["case"]
+    op, lin = _lin(g, case, tag)
+    est = lj.power_alpha(lin, None, rng=np.random.default_rng(0))
+    assert est.alpha == case["alpha"]
+    calls = op.calls
+    res = kr.phi_krylov(case["l"], lambda x: lj.fd_jvp(lin, x), g[f"{tag}__v"], case["dt"],
+                        case["tol"], case["m_max"])
+    assert (res.iterations, res.converged) == (case["iterations"], case["converged"])
+    assert op.calls - calls == case["rhs_calls"]
+    assert res.residual == case["residual"]
+    assert np.array_equal(res.vector, g[case["key"]])
+
+
+@pytest.mark.parametrize("case", golden_io.meta()["krylov"]["step"], ids=lambda m: m["name"])
+def test_oracle_krylov_step(case):
+    g = golden_io.arrays("krylov_cases")
+    tag = case["name"]
+    op, lin = _lin(g, case, tag)
+    est = lj.power_alpha(lin, None, rng=np.random.default_rng(0))
+    res = st.one_step(case["scheme"], op, lin.u, case["dt"], est, case["tol"], lin,
+                      lj.CoeffCache(), method="krylov")
+    assert res.converged == case["converged"]
+    assert res.phi_iterations == case["phi_iterations"]
+    assert res.error_estimate == case["error"]
+    assert np.array_equal(res.new_state, g[f"{tag}__new"])
+
+
+def test_oracle_krylov_errors():
+    with pytest.raises(ValueError):
+        kr.phi_krylov(1, lambda x: x, np.ones(4), 0.1, 0.0)
+    with pytest.raises(ValueError):
+        kr.phi_krylov(1, lambda x: x, np.ones(4), 0.1, 1e-8, m_max=201)
+    with pytest.raises(ValueError):
+        kr.phi_krylov(1, lambda x: x, np.zeros(4), 0.1, 1e-8)
+    # J = -I: exact after one vector (happy breakdown), phi_1(-dt) v
+    dt = 0.3
+    res = kr.phi_krylov(1, lambda x: -x, np.arange(1.0, 5.0), dt, 1e-12)
+    assert res.converged and res.iterations == 1 and res.residual == 0.0
+    assert np.allclose(res.vector, np.arange(1.0, 5.0) * (1 - np.exp(-dt)) / dt, rtol=1e-13)
+
+
+@pytest.mark.parametrize("case", golden_io.meta()["krylov"]["run"], ids=lambda m: m["name"])
+def test_oracle_krylov_run(case):
+    from paper_2108_13622_b200 import scenarios as sc
+    setup = sc.kh_setup(case["nx"], t_final=case["t_final"])
+    q = sc.initial_fields(setup)
+    rep = st.run(q, setup.dx, setup.dy, setup.mu, setup.eta, setup.kappa,
+                 case["scheme"], case["tol"], case["t_final"], cache=lj.CoeffCache(),
+                 method="krylov")
+    assert (rep.accepted, rep.rejected, rep.rhs_evals) == \
+        (case["accepted"], case["rejected"], case["rhs_evals"])
+    assert rep.checksum == case["checksum"]
