@@ -279,6 +279,17 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
     return fail(XMHD_CUDA_ERROR, std::string("device query: ") + cudaGetErrorString(e));
   }
   stencil_plan(g, c->nsm, c->units_x, c->nunits, c->seg_rows, c->grid);
+  if (const char* seg = std::getenv("XMHD_SEG_ROWS")) {
+    // testing knob: another work decomposition = another (equally valid)
+    // summation order of the norm partials; used to measure the rounding floor
+    const int s = std::atoi(seg);
+    if (s > 0 && s < ny) {
+      const int slots = c->grid;   // persistent grid of the automatic plan
+      c->seg_rows = s;
+      c->nunits = c->units_x * ((ny + s - 1) / s);
+      c->grid = c->nunits < slots ? c->nunits : slots;
+    }
+  }
   c->red_grid = 4 * c->nsm;
   const int slots = (c->red_grid > c->grid ? c->red_grid : c->grid) * 8 + 64;
   if ((e = cudaMalloc(&c->partials, sizeof(double) * slots)) != cudaSuccess ||
