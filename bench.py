@@ -53,6 +53,20 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(n, local_cells):
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture
+    (profiles/r01_leja_traffic.json), when it was taken on this grid and layout."""
+    path = os.path.join(REPO, "profiles", "r01_leja_traffic.json")
+    try:
+        rec = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    if rec.get("grid") != n or local_cells != n * n:
+        return None
+    return {"bytes": rec["dram_bytes_read"] + rec["dram_bytes_write"],
+            "algorithmic_bytes": rec["algorithmic_bytes"], "source": rec["source"]}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
@@ -301,13 +315,9 @@ def main():
     # ---- end to end through the public API with pinned host buffers
     u_pin = torch.from_numpy(q_loc.reshape(-1)).pin_memory()
     v_pin = torch.from_numpy(v_loc.reshape(-1)).pin_memory()
-    e2e_iters = 0
-    barrier()
-    t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
+
+    def e2e_step():
+        its = 0
         leja._coeff_cache.clear()
         op_e = xb.RhsOperator(mhd)
         lin_e = xb.FrozenLinearization(op_e, u_pin)            # H2D u, F(u)
@@ -316,7 +326,21 @@ def main():
             res = xb.apply_phi_leja(1, xb.JacobianAction(lin_e), v_pin, dt,
                                     xb.shift_and_scale(alpha * dt), LEJA_TOL)   # H2D v, D2H p
             assert isinstance(res.vector, np.ndarray)
-            e2e_iters += res.iterations
+            its += res.iterations
+        return its
+
+    # warm-up of the host side too: the first steps page-lock the result buffers
+    # (torch's caching host allocator), which later steps reuse
+    for _ in range(args.warmup):
+        e2e_step()
+    e2e_iters = 0
+    barrier()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_iters += e2e_step()
     e1.record(stream)
     barrier()
     e2e_ms = maxed(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)))
@@ -354,7 +378,7 @@ def main():
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
                          "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL_ITER,
-                         "traffic": None},
+                         "traffic": ncu_traffic(args.n, local_cells)},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),

@@ -142,3 +142,37 @@ def test_strip_adaptive_run_vs_reference(nranks):
     final = golden_io.arrays("run_cases")[case["name"] + "__final"]
     assert rel(rep.final_state.data, final) <= 1e-8
     assert abs(rep.max_divb - case["max_divb"]) <= 1e-12 + 1e-6 * case["max_divb"]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_strip_krylov_matches_single_domain(nranks):
+    """The Krylov arm on y-strips: every MGS coefficient reduced over the ranks."""
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import scenarios as sc, strips
+    s, q, params = _problem(48)
+    v = sc.unit_gaussian(q.size, 9).reshape(q.shape)
+    geo = xb.StateGrid(s.nx, s.ny, s.dx, s.dy, torch.from_numpy(q).cuda())
+    lin = xb.FrozenLinearization(xb.RhsOperator(xb.MhdRhs(geo, params)), geo.flat())
+    alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    dt = 5.0 / alpha
+    ref = xb.apply_phi_krylov(1, xb.JacobianAction(lin), torch.from_numpy(v).cuda().reshape(-1),
+                              dt, 1e-10)
+
+    def rank(comm):
+        mhd = strips.StripMhd(xb.StateGrid(s.nx, s.ny, s.dx, s.dy, None), params, comm)
+        prev = xb.linearize._ops.set_reducer(strips.Reducer(comm, torch.device("cuda")))
+        try:
+            lay = mhd.layout
+            u = torch.from_numpy(np.ascontiguousarray(lay.local_rows(q))).cuda().reshape(-1)
+            slin = xb.FrozenLinearization(xb.RhsOperator(mhd), u)
+            vl = torch.from_numpy(np.ascontiguousarray(lay.local_rows(v))).cuda().reshape(-1)
+            res = xb.apply_phi_krylov(1, xb.JacobianAction(slin), vl, dt, 1e-10)
+            return lay.y0, lay.ny, res.iterations, res.converged, res.vector.cpu().numpy()
+        finally:
+            xb.linearize._ops.set_reducer(prev)
+
+    results = run_ranks(nranks, rank)
+    full = np.concatenate([r[4].reshape(8, r[1], s.nx) for r in results], axis=1)
+    for r in results:
+        assert (r[2], r[3]) == (ref.iterations, ref.converged)
+    assert rel(full.reshape(-1), ref.vector) <= 1e-11
