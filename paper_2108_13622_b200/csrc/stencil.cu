@@ -37,63 +37,10 @@
 #include <climits>
 #include "kernels.h"
 
-#ifndef XB_EPI_PREFETCH
-#define XB_EPI_PREFETCH 0
-#endif
-#ifndef XB_GY_SMEM
-#define XB_GY_SMEM 0
-#endif
-// Variants kept for A/B measurement (all measured slower on B200 at 2048^2 /
-// 4096^2, see profiles/): epilogue operands prefetched to L2 only (no change),
-// GY ring in shared memory (-35%: smaller L1), L1 cache hints (-10%).
-#ifndef XB_CACHE_HINTS
-#define XB_CACHE_HINTS 0
-#endif
-// Variant: shared-memory rings hold field pairs as double2 (16-byte LDS/STS,
-// half the shared-memory instructions, same bytes).  Measured neutral on B200
-// (0.3488 vs 0.3461 ms at 2048^2): shared-memory issue is not the limiter.
-#ifndef XB_SMEM_V2
-#define XB_SMEM_V2 0
-#endif
-#if XB_SMEM_V2 && XB_GY_SMEM
-#error "XB_SMEM_V2 requires XB_GY_SMEM=0"
-#endif
-
-namespace xb {
-namespace {
-// L1 policy of the streamed operands.  u, F(u) and p are read once per
-// launch: do not let them displace the rows of y, which every thread reads
-// twice (as the JVP direction of row r, and again two rows later in the
-// Newton-update epilogue).
-__device__ __forceinline__ double ld_stream(const double* p) {
-#if XB_CACHE_HINTS
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double ld_keep(const double* p) {
-#if XB_CACHE_HINTS
-  double v;
-  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double ld_reuse(const double* p) {
-#if XB_CACHE_HINTS
-  double v;
-  asm("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
-}
-}  // namespace
-}  // namespace xb
+// Variants measured and dropped: epilogue operands staged by
+// cp.async (-43%: the larger shared-memory carve-out starves L1), epilogue
+// prefetch to L2 only (neutral), GY ring in shared memory (-35%), L1 cache
+// hints (-10%), double2 shared-memory rings (neutral).
 
 namespace xb {
 
@@ -104,29 +51,6 @@ __host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; } 
 __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }   // skip BY
 
 constexpr int RING_PD = 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
-#if XB_GY_SMEM
-constexpr int RING_GY = 3;   // own-column diffusive y-fluxes of rows r-1..r-3
-#else
-constexpr int RING_GY = 0;
-#endif
-// double2 slots per ring row (odd counts padded)
-constexpr int NPD2 = (NPD + 1) / 2, NFX2 = (NFX + 1) / 2, NFY2 = (NFY + 1) / 2, NG2 = (NG + 1) / 2;
-
-template <int N>
-__device__ __forceinline__ void st_pairs(double2* row, const double* v) {
-#pragma unroll
-  for (int k = 0; k < (N + 1) / 2; ++k)
-    row[k * SW] = make_double2(v[2 * k], (2 * k + 1 < N) ? v[2 * k + 1] : 0.0);
-}
-template <int N>
-__device__ __forceinline__ void ld_pairs(const double2* row, double* v) {
-#pragma unroll
-  for (int k = 0; k < (N + 1) / 2; ++k) {
-    const double2 p = row[k * SW];
-    v[2 * k] = p.x;
-    if (2 * k + 1 < N) v[2 * k + 1] = p.y;
-  }
-}
 
 // Source of one ghost-extended row.  Element offsets are 32-bit unsigned: a
 // per-GPU vector of 8*nx*ny < 2^32 doubles (34 GB) covers every grid that fits
@@ -217,24 +141,12 @@ __device__ __forceinline__ double sum_partials(const double* p, int nblk, int st
 template <int MODE, int KX, int KY>
 __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
   extern __shared__ __align__(16) double smem[];
-#if XB_SMEM_V2
-  double2* const s2 = reinterpret_cast<double2*>(smem);
-  double2 (*pd2)[NPD2][SW] = reinterpret_cast<double2 (*)[NPD2][SW]>(s2);
-  double2 (*fx2s)[NFX2][SW] = reinterpret_cast<double2 (*)[NFX2][SW]>(s2 + RING_PD * NPD2 * SW);
-  double2 (*fy2s)[NFY2][SW] =
-      reinterpret_cast<double2 (*)[NFY2][SW]>(s2 + (RING_PD * NPD2 + RING_FX * NFX2) * SW);
-  double2 (*gx2s)[NG2][SW] = reinterpret_cast<double2 (*)[NG2][SW]>(
-      s2 + (RING_PD * NPD2 + RING_FX * NFX2 + RING_FY * NFY2) * SW);
-#endif
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
   double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
   double (*fys)[NFY][SW] =
       reinterpret_cast<double (*)[NFY][SW]>(smem + (RING_PD * NPD + RING_FX * NFX) * SW);
   double (*gxs)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(
       smem + (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY) * SW);
-  double (*gys)[NG][SW] = reinterpret_cast<double (*)[NG][SW]>(
-      smem + (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG) * SW);
-  (void)gys;
   __shared__ double red[SW / 32];
   __shared__ int am_last;
 
@@ -299,11 +211,9 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       const int tl = max(t - 1, 0), tr = min(t + 1, SW - 1);
       const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
 
-#if !XB_GY_SMEM
       double gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
-#endif
       int s3 = 0;  // s % 3 (GY ring)
       // own-column differentiated primitives of rows r-1 and r-2 (registers);
       // shared memory holds only the row x-neighbours read (PD of row r-1)
@@ -319,8 +229,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         nflip = rs.flip;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          nu[f] = ld_stream(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-          if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+          nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+          if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
         }
       }
 
@@ -334,32 +244,17 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
         // epilogue operands of output row r-2: issue now, consume in P3
         double efu[NF], ey[NF], ep[NF];
-#if XB_EPI_PREFETCH
-        // variant: only pull the lines into L2 now; load them at P3 (fewer live registers)
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
             const unsigned i = obase + (unsigned)f * plane;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
+            efu[f] = __ldg(a.fu + i);
             if (MODE == MODE_LEJA) {
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
+              ey[f] = __ldg(dir + i);
+              ep[f] = __ldg(pin + i);
             }
           }
         }
-#else
-        if (MODE != MODE_RHS && out_row) {
-#pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const unsigned i = obase + (unsigned)f * plane;
-            efu[f] = ld_stream(a.fu + i);
-            if (MODE == MODE_LEJA) {
-              ey[f] = ld_reuse(dir + i);
-              ep[f] = ld_stream(pin + i);
-            }
-          }
-        }
-#endif
 
         // ---- P1: state at (r, cg) from the prefetch registers
         double pn[NPD];
@@ -375,8 +270,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
-              nu[f] = ld_stream(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-              if (MODE != MODE_RHS) nd[f] = ld_keep(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+              nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
             }
           }
           Prim p;
@@ -390,13 +285,6 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           pn[PD_T] = p.temp;
           pn[PD_B2] = p.b2;
           double fv[NFX];
-#if XB_SMEM_V2
-          st_pairs<NPD>(&pd2[s & 1][0][t], pn);
-          flux_x(p, g, fv);
-          st_pairs<NFX>(&fx2s[s4][0][t], fv);
-          flux_y(p, g, fv);
-          st_pairs<NFY>(&fy2s[s4][0][t], fv);
-#else
 #pragma unroll
           for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
           flux_x(p, g, fv);
@@ -405,7 +293,6 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           flux_y(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
-#endif
         }
         __syncthreads();
 
@@ -415,24 +302,15 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
         if (g.diffusive && s >= 2) {
           double xl[NPD], xr[NPD];   // PD of row r-1 at t-1, t+1
-#if XB_SMEM_V2
-          ld_pairs<NPD>(&pd2[(s + 1) & 1][0][tl], xl);
-          ld_pairs<NPD>(&pd2[(s + 1) & 1][0][tr], xr);
-#else
 #pragma unroll
           for (int k = 0; k < NPD; ++k) {
             xl[k] = pd[(s + 1) & 1][k][tl];
             xr[k] = pd[(s + 1) & 1][k][tr];
           }
-#endif
           double gxv[NG];
           diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyn);
-#if XB_SMEM_V2
-          st_pairs<NG>(&gx2s[(s + 1) & 1][0][t], gxv);
-#else
 #pragma unroll
           for (int k = 0; k < NG; ++k) gxs[(s + 1) & 1][k][t] = gxv[k];
-#endif
         }
 #pragma unroll
         for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
@@ -440,19 +318,6 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 
         // ---- P3: output row o = r-2
         if (out_row) {
-#if XB_EPI_PREFETCH
-          if (MODE != MODE_RHS) {
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const unsigned i = obase + (unsigned)f * plane;
-              efu[f] = ld_stream(a.fu + i);
-              if (MODE == MODE_LEJA) {
-                ey[f] = ld_reuse(dir + i);
-                ep[f] = ld_stream(pin + i);
-              }
-            }
-          }
-#endif
           const int fx2 = (s4 + 2) & 3;   // FX / FY slot of row r-2 (s-2 mod 4)
           const int fy1 = (s4 + 3) & 3;   // FY slot of row r-1
           const int fy3 = (s4 + 1) & 3;   // FY slot of row r-3
@@ -461,13 +326,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           // ideal part: out = -(dFX/2dx); out -= dFY/2dy       (mhd.py:177-178)
           {
             double a[NFX], b[NFX];
-#if XB_SMEM_V2
-            ld_pairs<NFX>(&fx2s[fx2][0][tr], a);
-            ld_pairs<NFX>(&fx2s[fx2][0][tl], b);
-#else
 #pragma unroll
             for (int k = 0; k < NFX; ++k) { a[k] = fxs[fx2][k][tr]; b[k] = fxs[fx2][k][tl]; }
-#endif
 #pragma unroll
             for (int k = 0; k < NFX; ++k)
               F[fx_field(k)] = -qdiv<KX>(__dsub_rn(a[k], b[k]), g.h2x);
@@ -475,13 +335,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           F[BX] = -0.0;
           {
             double a[NFY], b[NFY];
-#if XB_SMEM_V2
-            ld_pairs<NFY>(&fy2s[fy1][0][t], a);
-            ld_pairs<NFY>(&fy2s[fy3][0][t], b);
-#else
 #pragma unroll
             for (int k = 0; k < NFY; ++k) { a[k] = fys[fy1][k][t]; b[k] = fys[fy3][k][t]; }
-#endif
 #pragma unroll
             for (int k = 0; k < NFY; ++k) {
               const int f = fy_field(k);
@@ -492,13 +347,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           if (g.diffusive) {
             // out += dGX/2dx; out += dGY/2dy                 (mhd.py:222-223)
             double gr[NG], gl[NG];
-#if XB_SMEM_V2
-            ld_pairs<NG>(&gx2s[gs][0][tr], gr);
-            ld_pairs<NG>(&gx2s[gs][0][tl], gl);
-#else
 #pragma unroll
             for (int k = 0; k < NG; ++k) { gr[k] = gxs[gs][k][tr]; gl[k] = gxs[gs][k][tl]; }
-#endif
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BX] = __dadd_rn(F[BX], 0.0);
             F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gr[0], gl[0]), g.h2x));
@@ -509,14 +359,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
             F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gr[5], gl[5]), g.h2x));
             F[RHO] = __dadd_rn(F[RHO], 0.0);
             F[BY] = __dadd_rn(F[BY], 0.0);
-#if XB_GY_SMEM
-            double gy3[NG];   // GY of row r-3: written two steps ago (slot (s+1) % 3)
-            const int g3 = (s3 == 2) ? 0 : s3 + 1;
-#pragma unroll
-            for (int k = 0; k < NG; ++k) gy3[k] = gys[g3][k][t];
-#else
             const double* gy3 = gy2;
-#endif
             F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gyn[0], gy3[0]), g.h2y));
             F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gyn[1], gy3[1]), g.h2y));
             F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gyn[2], gy3[2]), g.h2y));
@@ -559,11 +402,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
         }
 
 #pragma unroll
-#if XB_GY_SMEM
-        for (int k = 0; k < NG; ++k) gys[s3][k][t] = gyn[k];
-#else
         for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
-#endif
         s3 = (s3 == 2) ? 0 : s3 + 1;
         s4 = (s4 + 1) & 3;
       }
@@ -609,12 +448,8 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
 }
 
 size_t stencil_smem_bytes() {
-#if XB_SMEM_V2
-  return sizeof(double2) * (size_t)SW *
-         (RING_PD * NPD2 + RING_FX * NFX2 + RING_FY * NFY2 + RING_GX * NG2);
-#endif
   return sizeof(double) * (size_t)SW *
-         (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG + RING_GY * NG);
+         (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG);
 }
 
 // Work decomposition: column strips of SOUT outputs x y-segments; the
