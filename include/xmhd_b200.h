@@ -43,6 +43,7 @@ extern "C" {
 #define XMHD_LEJA_RHS_NONFINITE 3 /* matvec hit a non-finite RHS: caller raises            */
 #define XMHD_LEJA_NEED_COEFFS 4   /* grow the coefficient chunk (leja.py:128-130)           */
 #define XMHD_LEJA_EXHAUSTED 5     /* 499 terms, not converged (leja.py:149-150)            */
+#define XMHD_LEJA_PEER_TIMEOUT 6  /* y-strips over peer memory: a rank never posted its sums */
 
 typedef struct xmhd_ctx xmhd_ctx;
 
@@ -166,6 +167,42 @@ int xmhd_time_leja_iterations(xmhd_ctx* ctx, const double* u, const double* fu, 
                               const double* v, double dt, double q, double theta,
                               const double* xi, const double* coeffs500, int n_iter,
                               double* ms_per_iter);
+
+/* ---- y-strips over peer memory (one NVLink / NVSwitch node, CUDA IPC) ----
+ * Replaces the per-term halo exchange + allreduce of the strip driver (the
+ * NCCL path above) inside the fused iteration kernel: it stores the boundary
+ * rows of y' into the neighbours' ghost-row buffers and all-reduces its
+ * [sum y'^2, sum p'^2, bad] through per-rank boards in peer memory, so a
+ * Newton term is one kernel launch on every rank and no host call.
+ *
+ * Setup (once per strip context): xmhd_p2p_alloc returns this rank's 64-byte
+ * CUDA IPC handle; the caller all-gathers the handles (any transport) and
+ * calls xmhd_p2p_connect with all of them.  periodic: the strips form a ring
+ * in y; otherwise the end ranks build mirrored ghost rows (reflecting walls).
+ * The state's ghost rows are still set with xmhd_set_halo (once per call). */
+int xmhd_p2p_alloc(xmhd_ctx* ctx, void* ipc_handle_out);
+int xmhd_p2p_connect(xmhd_ctx* ctx, int rank, int nranks, const void* ipc_handles,
+                     int periodic);
+/* Connectivity probe: write `value` into every rank's board (no waiting) /
+ * read this rank's board: out[4*q] = value written by rank q, out[4*q+1] = q. */
+int xmhd_p2p_probe(xmhd_ctx* ctx, double value);
+int xmhd_p2p_read_board(xmhd_ctx* ctx, double* out /* 32 doubles */);
+/* One phi-action on the strips: start (y0 = v, p0 = c0*v, global ||v||, ghost
+ * rows of y0), then run until the status leaves RUNNING; NEED_COEFFS:
+ * xmhd_leja_set_coeffs + xmhd_leja_p2p_run again.  Results: xmhd_leja_result. */
+int xmhd_leja_p2p_start(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                        const double* v, double dt, double q, double theta, double tol,
+                        const double* xi, const double* coeffs, int ncoef);
+int xmhd_leja_p2p_run(xmhd_ctx* ctx, xmhd_leja_state* st);
+/* Test driver: nranks strip contexts on ONE GPU sharing one stream, wired to
+ * each other's regions directly, every Newton term ONE cooperative launch
+ * over all ranks' blocks (ranks that wait on each other must be co-resident). */
+int xmhd_p2p_connect_local(xmhd_ctx* const* ctxs, int nranks, int periodic);
+int xmhd_leja_p2p_emul_start(xmhd_ctx* const* ctxs, int nranks, const double* const* u,
+                             const double* const* fu, double unorm, const double* const* v,
+                             double dt, double q, double theta, double tol, const double* xi,
+                             const double* coeffs, int ncoef);
+int xmhd_leja_p2p_emul_run(xmhd_ctx* const* ctxs, int nranks, xmhd_leja_state* st);
 
 /* ---- Krylov baseline (replaces the NumPy Arnoldi loop of krylov.py:34-84) ----
  * The paper's Leja-vs-Krylov comparison arm; the Hessenberg matrix and its

@@ -16,7 +16,7 @@ from paper_2108_13622_b200 import build as _build
 OK, NONFINITE, BADARG, CUDA_ERROR = 0, 1, 2, 3
 BC_PERIODIC, BC_REFLECTING, BC_HALO = 0, 1, 2
 (LEJA_RUNNING, LEJA_CONVERGED, LEJA_BLOWUP, LEJA_RHS_NONFINITE, LEJA_NEED_COEFFS,
- LEJA_EXHAUSTED) = range(6)
+ LEJA_EXHAUSTED, LEJA_PEER_TIMEOUT) = range(7)
 
 
 class NativeUnavailable(RuntimeError):
@@ -83,6 +83,17 @@ _SIGS = {
     "xmhd_krylov_mgs": (_I, [_P, ctypes.POINTER(_P), _I, _P, _L, _PD, _PD]),
     "xmhd_mgs_update": (_I, [_P, _P, _L, _P, _D, _P, _PD]),
     "xmhd_krylov_combine": (_I, [_P, ctypes.POINTER(_P), _PD, _I, _D, _L, _P]),
+    "xmhd_p2p_alloc": (_I, [_P, _P]),
+    "xmhd_p2p_connect": (_I, [_P, _I, _I, _P, _I]),
+    "xmhd_p2p_connect_local": (_I, [ctypes.POINTER(_P), _I, _I]),
+    "xmhd_p2p_probe": (_I, [_P, _D]),
+    "xmhd_p2p_read_board": (_I, [_P, _PD]),
+    "xmhd_leja_p2p_start": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I]),
+    "xmhd_leja_p2p_run": (_I, [_P, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_p2p_emul_start": (_I, [ctypes.POINTER(_P), _I, ctypes.POINTER(_P),
+                                      ctypes.POINTER(_P), _D, ctypes.POINTER(_P), _D, _D, _D,
+                                      _D, _PD, _PD, _I]),
+    "xmhd_leja_p2p_emul_run": (_I, [ctypes.POINTER(_P), _I, ctypes.POINTER(LejaState)]),
 }
 
 EXPORTED = tuple(_SIGS)

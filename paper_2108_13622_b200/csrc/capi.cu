@@ -38,6 +38,14 @@ struct xmhd_ctx {
   long long gen_n = 0;         // vector length of the current generic Leja call
   const double* leja_u = nullptr;
   const double* leja_fu = nullptr;
+  // y-strips over peer memory (P2PArgs): own region [ghost rows x 2 parities,
+  // board, flags], the peers' regions mapped through CUDA IPC
+  char* p2p_base = nullptr;
+  char* p2p_peer[P2P_MAX] = {};
+  P2PArgs p2p;
+  bool p2p_ready = false;
+  unsigned long long p2p_epoch = 0;   // last exchange epoch (continues across calls)
+  StencilArgs* emul_args = nullptr;   // device [P2P_MAX] (one-GPU emulation driver)
   double* kry_d = nullptr;     // [512] MGS coefficient slots (Krylov baseline)
   double* kry_h = nullptr;     // pinned [512]
   long long launches = 0;
@@ -155,7 +163,7 @@ int sync_ctl(xmhd_ctx* c) {
 // Device-resident fused Leja loop: launch iterations in growing batches; each
 // kernel exits immediately once the control block left RUNNING, so the host
 // only synchronises once per batch.
-int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
+int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   StencilArgs a = base_args(c);
   a.u = c->leja_u;
   a.fu = c->leja_fu;
@@ -166,6 +174,7 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
   a.coeffs = c->coeffs_d;
   a.xi = c->xi_d;
   a.ctl = c->ctl;
+  if (peer) a.p2p = c->p2p;
   // first batch: the caller's degree hint (xmhd_leja_hint; the host keys it by
   // phi order and interval scale), so most calls need a single sync
   const int done = c->ctl_h->iters;
@@ -174,7 +183,8 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
   if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
     for (int k = 0; k < batch; ++k) {
-      CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+      if (peer) CK(launch_leja_peer(a, c->grid, c->stream));
+      else CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
       c->launches++;
     }
     int rc = sync_ctl(c);
@@ -183,6 +193,11 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st) {
     batch = batch * 2 < c->batch_max ? batch * 2 : c->batch_max;
   }
   fill_state(*c->ctl_h, st);
+  if (peer) {
+    c->p2p_epoch = c->ctl_h->epoch;
+    if (c->ctl_h->status == LJ_PEER_TIMEOUT)
+      return fail(XMHD_CUDA_ERROR, "peer-memory exchange timed out (a rank stopped)");
+  }
   return XMHD_OK;
 }
 
@@ -211,6 +226,7 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.tol = tol;
   h.thetad = make_divisor(theta, c->force_ieee);
   h.force_ieee = c->force_ieee ? 1 : 0;
+  h.epoch = c->p2p_epoch;
   *c->ctl_h = h;
   CK(cudaMemcpyAsync(c->ctl, c->ctl_h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
@@ -331,6 +347,10 @@ int xmhd_destroy(xmhd_ctx* c) {
   cudaFreeHost(c->h_int);
   cudaFree(c->kry_d);
   cudaFreeHost(c->kry_h);
+  for (int q = 0; q < P2P_MAX; ++q)
+    if (c->p2p_peer[q]) cudaIpcCloseMemHandle(c->p2p_peer[q]);
+  cudaFree(c->p2p_base);
+  cudaFree(c->emul_args);
   delete c;
   return XMHD_OK;
 }
@@ -793,6 +813,254 @@ int xmhd_leja_set_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
   c->ctl_h->status = LJ_RUNNING;
   CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  return XMHD_OK;
+}
+
+// ---- y-strips over peer memory (NVLink / NVSwitch, CUDA IPC) -------------
+
+namespace {
+
+struct P2PLayout {
+  size_t halo[2][2];   // [parity][lo, hi] byte offsets of [NF][2][nx] ghost rows
+  size_t board, flag, bytes;
+};
+
+P2PLayout p2p_layout(int nx) {
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  const size_t hb = al(sizeof(double) * NF * 2 * (size_t)nx);
+  P2PLayout L;
+  for (int par = 0; par < 2; ++par)
+    for (int side = 0; side < 2; ++side) L.halo[par][side] = hb * (par * 2 + side);
+  L.board = 4 * hb;
+  L.flag = L.board + al(sizeof(double) * 2 * P2P_MAX * 4);
+  L.bytes = L.flag + al(sizeof(unsigned long long) * 2 * P2P_MAX);
+  return L;
+}
+
+// Neighbours of `rank` on the strip chain (a ring when periodic in y); a
+// missing neighbour is a reflecting wall whose ghost rows the rank builds itself.
+void p2p_wire(xmhd_ctx* c, int rank, int nranks, char* const* bases, int periodic) {
+  const P2PLayout L = p2p_layout(c->g.nx);
+  P2PArgs& x = c->p2p;
+  std::memset(&x, 0, sizeof(x));
+  x.rank = rank;
+  x.nranks = nranks;
+  const int below = rank > 0 ? rank - 1 : (periodic ? nranks - 1 : -1);
+  const int above = rank < nranks - 1 ? rank + 1 : (periodic ? 0 : -1);
+  for (int par = 0; par < 2; ++par) {
+    double* own_lo = (double*)(bases[rank] + L.halo[par][0]);
+    double* own_hi = (double*)(bases[rank] + L.halo[par][1]);
+    x.halo_lo_dir[par] = own_lo;
+    x.halo_hi_dir[par] = own_hi;
+    // my rows 0, 1 are the rows ny, ny+1 of the rank below (its "hi" ghost rows)
+    x.dst_lo[par] = below >= 0 ? (double*)(bases[below] + L.halo[par][1]) : own_lo;
+    x.dst_hi[par] = above >= 0 ? (double*)(bases[above] + L.halo[par][0]) : own_hi;
+  }
+  x.mirror_lo = below < 0;
+  x.mirror_hi = above < 0;
+  for (int q = 0; q < nranks; ++q) {
+    x.board[q] = (double*)(bases[q] + L.board);
+    x.flag[q] = (unsigned long long*)(bases[q] + L.flag);
+  }
+  c->p2p_ready = true;
+}
+
+// Ghost rows of y0 (parity 0) into the neighbours / my mirror rows.
+int p2p_push_y0(xmhd_ctx* c) {
+  const P2PArgs& x = c->p2p;
+  CK(launch_leja_pack_halo(c->ctl, c->ybuf[0], c->ybuf[1], c->g.nx, c->g.ny,
+                           x.mirror_lo ? nullptr : x.dst_lo[0],
+                           x.mirror_hi ? nullptr : x.dst_hi[0],
+                           x.mirror_lo ? x.dst_lo[0] : nullptr,
+                           x.mirror_hi ? x.dst_hi[0] : nullptr, x.mirror_lo, x.mirror_hi,
+                           c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int p2p_check(xmhd_ctx* c) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  if (c->g.bcy != BC_HALO) return fail(XMHD_BADARG, "peer transport needs a y-strip context");
+  if (!c->p2p_ready) return fail(XMHD_BADARG, "peer transport not connected");
+  if (!c->g.halo_lo) return fail(XMHD_BADARG, "state halo rows not set");
+  return XMHD_OK;
+}
+
+}  // namespace
+
+int xmhd_p2p_alloc(xmhd_ctx* c, void* handle_out) {
+  if (!c || !handle_out) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy != BC_HALO) return fail(XMHD_BADARG, "peer transport needs a y-strip context");
+  if (!c->p2p_base) {
+    const P2PLayout L = p2p_layout(c->g.nx);
+    CK(cudaMalloc((void**)&c->p2p_base, L.bytes));
+    CK(cudaMemset(c->p2p_base, 0, L.bytes));
+    CK(cudaDeviceSynchronize());
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->p2p_base));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return XMHD_OK;
+}
+
+int xmhd_p2p_connect(xmhd_ctx* c, int rank, int nranks, const void* handles, int periodic) {
+  if (!c || !handles) return fail(XMHD_BADARG, "null arg");
+  if (nranks < 2 || nranks > P2P_MAX || rank < 0 || rank >= nranks)
+    return fail(XMHD_BADARG, "rank / nranks out of range (2..8 ranks per node)");
+  if (!c->p2p_base) return fail(XMHD_BADARG, "xmhd_p2p_alloc first");
+  char* bases[P2P_MAX] = {};
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) {
+      bases[q] = c->p2p_base;
+      continue;
+    }
+    if (!c->p2p_peer[q]) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, (const char*)handles + q * sizeof(cudaIpcMemHandle_t), sizeof(h));
+      CK(cudaIpcOpenMemHandle((void**)&c->p2p_peer[q], h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    bases[q] = c->p2p_peer[q];
+  }
+  p2p_wire(c, rank, nranks, bases, periodic);
+  return XMHD_OK;
+}
+
+int xmhd_p2p_connect_local(xmhd_ctx* const* ctxs, int nranks, int periodic) {
+  if (!ctxs || nranks < 2 || nranks > P2P_MAX) return fail(XMHD_BADARG, "bad ranks");
+  char* bases[P2P_MAX] = {};
+  for (int q = 0; q < nranks; ++q) {
+    if (!ctxs[q] || !ctxs[q]->p2p_base) return fail(XMHD_BADARG, "xmhd_p2p_alloc every rank first");
+    if (ctxs[q]->g.nx != ctxs[0]->g.nx) return fail(XMHD_BADARG, "ranks differ in nx");
+    bases[q] = ctxs[q]->p2p_base;
+  }
+  for (int r = 0; r < nranks; ++r) p2p_wire(ctxs[r], r, nranks, bases, periodic);
+  return XMHD_OK;
+}
+
+int xmhd_p2p_probe(xmhd_ctx* c, double value) {
+  if (!c || !c->p2p_ready) return fail(XMHD_BADARG, "peer transport not connected");
+  CK(launch_p2p_probe(c->p2p, value, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return XMHD_OK;
+}
+
+int xmhd_p2p_read_board(xmhd_ctx* c, double* out) {
+  if (!c || !out || !c->p2p_base) return fail(XMHD_BADARG, "null arg");
+  const P2PLayout L = p2p_layout(c->g.nx);
+  CK(cudaMemcpy(out, c->p2p_base + L.board, sizeof(double) * P2P_MAX * 4,
+                cudaMemcpyDeviceToHost));
+  return XMHD_OK;
+}
+
+int xmhd_leja_p2p_start(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                        const double* v, double dt, double q, double theta, double tol,
+                        const double* xi, const double* coeffs, int ncoef) {
+  int rc = p2p_check(c);
+  if (rc) return rc;
+  if (!u || !fu || !v || !xi || !coeffs) return fail(XMHD_BADARG, "null arg");
+  c->leja_u = u;
+  c->leja_fu = fu;
+  double* sums = c->result + 8;
+  rc = leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef, sums);
+  if (rc) return rc;
+  rc = p2p_push_y0(c);
+  if (rc) return rc;
+  StencilArgs a = leja_args(c);
+  a.ext_sums = sums;
+  a.p2p = c->p2p;
+  CK(launch_leja_p2p_init(a, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_p2p_run(xmhd_ctx* c, xmhd_leja_state* st) {
+  int rc = p2p_check(c);
+  if (rc) return rc;
+  return leja_run(c, st, true);
+}
+
+// ---- the same driver with P ranks emulated on one GPU (tests) -------------
+
+namespace {
+
+int emul_args(xmhd_ctx* const* ctxs, int nranks, StencilArgs** dev) {
+  xmhd_ctx* c0 = ctxs[0];
+  if (!c0->emul_args) CK(cudaMalloc(&c0->emul_args, sizeof(StencilArgs) * P2P_MAX));
+  static StencilArgs host[P2P_MAX];
+  for (int r = 0; r < nranks; ++r) {
+    host[r] = leja_args(ctxs[r]);
+    host[r].ext_sums = ctxs[r]->result + 8;
+    host[r].p2p = ctxs[r]->p2p;
+  }
+  CK(cudaMemcpy(c0->emul_args, host, sizeof(StencilArgs) * nranks, cudaMemcpyHostToDevice));
+  *dev = c0->emul_args;
+  return XMHD_OK;
+}
+
+int emul_check(xmhd_ctx* const* ctxs, int nranks) {
+  if (!ctxs || nranks < 2 || nranks > P2P_MAX) return fail(XMHD_BADARG, "bad ranks");
+  for (int r = 0; r < nranks; ++r) {
+    int rc = p2p_check(ctxs[r]);
+    if (rc) return rc;
+    if (ctxs[r]->stream != ctxs[0]->stream) return fail(XMHD_BADARG, "ranks must share a stream");
+  }
+  return XMHD_OK;
+}
+
+}  // namespace
+
+int xmhd_leja_p2p_emul_start(xmhd_ctx* const* ctxs, int nranks, const double* const* u,
+                             const double* const* fu, double unorm, const double* const* v,
+                             double dt, double q, double theta, double tol, const double* xi,
+                             const double* coeffs, int ncoef) {
+  int rc = emul_check(ctxs, nranks);
+  if (rc) return rc;
+  for (int r = 0; r < nranks; ++r) {
+    xmhd_ctx* c = ctxs[r];
+    c->leja_u = u[r];
+    c->leja_fu = fu[r];
+    rc = leja_setup(c, v[r], NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef,
+                    c->result + 8);
+    if (!rc) rc = p2p_push_y0(c);
+    if (rc) return rc;
+  }
+  StencilArgs* dev = nullptr;
+  rc = emul_args(ctxs, nranks, &dev);
+  if (rc) return rc;
+  CK(launch_leja_p2p_init_emul(dev, nranks, ctxs[0]->stream));
+  CK(cudaStreamSynchronize(ctxs[0]->stream));
+  return XMHD_OK;
+}
+
+int xmhd_leja_p2p_emul_run(xmhd_ctx* const* ctxs, int nranks, xmhd_leja_state* st) {
+  int rc = emul_check(ctxs, nranks);
+  if (rc) return rc;
+  StencilArgs* dev = nullptr;
+  rc = emul_args(ctxs, nranks, &dev);
+  if (rc) return rc;
+  const int cap = leja_emul_max_blocks(ctxs[0]->nsm) / nranks;
+  int nblk = 0;
+  for (int r = 0; r < nranks; ++r) nblk = ctxs[r]->grid > nblk ? ctxs[r]->grid : nblk;
+  if (nblk > cap) nblk = cap;
+  if (nblk < 1) return fail(XMHD_BADARG, "too many emulated ranks for one cooperative launch");
+  const StencilArgs a0 = leja_args(ctxs[0]);
+  for (;;) {
+    CK(launch_leja_emul(dev, a0, nranks, nblk, ctxs[0]->stream));
+    for (int r = 0; r < nranks; ++r) ctxs[r]->launches++;
+    for (int r = 0; r < nranks; ++r) {
+      rc = sync_ctl(ctxs[r]);
+      if (rc) return rc;
+      const LejaCtl& h = *ctxs[r]->ctl_h;
+      const LejaCtl& h0 = *ctxs[0]->ctl_h;
+      if (h.status != h0.status || h.iters != h0.iters || h.epoch != h0.epoch)
+        return fail(XMHD_CUDA_ERROR, "emulated ranks diverged");
+    }
+    if (ctxs[0]->ctl_h->status != LJ_RUNNING) break;
+  }
+  for (int r = 0; r < nranks; ++r) ctxs[r]->p2p_epoch = ctxs[r]->ctl_h->epoch;
+  fill_state(*ctxs[0]->ctl_h, st);
+  if (ctxs[0]->ctl_h->status == LJ_PEER_TIMEOUT)
+    return fail(XMHD_CUDA_ERROR, "peer-memory exchange timed out");
   return XMHD_OK;
 }
 

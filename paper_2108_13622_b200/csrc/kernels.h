@@ -30,6 +30,7 @@ struct LejaCtl {
   Divisor thetad;   // theta, likewise (host-computed)
   int force_ieee;   // testing: plain IEEE division for eps as well
   int pad2_;
+  unsigned long long epoch;   // y-strips over peer memory: last exchange epoch
 };
 
 enum LejaStatus {
@@ -39,6 +40,28 @@ enum LejaStatus {
   LJ_RHS_BAD = 3,      // non-finite RHS: the reference raises RhsBlowupError
   LJ_NEED_COEFFS = 4,  // m reached the coefficient chunk size (leja.py:128-130)
   LJ_EXHAUSTED = 5,    // 499 terms without convergence (leja.py:149-150)
+  LJ_PEER_TIMEOUT = 6, // y-strips over peer memory: a peer never posted its sums
+};
+
+constexpr int P2P_MAX = 8;   // ranks of one NVLink / NVSwitch node
+
+// Peer-memory transport of the y-strip Leja loop.  The fused iteration kernel
+// stores the boundary rows of y' straight into the neighbours' ghost-row
+// buffers and all-reduces [sum y'^2, sum p'^2, bad] through per-rank boards
+// whose flags carry a monotonically increasing epoch, so a Newton term needs
+// no host call and no collective library.  Pointers are this process's CUDA
+// IPC mappings of the peers' regions (or plain device pointers when the ranks
+// are emulated in one launch on one GPU).  Ghost-row buffers are
+// double-buffered by the parity of the current y (LejaCtl::cur).
+struct P2PArgs {
+  double* dst_lo[2];                 // per parity: destination of my rows 0, 1 ([f][2][nx])
+  double* dst_hi[2];                 // destination of my rows ny-2, ny-1
+  int mirror_lo, mirror_hi;          // the destination is my own ghost rows (reflecting wall)
+  const double* halo_lo_dir[2];      // my ghost rows -2, -1 of the direction, per parity
+  const double* halo_hi_dir[2];      // my ghost rows ny, ny+1
+  double* board[P2P_MAX];            // rank q's board: [2 slots][P2P_MAX][4] doubles
+  unsigned long long* flag[P2P_MAX]; // rank q's flags: [2 slots][P2P_MAX]
+  int rank, nranks;
 };
 
 enum StencilMode { MODE_RHS = 0, MODE_JVP = 1, MODE_LEJA = 2 };
@@ -64,6 +87,7 @@ struct StencilArgs {
   int* bad;            // |= 1 when a non-finite F cell is produced
   double* ext_sums;    // MODE_LEJA y-strips: [sum y'^2, sum p'^2, bad] of this rank
   int units_x, nunits, seg_rows;
+  P2PArgs p2p;         // MODE_LEJA y-strips over peer memory
 };
 
 constexpr int SW = 128;          // threads per block = ghost-extended columns per strip
@@ -137,7 +161,61 @@ cudaError_t launch_mgs(double* w, long long n, const double* v, const double* ci
 cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B, int m,
                                   double scale, RedBuf rb, cudaStream_t s);
 
+// Kernels of the peer-memory strip driver (stencil.cu / vec.cu).
+cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s);
+// Emulation of P ranks on one GPU: ONE cooperative launch over all ranks'
+// blocks (args: device array of P StencilArgs; nblk blocks per rank).
+cudaError_t launch_leja_emul(const StencilArgs* args_dev, const StencilArgs& a0, int nranks,
+                             int nblk, cudaStream_t s);
+int leja_emul_max_blocks(int nsm);
+// Start of a peer-memory strip Leja call: exchange of sum(v^2) (ext_sums[0])
+// and leja_init_ctl on the global sum.  Real ranks: one block; emulation: one
+// block per rank over args_dev (cooperative).
+cudaError_t launch_leja_p2p_init(const StencilArgs& a, cudaStream_t s);
+cudaError_t launch_leja_p2p_init_emul(const StencilArgs* args_dev, int nranks, cudaStream_t s);
+// Connectivity probe: write `value` into every peer board (slot 0, my row).
+cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s);
+
 #ifdef __CUDACC__
+// All-reduce of 3 doubles over the ranks through peer memory (one thread).
+// Every rank adds the same P entries in rank order, so all ranks obtain the
+// same bits.  Slot = epoch parity: a rank can only reuse a slot after every
+// rank has consumed it (it must first pass the exchange of epoch+1).
+__device__ __forceinline__ bool p2p_allreduce3(const P2PArgs& x, unsigned long long epoch,
+                                               const double v[3], double out[3]) {
+  const int P = x.nranks, me = x.rank, slot = (int)(epoch & 1ull);
+  for (int q = 0; q < P; ++q) {
+    volatile double* b = x.board[q] + (slot * P2P_MAX + me) * 4;
+    b[0] = v[0];
+    b[1] = v[1];
+    b[2] = v[2];
+  }
+  __threadfence_system();
+  for (int q = 0; q < P; ++q) {
+    volatile unsigned long long* f = x.flag[q] + slot * P2P_MAX + me;
+    *f = epoch;
+  }
+  volatile unsigned long long* mine = x.flag[me] + slot * P2P_MAX;
+  for (int q = 0; q < P; ++q) {
+    long long spins = 0;
+    while (mine[q] < epoch) {
+      __nanosleep(128);
+      if (++spins > (1ll << 26)) return false;   // seconds: a peer is gone
+    }
+  }
+  __threadfence_system();
+  volatile const double* mb = x.board[me] + slot * P2P_MAX * 4;
+  out[0] = mb[0];
+  out[1] = mb[1];
+  out[2] = mb[2];
+  for (int q = 1; q < P; ++q) {
+    out[0] = __dadd_rn(out[0], mb[q * 4]);
+    out[1] = __dadd_rn(out[1], mb[q * 4 + 1]);
+    out[2] = __dadd_rn(out[2], mb[q * 4 + 2]);
+  }
+  return true;
+}
+
 // Control update after one Newton term (leja.py:134-148); run by one thread
 // of the last CTA of the iteration kernel, after the deterministic reduction.
 __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp, int bad,

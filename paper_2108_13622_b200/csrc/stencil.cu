@@ -35,6 +35,7 @@
 // completed by the two-correction Markstein sequence (exact for any divisor).
 #include <cfloat>
 #include <climits>
+#include <type_traits>
 #include "kernels.h"
 
 // Variants measured and dropped: epilogue operands staged by
@@ -65,7 +66,8 @@ struct RowSrc {
 };
 
 __device__ __forceinline__ RowSrc row_source(int r, const Geom& g, const double* u,
-                                             const double* d) {
+                                             const double* d, const double* hlo_dir,
+                                             const double* hhi_dir) {
   RowSrc s;
   s.flip = 0;
   s.fs = (unsigned)g.plane;
@@ -82,14 +84,14 @@ __device__ __forceinline__ RowSrc row_source(int r, const Geom& g, const double*
   } else {  // BC_HALO: rows owned by the y-neighbours, [field][2][nx]
     if (r < 0) {
       s.u = g.halo_lo;
-      s.d = g.halo_lo_dir;
+      s.d = hlo_dir;
       s.off = (unsigned)(r + 2) * (unsigned)g.nx;
       s.fs = 2u * (unsigned)g.nx;
       return s;
     }
     if (r >= g.ny) {
       s.u = g.halo_hi;
-      s.d = g.halo_hi_dir;
+      s.d = hhi_dir;
       s.off = (unsigned)(r - g.ny) * (unsigned)g.nx;
       s.fs = 2u * (unsigned)g.nx;
       return s;
@@ -136,10 +138,36 @@ __device__ __forceinline__ double sum_partials(const double* p, int nblk, int st
   return __shfl_sync(0xffffffffu, s, 0);
 }
 
+// Exchange kind of a MODE_LEJA launch: none (single domain, or y-strips over
+// NCCL with ext_sums), peer memory (one launch per rank), or P ranks emulated
+// in one cooperative launch on one GPU.
+enum { XR_NONE = 0, XR_PEER = 1, XR_EMUL = 2 };
+
+// y' of boundary row o of this strip into the ghost-row buffers it feeds
+// ([field][2][nx]): rows 0, 1 -> the rank below (its rows ny, ny+1) or, at a
+// reflecting wall, my own ghost rows -1, -2 with MY, BY odd; rows ny-2, ny-1
+// likewise upwards.  Same values as leja_pack_halo_kernel (vec.cu).
+__device__ __forceinline__ void push_ghost(double* dlo, int mlo, double* dhi, int mhi, int f,
+                                           int o, int ny, int nx, int c, double y) {
+  const double s = (f == MY || f == BY) ? -1.0 : 1.0;
+  if (o < 2 && dlo) {
+    const int k = mlo ? 1 - o : o;
+    dlo[(f * 2 + k) * nx + c] = mlo ? __dmul_rn(s, y) : y;
+  }
+  if (o >= ny - 2 && dhi) {
+    const int k = mhi ? ny - 1 - o : o - (ny - 2);
+    dhi[(f * 2 + k) * nx + c] = mhi ? __dmul_rn(s, y) : y;
+  }
+}
+
 }  // namespace
 
-template <int MODE, int KX, int KY>
-__global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
+// One launch of the fused stencil.  bid / nblk: this block's index among the
+// nblk blocks working on this rank's grid (the launch grid, except in the
+// one-launch emulation of several ranks).
+template <int MODE, int KX, int KY, int XR>
+__device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid,
+                                             const int nblk) {
   extern __shared__ __align__(16) double smem[];
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
   double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
@@ -163,10 +191,20 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
   double* pout = nullptr;
   double dt = 0.0, q = 0.0, xim = 0.0, cm = 0.0;
   int zero_dir = 0;
+  const double* hlo_dir = g.halo_lo_dir;
+  const double* hhi_dir = g.halo_hi_dir;
+  double* push_lo = nullptr;
+  double* push_hi = nullptr;
   if (MODE == MODE_LEJA) {
     const LejaCtl* c = a.ctl;
     if (c->status != LJ_RUNNING) return;
     const int cur = c->cur, m = c->m;
+    if (XR != XR_NONE) {
+      hlo_dir = a.p2p.halo_lo_dir[cur];
+      hhi_dir = a.p2p.halo_hi_dir[cur];
+      push_lo = a.p2p.dst_lo[cur ^ 1];
+      push_hi = a.p2p.dst_hi[cur ^ 1];
+    }
     eps = c->eps;
     epsd = c->epsd;
     thd = c->thetad;
@@ -187,18 +225,24 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
   if (MODE == MODE_LEJA && zero_dir) {
     // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
     const long long n = (long long)NF * g.plane;
-    for (long long i = (long long)blockIdx.x * SW + t; i < n; i += (long long)gridDim.x * SW) {
+    for (long long i = (long long)bid * SW + t; i < n; i += (long long)nblk * SW) {
       const double y = dir[i];
       const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
       const double pn = __dadd_rn(pin[i], __dmul_rn(cm, yn));
       yout[i] = yn;
       pout[i] = pn;
+      if (XR != XR_NONE) {
+        const int f = (int)(i / g.plane);
+        const long long rem = i - (long long)f * g.plane;
+        const int o = (int)(rem / g.nx), c = (int)(rem - (long long)o * g.nx);
+        push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, o, g.ny, g.nx, c, yn);
+      }
       acc0 = __fma_rn(yn, yn, acc0);
       acc1 = __fma_rn(pn, pn, acc1);
     }
   } else {
-    for (int unit = blockIdx.x; unit < a.nunits; unit += gridDim.x) {
+    for (int unit = bid; unit < a.nunits; unit += nblk) {
       const int ux = unit % a.units_x, uy = unit / a.units_x;
       const int X0 = ux * SOUT;
       const int Y0 = uy * a.seg_rows;
@@ -225,7 +269,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       double nu[NF], nd[NF];
       int nflip;   // mirror flag of the prefetched row
       {
-        const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc);
+        const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc, hlo_dir, hhi_dir);
         nflip = rs.flip;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
@@ -266,7 +310,7 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
           if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
           if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
           if (s + 1 < nsteps) {
-            const RowSrc rs = row_source(r + 1, g, a.u, dsrc);
+            const RowSrc rs = row_source(r + 1, g, a.u, dsrc, hlo_dir, hhi_dir);
             nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
@@ -395,6 +439,9 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
               const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
               yout[i] = yn;
               pout[i] = pn;
+              if (XR != XR_NONE)
+                push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
+                           g.nx, c_out, yn);
               acc0 = __fma_rn(yn, yn, acc0);
               acc1 = __fma_rn(pn, pn, acc1);
             }
@@ -416,21 +463,36 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
   const double s0 = block_sum(acc0, red);
   const double s1 = (MODE == MODE_LEJA) ? block_sum(acc1, red) : 0.0;
   if (t == 0) {
-    a.partials[2 * blockIdx.x] = s0;
-    a.partials[2 * blockIdx.x + 1] = s1;
-    __threadfence();
+    a.partials[2 * bid] = s0;
+    a.partials[2 * bid + 1] = s1;
+    // peer memory: this block's ghost-row stores to the neighbours must be
+    // visible system-wide before the last block publishes the epoch
+    if (XR != XR_NONE) __threadfence_system();
+    else __threadfence();
     const unsigned prev = atomicAdd(a.ticket, 1u);
-    am_last = (prev == gridDim.x - 1);
+    am_last = (prev == (unsigned)nblk - 1);
   }
   __syncthreads();
   if (!am_last) return;
   __threadfence();
   if (t < 32) {
-    const double sy = sum_partials(a.partials, gridDim.x, 2, 0);
-    const double sp = (MODE == MODE_LEJA) ? sum_partials(a.partials, gridDim.x, 2, 1) : 0.0;
+    const double sy = sum_partials(a.partials, nblk, 2, 0);
+    const double sp = (MODE == MODE_LEJA) ? sum_partials(a.partials, nblk, 2, 1) : 0.0;
     if (t == 0) {
       if (MODE == MODE_JVP) {
         a.result[0] = sqrt(sy);
+      } else if (MODE == MODE_LEJA && XR != XR_NONE) {
+        // y-strips over peer memory: all-reduce the three sums, then every rank
+        // runs the identical control update
+        LejaCtl* c = a.ctl;
+        const double v[3] = {sy, sp, *((volatile int*)a.bad) ? 1.0 : 0.0};
+        double tot[3];
+        const unsigned long long ep = c->epoch + 1;
+        c->epoch = ep;
+        if (p2p_allreduce3(a.p2p, ep, v, tot))
+          leja_finalize(c, tot[0], tot[1], tot[2] > 0.0, !zero_dir, cm);
+        else
+          c->status = LJ_PEER_TIMEOUT;
       } else if (a.ext_sums) {
         // y-strips: publish this rank's partial sums; the control update runs
         // after the cross-rank allreduce (leja_finalize_kernel)
@@ -445,6 +507,26 @@ __global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
       *a.ticket = 0u;
     }
   }
+}
+
+template <int MODE, int KX, int KY>
+__global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
+  stencil_body<MODE, KX, KY, XR_NONE>(a, blockIdx.x, gridDim.x);
+}
+
+// Fused Leja iteration of one y-strip with the peer-memory exchange.
+template <int KX, int KY>
+__global__ void __launch_bounds__(SW, 2) leja_peer_kernel(const StencilArgs a) {
+  stencil_body<MODE_LEJA, KX, KY, XR_PEER>(a, blockIdx.x, gridDim.x);
+}
+
+// P ranks in one cooperative launch on one GPU (tests): blocks
+// [r*nblk, (r+1)*nblk) run rank r with args[r]; the ranks' last blocks meet
+// in p2p_allreduce3, which the cooperative launch makes safe (co-resident).
+template <int KX, int KY>
+__global__ void __launch_bounds__(SW, 2) leja_emul_kernel(const StencilArgs* args, int nblk) {
+  const int rank = blockIdx.x / nblk;
+  stencil_body<MODE_LEJA, KX, KY, XR_EMUL>(args[rank], blockIdx.x - rank * nblk, nblk);
 }
 
 size_t stencil_smem_bytes() {
@@ -514,20 +596,86 @@ cudaError_t launch_one(const StencilArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int MODE>
-cudaError_t launch_mode(const StencilArgs& a, int grid, cudaStream_t s) {
-  const int kx = a.g.h2x.kind, ky = a.g.h2y.kind;
-  if (kx == DIV_IEEE || ky == DIV_IEEE) return launch_one<MODE, DIV_IEEE, DIV_IEEE>(a, grid, s);
-  if (kx == DIV_MUL && ky == DIV_MUL) return launch_one<MODE, DIV_MUL, DIV_MUL>(a, grid, s);
+// Calls f(KX, KY) with the compile-time division kinds of the geometry.
+template <typename F>
+cudaError_t with_div_kinds(const Geom& g, F&& f) {
+  using M = std::integral_constant<int, DIV_MUL>;
+  using K1 = std::integral_constant<int, DIV_MK1>;
+  using K2 = std::integral_constant<int, DIV_MK2>;
+  using IE = std::integral_constant<int, DIV_IEEE>;
+  const int kx = g.h2x.kind, ky = g.h2y.kind;
+  if (kx == DIV_IEEE || ky == DIV_IEEE) return f(IE{}, IE{});
+  if (kx == DIV_MUL && ky == DIV_MUL) return f(M{}, M{});
   // a power-of-two divisor is also exact on the one-correction path
   const int x2 = (kx == DIV_MK2), y2 = (ky == DIV_MK2);
-  if (x2 && y2) return launch_one<MODE, DIV_MK2, DIV_MK2>(a, grid, s);
-  if (x2) return launch_one<MODE, DIV_MK2, DIV_MK1>(a, grid, s);
-  if (y2) return launch_one<MODE, DIV_MK1, DIV_MK2>(a, grid, s);
-  return launch_one<MODE, DIV_MK1, DIV_MK1>(a, grid, s);
+  if (x2 && y2) return f(K2{}, K2{});
+  if (x2) return f(K2{}, K1{});
+  if (y2) return f(K1{}, K2{});
+  return f(K1{}, K1{});
+}
+
+template <int MODE>
+cudaError_t launch_mode(const StencilArgs& a, int grid, cudaStream_t s) {
+  return with_div_kinds(a.g, [&](auto X, auto Y) {
+    return launch_one<MODE, decltype(X)::value, decltype(Y)::value>(a, grid, s);
+  });
+}
+
+template <typename K>
+cudaError_t smem_attr_once(K kernel, bool& done) {
+  if (done) return cudaSuccess;
+  cudaError_t err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)stencil_smem_bytes());
+  if (err == cudaSuccess) done = true;
+  return err;
+}
+
+template <int KX, int KY>
+cudaError_t launch_peer_one(const StencilArgs& a, int grid, cudaStream_t s) {
+  static bool done = false;
+  cudaError_t err = smem_attr_once(leja_peer_kernel<KX, KY>, done);
+  if (err != cudaSuccess) return err;
+  leja_peer_kernel<KX, KY><<<grid, SW, stencil_smem_bytes(), s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int KX, int KY>
+cudaError_t launch_emul_one(const StencilArgs* args_dev, int nranks, int nblk, cudaStream_t s) {
+  static bool done = false;
+  cudaError_t err = smem_attr_once(leja_emul_kernel<KX, KY>, done);
+  if (err != cudaSuccess) return err;
+  void* kargs[] = {(void*)&args_dev, (void*)&nblk};
+  return cudaLaunchCooperativeKernel((const void*)leja_emul_kernel<KX, KY>, dim3(nranks * nblk),
+                                     dim3(SW), kargs, stencil_smem_bytes(), s);
 }
 
 }  // namespace
+
+cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s) {
+  return with_div_kinds(a.g, [&](auto X, auto Y) {
+    return launch_peer_one<decltype(X)::value, decltype(Y)::value>(a, grid, s);
+  });
+}
+
+cudaError_t launch_leja_emul(const StencilArgs* args_dev, const StencilArgs& a0, int nranks,
+                             int nblk, cudaStream_t s) {
+  return with_div_kinds(a0.g, [&](auto X, auto Y) {
+    return launch_emul_one<decltype(X)::value, decltype(Y)::value>(args_dev, nranks, nblk, s);
+  });
+}
+
+// Co-resident blocks of the emulation kernel on the whole device.
+int leja_emul_max_blocks(int nsm) {
+  int n = 0;
+  static bool done = false;
+  if (smem_attr_once(leja_emul_kernel<DIV_MUL, DIV_MUL>, done) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, leja_emul_kernel<DIV_MUL, DIV_MUL>, SW,
+                                                    stencil_smem_bytes()) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n * nsm;
+}
 
 cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s) {
   switch (mode) {

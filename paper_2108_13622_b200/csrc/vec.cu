@@ -7,6 +7,7 @@
 // Element-wise arithmetic reproduces NumPy's single-rounding-per-ufunc order
 // (integrators.py:146-199, linearize.py:113-127, leja.py:121-123).
 #include <cfloat>
+#include <cstring>
 #include "kernels.h"
 
 namespace xb {
@@ -296,6 +297,7 @@ __global__ void leja_pack_halo_kernel(const LejaCtl* ctl, const double* y0, cons
     if (mirror_lo) halo_lo[k] = __dmul_rn(s, y[f * plane + (long long)(1 - rr) * nx + i]);
     if (mirror_hi) halo_hi[k] = __dmul_rn(s, y[f * plane + (long long)(ny - 1 - rr) * nx + i]);
   }
+  __threadfence_system();   // the destinations may be peer memory (y-strips over NVLink)
 }
 
 __global__ void __launch_bounds__(VT) sumsq_kernel(const double* __restrict__ x, long long n,
@@ -379,6 +381,34 @@ __global__ void __launch_bounds__(VT) krylov_combine_kernel(double* __restrict__
   }
 }
 
+// Start of a peer-memory strip Leja call (one thread per rank): all-reduce of
+// the local sum(v^2) in ext_sums[0], then the control-block start on the
+// global sum (leja.py:121-123) -- the peer counterpart of
+// leja_init_finalize_kernel.
+template <bool EMUL>
+__global__ void leja_p2p_init_kernel(const StencilArgs a0, const StencilArgs* args) {
+  if (threadIdx.x != 0) return;
+  const StencilArgs& a = EMUL ? args[blockIdx.x] : a0;
+  LejaCtl* c = a.ctl;
+  const double v[3] = {a.ext_sums[0], 0.0, 0.0};
+  double tot[3];
+  const unsigned long long ep = c->epoch + 1;
+  c->epoch = ep;
+  if (p2p_allreduce3(a.p2p, ep, v, tot)) leja_init_ctl(c, tot[0]);
+  else c->status = LJ_PEER_TIMEOUT;
+}
+
+// Connectivity probe: `value` into slot 0, row `rank`, of every rank's board.
+__global__ void p2p_probe_kernel(const P2PArgs x, double value) {
+  const int q = threadIdx.x;
+  if (q < x.nranks) {
+    volatile double* b = x.board[q] + x.rank * 4;
+    b[0] = value;
+    b[1] = (double)x.rank;
+  }
+  __threadfence_system();
+}
+
 int grid_for(long long n, int maxg) {
   long long g = (n + VT - 1) / VT;
   if (g > maxg) g = maxg;
@@ -398,6 +428,24 @@ cudaError_t launch_mgs(double* w, long long n, const double* v, const double* ci
 cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B, int m,
                                   double scale, RedBuf rb, cudaStream_t s) {
   krylov_combine_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, n, B, m, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leja_p2p_init(const StencilArgs& a, cudaStream_t s) {
+  leja_p2p_init_kernel<false><<<1, 32, 0, s>>>(a, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leja_p2p_init_emul(const StencilArgs* args_dev, int nranks, cudaStream_t s) {
+  StencilArgs dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  void* kargs[] = {(void*)&dummy, (void*)&args_dev};
+  return cudaLaunchCooperativeKernel((const void*)leja_p2p_init_kernel<true>, dim3(nranks),
+                                     dim3(32), kargs, 0, s);
+}
+
+cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s) {
+  p2p_probe_kernel<<<1, 32, 0, s>>>(x, value);
   return cudaGetLastError();
 }
 

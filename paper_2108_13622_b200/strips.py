@@ -16,8 +16,13 @@ synchronisation:
     allreduce of [sum y'^2, sum p'^2, non-finite]     (one 24-byte NCCL allreduce)
     control update from the global sums               (1-thread kernel, identical on all ranks)
 
-and synchronises once per batch of terms.  u's halo rows are exchanged once per
-phi-call (u is frozen).  Every other norm of the host layer (FD step, error
+and synchronises once per batch of terms.  That is the NCCL transport.  On one
+NVLink / NVSwitch node the default is the peer-memory transport instead: the
+fused kernel itself stores its boundary rows of y' into the neighbours'
+ghost-row buffers (CUDA IPC mappings) and all-reduces the three sums through
+per-rank boards in peer memory, so a Newton term is ONE kernel launch per rank
+with no host call and no collective (``XMHD_STRIP_TRANSPORT=nccl`` selects the
+NCCL path).  u's halo rows are exchanged once per phi-call (u is frozen).  Every other norm of the host layer (FD step, error
 norm, power iteration, totals) becomes a cross-rank reduction through
 ``_ops.set_reducer``.
 
@@ -211,6 +216,30 @@ class StripMhd:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.state_halo = HaloSet(self.nx, dev)
         self.dir_halo = HaloSet(self.nx, dev)
+        self._peer = False
+
+    def peer_transport(self):
+        """True when the Leja loop runs over peer memory (and the link is set up).
+
+        Real ranks of one node (torch.distributed) use it unless
+        XMHD_STRIP_TRANSPORT=nccl; host-thread emulations of ranks cannot (their
+        kernels would wait on each other on one GPU) and use the NCCL-style path.
+        """
+        import os
+        if self._peer:
+            return True
+        if (os.environ.get("XMHD_STRIP_TRANSPORT", "peer") != "peer" or self.comm.size < 2
+                or not isinstance(self.comm, Comm) or self.comm.size > 8):
+            return False
+        lib = _lib.load()
+        handle = (ctypes.c_char * 64)()
+        _lib.check(lib.xmhd_p2p_alloc(self.ctx.h, handle), "xmhd_p2p_alloc")
+        handles = self.comm.gather_host(bytes(handle))
+        blob = (ctypes.c_char * (64 * len(handles))).from_buffer_copy(b"".join(handles))
+        _lib.check(lib.xmhd_p2p_connect(self.ctx.h, self.comm.rank, self.comm.size, blob,
+                                        int(self.periodic_y)), "xmhd_p2p_connect")
+        self._peer = True
+        return True
 
     def _set_halo(self, u_halo, d_halo=None):
         lib = _lib.load()
@@ -371,6 +400,36 @@ def leja_strips(backend, comm, periodic, l, v, dt, q, theta, tol, xi, coeff_fn, 
         batch = min(2 * batch, batch_max)
 
 
+def leja_peer(mhd, lin, l, vd, dt, q, theta, tol, xi):
+    """The Leja loop over peer memory: one fused launch per term on every rank."""
+    from paper_2108_13622_b200 import leja
+    lib = _lib.load()
+    mhd.exchange(lin.base_state, mhd.state_halo)
+    mhd._set_halo(mhd.state_halo, mhd.dir_halo)
+    h = mhd.ctx.bind_stream()
+    chunk = 64
+    coeffs = np.ascontiguousarray(leja._newton_coeffs(l, q, theta, chunk))
+    leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
+    hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
+    lib.xmhd_leja_hint(h, int(leja._degree_hint.get(hkey, 2)))
+    rc = lib.xmhd_leja_p2p_start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
+                                 float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
+                                 float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
+                                 int(coeffs.size))
+    _lib.check(rc, "xmhd_leja_p2p_start")
+    st = _lib.LejaState()
+    _lib.check(lib.xmhd_leja_p2p_run(h, ctypes.byref(st)), "xmhd_leja_p2p_run")
+    while st.status == _lib.LEJA_NEED_COEFFS:
+        chunk, grown = leja._grow(l, q, theta, chunk, coeffs, st.m)
+        coeffs = np.ascontiguousarray(grown)
+        leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
+        _lib.check(lib.xmhd_leja_set_coeffs(h, _ptr_d(coeffs), int(coeffs.size)),
+                   "xmhd_leja_set_coeffs")
+        _lib.check(lib.xmhd_leja_p2p_run(h, ctypes.byref(st)), "xmhd_leja_p2p_run")
+    leja._degree_hint[hkey] = int(st.iterations)
+    return st
+
+
 def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
     """apply_phi_leja for a linearization whose RHS is a StripMhd (called by leja.py)."""
     from paper_2108_13622_b200 import leja
@@ -379,6 +438,10 @@ def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
     q, theta = shift.q, shift.theta
     vd = _ops.as_device(v).reshape(-1)
     backend = CudaStripBackend(mhd, lin)
+    if mhd.peer_transport():
+        st = leja_peer(mhd, lin, l, vd, dt, q, theta, tol, xi)
+        leja._drop_speculation(l, q, theta)
+        return _finish(l, lin, mhd, backend, vd, v, st)
 
     def coeff_fn(chunk):
         c = np.ascontiguousarray(leja._newton_coeffs(l, q, theta, chunk))
@@ -393,6 +456,12 @@ def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
     st = leja_strips(backend, mhd.comm, mhd.periodic_y, l, vd, dt, q, theta, tol, xi,
                      coeff_fn, grow_fn)
     leja._drop_speculation(l, q, theta)
+    return _finish(l, lin, mhd, backend, vd, v, st)
+
+
+def _finish(l, lin, mhd, backend, vd, v, st):
+    from paper_2108_13622_b200 import leja
+    from paper_2108_13622_b200.linearize import RhsBlowupError
     lin.rhs.calls += st.rhs_calls
     if st.status == _lib.LEJA_RHS_NONFINITE:
         y = backend.current_y(vd)

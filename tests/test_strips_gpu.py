@@ -176,3 +176,100 @@ def test_strip_krylov_matches_single_domain(nranks):
     for r in results:
         assert (r[2], r[3]) == (ref.iterations, ref.converged)
     assert rel(full.reshape(-1), ref.vector) <= 1e-11
+
+
+@pytest.mark.parametrize("nranks,refl", [(2, False), (3, False), (3, True)])
+def test_strip_peer_transport_emulated(nranks, refl):
+    """The peer-memory Leja loop (boundary rows pushed into the neighbours'
+    ghost rows and the sums all-reduced through peer boards, all inside the
+    fused kernel), with the ranks emulated in ONE cooperative launch per term on
+    this GPU: bit-identical to the NCCL-style strip loop (same sums in the same
+    rank order), same iteration counts."""
+    import ctypes
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import _lib, leja, scenarios as sc, strips
+    s, q, params = _problem(48, refl=refl)
+    v = sc.unit_gaussian(q.size, 9).reshape(q.shape)
+    geo = xb.StateGrid(s.nx, s.ny, s.dx, s.dy, torch.from_numpy(q).cuda())
+    lin = xb.FrozenLinearization(xb.RhsOperator(xb.MhdRhs(geo, params)), geo.flat())
+    alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    cases = [(1, 2.0), (2, 30.0)]
+
+    def rank(comm):
+        mhd = strips.StripMhd(xb.StateGrid(s.nx, s.ny, s.dx, s.dy, None), params, comm)
+        prev = xb.linearize._ops.set_reducer(strips.Reducer(comm, torch.device("cuda")))
+        try:
+            lay = mhd.layout
+            u = torch.from_numpy(np.ascontiguousarray(lay.local_rows(q))).cuda().reshape(-1)
+            slin = xb.FrozenLinearization(xb.RhsOperator(mhd), u)
+            vl = torch.from_numpy(np.ascontiguousarray(lay.local_rows(v))).cuda().reshape(-1)
+            out = []
+            for l, adt in cases:
+                res = xb.apply_phi_leja(l, xb.JacobianAction(slin), vl, adt / alpha,
+                                        xb.shift_and_scale(adt), 1e-10)
+                out.append((res.iterations, res.converged, res.vector.cpu().numpy()))
+            mhd.exchange(slin.base_state, mhd.state_halo)
+            mhd._set_halo(mhd.state_halo, mhd.dir_halo)
+            torch.cuda.current_stream().synchronize()
+            return mhd, slin, vl, out
+        finally:
+            xb.linearize._ops.set_reducer(prev)
+
+    results = run_ranks(nranks, rank)
+    lib = _lib.load()
+    P = nranks
+    ctxs = (ctypes.c_void_p * P)(*[r[0].ctx.bind_stream().value for r in results])
+    for r in results:
+        buf = (ctypes.c_char * 64)()
+        _lib.check(lib.xmhd_p2p_alloc(r[0].ctx.h, buf), "xmhd_p2p_alloc")
+    _lib.check(lib.xmhd_p2p_connect_local(ctxs, P, int(not refl)), "xmhd_p2p_connect_local")
+    ptrs = lambda ts: (ctypes.c_void_p * P)(*[t.data_ptr() for t in ts])
+    u_p = ptrs([r[1].base_state for r in results])
+    f_p = ptrs([r[1].base_rhs for r in results])
+    v_p = ptrs([r[2] for r in results])
+    unorm = float(results[0][1]._base_norm)
+    xi = np.ascontiguousarray(leja.leja_points(500))
+    dp = ctypes.POINTER(ctypes.c_double)
+    for k, (l, adt) in enumerate(cases):
+        sh = xb.shift_and_scale(adt)
+        chunk = 64
+        coeffs = np.ascontiguousarray(leja._newton_coeffs(l, sh.q, sh.theta, chunk))
+        rc = lib.xmhd_leja_p2p_emul_start(ctxs, P, u_p, f_p, unorm, v_p, adt / alpha, sh.q,
+                                          sh.theta, 1e-10, xi.ctypes.data_as(dp),
+                                          coeffs.ctypes.data_as(dp), coeffs.size)
+        _lib.check(rc, "xmhd_leja_p2p_emul_start")
+        st = _lib.LejaState()
+        _lib.check(lib.xmhd_leja_p2p_emul_run(ctxs, P, ctypes.byref(st)), "emul_run")
+        while st.status == _lib.LEJA_NEED_COEFFS:
+            chunk, coeffs = leja._grow(l, sh.q, sh.theta, chunk, coeffs, st.m)
+            coeffs = np.ascontiguousarray(coeffs)
+            for r in results:
+                _lib.check(lib.xmhd_leja_set_coeffs(r[0].ctx.h, coeffs.ctypes.data_as(dp),
+                                                    coeffs.size), "set_coeffs")
+            _lib.check(lib.xmhd_leja_p2p_emul_run(ctxs, P, ctypes.byref(st)), "emul_run")
+        assert st.status == _lib.LEJA_CONVERGED
+        for r in results:
+            its, conv, ref_vec = r[3][k]
+            assert st.iterations == its and conv
+            p = torch.empty_like(r[2])
+            _lib.check(lib.xmhd_leja_result(r[0].ctx.h, _lib.ptr(p)), "xmhd_leja_result")
+            assert np.array_equal(p.cpu().numpy(), ref_vec), (k, r[0].layout.y0)
+
+
+def test_peer_transport_setup_errors():
+    import ctypes
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import _lib
+    lib = _lib.load()
+    c = _lib.Context(16, 8, 0.1, 0.1, 0.01, 0.01, 0.01, 5.0 / 3.0, 1.0, _lib.BC_PERIODIC,
+                     _lib.BC_PERIODIC)
+    buf = (ctypes.c_char * 64)()
+    assert lib.xmhd_p2p_alloc(c.h, buf) == 2            # not a y-strip context
+    s = _lib.Context(16, 8, 0.1, 0.1, 0.01, 0.01, 0.01, 5.0 / 3.0, 1.0, _lib.BC_PERIODIC,
+                     _lib.BC_HALO)
+    st = _lib.LejaState()
+    assert lib.xmhd_leja_p2p_run(s.h, ctypes.byref(st)) == 2   # not connected
+    assert lib.xmhd_p2p_alloc(s.h, buf) == 0
+    handles = (ctypes.c_char * 128)()
+    assert lib.xmhd_p2p_connect(s.h, 0, 1, handles, 1) == 2    # one rank: no peers
+    assert lib.xmhd_p2p_connect(s.h, 2, 2, handles, 1) == 2    # rank out of range
