@@ -90,7 +90,11 @@ struct StencilArgs {
   P2PArgs p2p;         // MODE_LEJA y-strips over peer memory
 };
 
-constexpr int SW = 128;          // threads per block = ghost-extended columns per strip
+#ifndef XB_SW
+#define XB_SW 128
+#endif
+constexpr int SW = XB_SW;        // threads per block = ghost-extended columns per strip
+constexpr int SW_MINB = 256 / SW;   // resident blocks per SM the register budget targets
 constexpr int SOUT = SW - 4;     // output columns per strip
 size_t stencil_smem_bytes();
 void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows, int& grid);

@@ -41,7 +41,8 @@
 // Variants measured and dropped: epilogue operands staged by
 // cp.async (-43%: the larger shared-memory carve-out starves L1), epilogue
 // prefetch to L2 only (neutral), GY ring in shared memory (-35%), L1 cache
-// hints (-10%), double2 shared-memory rings (neutral).
+// hints (-10%), double2 shared-memory rings (neutral), 256-thread strips with
+// one CTA per SM (XB_SW=256: -20%, barrier stalls hit all 8 warps at once).
 
 namespace xb {
 
@@ -510,13 +511,13 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 }
 
 template <int MODE, int KX, int KY>
-__global__ void __launch_bounds__(SW, 2) stencil_kernel(const StencilArgs a) {
+__global__ void __launch_bounds__(SW, SW_MINB) stencil_kernel(const StencilArgs a) {
   stencil_body<MODE, KX, KY, XR_NONE>(a, blockIdx.x, gridDim.x);
 }
 
 // Fused Leja iteration of one y-strip with the peer-memory exchange.
 template <int KX, int KY>
-__global__ void __launch_bounds__(SW, 2) leja_peer_kernel(const StencilArgs a) {
+__global__ void __launch_bounds__(SW, SW_MINB) leja_peer_kernel(const StencilArgs a) {
   stencil_body<MODE_LEJA, KX, KY, XR_PEER>(a, blockIdx.x, gridDim.x);
 }
 
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(SW, 2) leja_peer_kernel(const StencilArgs a) {
 // [r*nblk, (r+1)*nblk) run rank r with args[r]; the ranks' last blocks meet
 // in p2p_allreduce3, which the cooperative launch makes safe (co-resident).
 template <int KX, int KY>
-__global__ void __launch_bounds__(SW, 2) leja_emul_kernel(const StencilArgs* args, int nblk) {
+__global__ void __launch_bounds__(SW, SW_MINB) leja_emul_kernel(const StencilArgs* args, int nblk) {
   const int rank = blockIdx.x / nblk;
   stencil_body<MODE_LEJA, KX, KY, XR_EMUL>(args[rank], blockIdx.x - rank * nblk, nblk);
 }

@@ -161,6 +161,55 @@ def leja_cases():
     return meta
 
 
+def leja_bc_cases():
+    """JVP, power iteration and phi on reflecting walls, mu0 != 1, gamma != 5/3 and
+    non-power-of-two spacings (the Markstein division paths of the kernels)."""
+    out = {}
+    meta = []
+    rng = np.random.default_rng(21)
+    for tag, nx, ny, dx, dy, px, py, prm in (
+            ("rand40x28_refl_xy", 40, 28, 0.07, 0.11, False, False,
+             dict(mu=0.02, eta=0.01, kappa=0.05, gamma=1.4, mu0=1.3)),
+            ("rand36x30_refl_y", 36, 30, 0.1, 0.15, True, False,
+             dict(mu=0.01, eta=0.02, kappa=0.03)),
+            ("rand33x21_refl_x_ideal", 33, 21, 0.05, 0.2, False, True,
+             dict(mu=0.0, eta=0.0, kappa=0.0))):
+        q = random_state(rng, nx, ny)
+        params = MHDParams(bc_x=bc(px), bc_y=bc(py), **prm)
+        op = mhd_op(q, dx, dy, params)
+        u = q.reshape(-1).copy()
+        lin = ref_lin.FrozenLinearization(op, u)
+        before = op.calls
+        est = ref_lin.estimate_alpha(lin, None, rng=np.random.default_rng(0))
+        power_calls = op.calls - before
+        w = sc.unit_gaussian(u.size, 7)
+        out[f"{tag}__u"] = q
+        out[f"{tag}__fu"] = lin.base_rhs
+        out[f"{tag}__w"] = w
+        out[f"{tag}__jw"] = ref_lin.jvp(lin, w)
+        out[f"{tag}__power_vec"] = est.vector
+        v = sc.unit_gaussian(u.size, 8)
+        out[f"{tag}__v"] = v
+        rec = dict(name=tag, dx=dx, dy=dy, periodic_x=px, periodic_y=py, mu=params.mu,
+                   eta=params.eta, kappa=params.kappa, gamma=params.gamma, mu0=params.mu0,
+                   alpha=est.alpha, power_calls=power_calls, phi=[])
+        for l, adt in ((1, 1.0), (1, 10.0), (4, 10.0), (0, 3.0)):
+            dt = adt / est.alpha
+            shift = ref_leja.shift_and_scale(est.alpha * dt)
+            ref_leja._coeff_cache.clear()
+            before = op.calls
+            res = ref_leja.apply_phi_leja(l, lambda x: ref_lin.jvp(lin, x), v, dt, shift, 1e-10)
+            key = f"{tag}__phi_l{l}_a{adt:g}"
+            out[key] = res.vector
+            rec["phi"].append(dict(key=key, l=l, adt=adt, dt=dt, q=shift.q, theta=shift.theta,
+                                   tol=1e-10, iterations=res.iterations,
+                                   converged=res.converged, residual=res.residual,
+                                   rhs_calls=op.calls - before))
+        meta.append(rec)
+    np.savez_compressed(os.path.join(HERE, "leja_bc_cases.npz"), **out)
+    return meta
+
+
 def coeff_cases():
     out = {"leja_points": np.asarray(ref_leja.leja_points(500))}
     meta = []
@@ -364,13 +413,13 @@ def wp_cases():
 
 
 def main():
-    which = sys.argv[1:] or ["rhs", "leja", "coeff", "step", "run", "krylov", "wp"]
+    which = sys.argv[1:] or ["rhs", "leja", "leja_bc", "coeff", "step", "run", "krylov", "wp"]
     path = os.path.join(HERE, "golden_meta.json")
     meta = json.load(open(path)) if os.path.exists(path) else {}
     meta["generator"] = "tests/golden/make_golden.py (reference xmhd %s, numpy %s)" % (
         xmhd.__version__, np.__version__)
     fns = dict(rhs=rhs_cases, leja=leja_cases, coeff=coeff_cases, step=step_cases,
-               run=run_cases, krylov=krylov_cases, wp=wp_cases)
+               run=run_cases, krylov=krylov_cases, wp=wp_cases, leja_bc=leja_bc_cases)
     for w in which:
         t0 = time.perf_counter()
         meta[w] = fns[w]()

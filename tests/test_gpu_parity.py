@@ -293,3 +293,37 @@ def test_rhs_large_grid_vs_oracle(xb):
         ref = mhd_np.rhs(strip, s.dx, s.dy, s.mu, s.eta, s.kappa).reshape(strip.shape)
         got = f[:, [(j0 + k) % s.ny for k in range(0, 8)], :]
         assert np.array_equal(got, ref[:, 2:10, :])
+
+
+BC_CASES = golden_io.meta()["leja_bc"]
+
+
+@pytest.mark.parametrize("case", BC_CASES, ids=lambda m: m["name"])
+def test_leja_boundaries_vs_reference(xb, case):
+    """Reflecting walls in x and/or y, mu0 != 1, gamma != 5/3, ideal MHD and
+    non-power-of-two spacings (Markstein division kinds) through the fused
+    JVP, the power iteration and the fused Leja loop."""
+    from paper_2108_13622_b200 import leja
+    g = golden_io.arrays("leja_bc_cases")
+    tag = case["name"]
+    q = g[tag + "__u"]
+    ny, nx = q.shape[1:]
+    st = xb.StateGrid(nx, ny, case["dx"], case["dy"], torch.from_numpy(q).cuda())
+    op = xb.RhsOperator(xb.MhdRhs(st, _params(xb, case)))
+    lin = xb.FrozenLinearization(op, st.flat())
+    assert np.array_equal(lin.base_rhs.cpu().numpy(), g[tag + "__fu"])
+    jw = xb.jvp(lin, torch.from_numpy(g[tag + "__w"]).cuda())
+    assert rel(jw, g[tag + "__jw"]) <= PHI_TOL
+    calls = op.calls
+    est = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0))
+    assert op.calls - calls == case["power_calls"]
+    assert abs(est.alpha - case["alpha"]) <= 1e-10 * case["alpha"]
+    v = torch.from_numpy(g[tag + "__v"]).cuda()
+    for p in case["phi"]:
+        leja._coeff_cache.clear()
+        calls = op.calls
+        res = xb.apply_phi_leja(p["l"], xb.JacobianAction(lin), v, p["dt"],
+                                xb.ShiftScale(p["q"], p["theta"]), p["tol"])
+        assert (res.iterations, res.converged) == (p["iterations"], p["converged"]), p["key"]
+        assert op.calls - calls == p["rhs_calls"]
+        assert rel(res.vector, g[p["key"]]) <= PHI_TOL, p["key"]

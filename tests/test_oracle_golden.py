@@ -197,3 +197,31 @@ def test_oracle_krylov_run(case):
     assert (rep.accepted, rep.rejected, rep.rhs_evals) == \
         (case["accepted"], case["rejected"], case["rhs_evals"])
     assert rep.checksum == case["checksum"]
+
+
+# ---- walls, mu0 != 1, gamma != 5/3, Markstein spacings -----------------------------
+
+@pytest.mark.parametrize("case", golden_io.meta()["leja_bc"], ids=lambda m: m["name"])
+def test_oracle_leja_boundaries(case):
+    g = golden_io.arrays("leja_bc_cases")
+    tag = case["name"]
+    q = g[f"{tag}__u"]
+
+    def f(flat):
+        return mhd_np.rhs(flat.reshape(q.shape), case["dx"], case["dy"], case["mu"],
+                          case["eta"], case["kappa"], case["gamma"], case["mu0"],
+                          case["periodic_x"], case["periodic_y"])
+
+    op = lj.CountedRhs(f)
+    lin = lj.Frozen(op, q.reshape(-1).copy())
+    assert np.array_equal(lin.fu, g[f"{tag}__fu"])
+    assert np.array_equal(lj.fd_jvp(lin, g[f"{tag}__w"]), g[f"{tag}__jw"])
+    calls = op.calls
+    est = lj.power_alpha(lin, None, rng=np.random.default_rng(0))
+    assert (est.alpha, op.calls - calls) == (case["alpha"], case["power_calls"])
+    for p in case["phi"]:
+        res = lj.phi_leja(p["l"], lambda x: lj.fd_jvp(lin, x), g[f"{tag}__v"], p["dt"], p["q"],
+                          p["theta"], p["tol"], lj.CoeffCache())
+        assert (res.iterations, res.converged, res.residual) == \
+            (p["iterations"], p["converged"], p["residual"])
+        assert np.array_equal(res.vector, g[p["key"]])
