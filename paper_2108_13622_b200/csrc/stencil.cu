@@ -42,7 +42,8 @@
 // cp.async (-43%: the larger shared-memory carve-out starves L1), epilogue
 // prefetch to L2 only (neutral), GY ring in shared memory (-35%), L1 cache
 // hints (-10%), double2 shared-memory rings (neutral), 256-thread strips with
-// one CTA per SM (XB_SW=256: -20%, barrier stalls hit all 8 warps at once).
+// one CTA per SM (XB_SW=256: -20%, barrier stalls hit all 8 warps at once),
+// one-correction bodies for eps / theta when exact (neutral).
 
 namespace xb {
 
