@@ -115,6 +115,20 @@ int xmhd_leja_start(xmhd_ctx* ctx, const double* u, const double* fu, double uno
 /* Expected number of Newton terms of the next xmhd_leja_start (host-side
  * launch batching only; results do not depend on it). */
 int xmhd_leja_hint(xmhd_ctx* ctx, int expected_iterations);
+/* Host-paced form of the same loop (what the Python mirror uses): start
+ * without running (xmhd_leja_start_async, or xmhd_leja_p2p_start), enqueue n
+ * iteration kernels without waiting (peer != 0: the y-strip peer-memory
+ * kernel); extend the device coefficient table to `to` entries with
+ * coeffs[from..to) ahead of the terms that need them (the values the reference
+ * would fetch when the chunk grows, leja.py:128-130), so the loop never stops
+ * at a chunk boundary; sync and read the state.  Kernels enqueued after the
+ * status left RUNNING exit immediately. */
+int xmhd_leja_start_async(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                          const double* v, double dt, double q, double theta, double tol,
+                          const double* xi, const double* coeffs, int ncoef);
+int xmhd_leja_launch(xmhd_ctx* ctx, int n, int peer);
+int xmhd_leja_extend(xmhd_ctx* ctx, const double* coeffs, int from, int to);
+int xmhd_leja_sync(xmhd_ctx* ctx, xmhd_leja_state* st);
 /* After XMHD_LEJA_NEED_COEFFS: upload the grown chunk and continue. */
 int xmhd_leja_resume(xmhd_ctx* ctx, const double* coeffs, int ncoef, xmhd_leja_state* st);
 /* Copy the interpolant p of the finished call into p_out (device, 8*nx*ny). */

@@ -83,6 +83,10 @@ _SIGS = {
     "xmhd_krylov_mgs": (_I, [_P, ctypes.POINTER(_P), _I, _P, _L, _PD, _PD]),
     "xmhd_mgs_update": (_I, [_P, _P, _L, _P, _D, _P, _PD]),
     "xmhd_krylov_combine": (_I, [_P, ctypes.POINTER(_P), _PD, _I, _D, _L, _P]),
+    "xmhd_leja_start_async": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I]),
+    "xmhd_leja_launch": (_I, [_P, _I, _I]),
+    "xmhd_leja_extend": (_I, [_P, _PD, _I, _I]),
+    "xmhd_leja_sync": (_I, [_P, ctypes.POINTER(LejaState)]),
     "xmhd_p2p_alloc": (_I, [_P, _P]),
     "xmhd_p2p_connect": (_I, [_P, _I, _I, _P, _I]),
     "xmhd_p2p_connect_local": (_I, [ctypes.POINTER(_P), _I, _I]),

@@ -46,6 +46,7 @@ struct xmhd_ctx {
   bool p2p_ready = false;
   unsigned long long p2p_epoch = 0;   // last exchange epoch (continues across calls)
   StencilArgs* emul_args = nullptr;   // device [P2P_MAX] (one-GPU emulation driver)
+  double* coef_h = nullptr;    // pinned [512]: staging of coefficient extensions
   double* kry_d = nullptr;     // [512] MGS coefficient slots (Krylov baseline)
   double* kry_h = nullptr;     // pinned [512]
   long long launches = 0;
@@ -201,6 +202,13 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   return XMHD_OK;
 }
 
+int p2p_check_ready(xmhd_ctx* c) {
+  if (c->g.bcy != BC_HALO) return fail(XMHD_BADARG, "peer transport needs a y-strip context");
+  if (!c->p2p_ready) return fail(XMHD_BADARG, "peer transport not connected");
+  if (!c->g.halo_lo) return fail(XMHD_BADARG, "state halo rows not set");
+  return XMHD_OK;
+}
+
 int upload_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
   if (ncoef < 1 || ncoef > 512) return fail(XMHD_BADARG, "ncoef out of range");
   CK(cudaMemcpyAsync(c->coeffs_d, coeffs, sizeof(double) * ncoef, cudaMemcpyHostToDevice,
@@ -318,6 +326,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
       (e = cudaMallocHost(&c->ctl_h, sizeof(LejaCtl))) != cudaSuccess ||
       (e = cudaMallocHost(&c->h_dbl, sizeof(double) * 16)) != cudaSuccess ||
       (e = cudaMallocHost(&c->h_int, sizeof(int) * 4)) != cudaSuccess ||
+      (e = cudaMallocHost(&c->coef_h, sizeof(double) * 512)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->tickets, 0, sizeof(unsigned) * 8, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->bad, 0, sizeof(int) * 4, c->stream)) != cudaSuccess ||
       (e = cudaStreamSynchronize(c->stream)) != cudaSuccess) {
@@ -347,6 +356,7 @@ int xmhd_destroy(xmhd_ctx* c) {
   cudaFreeHost(c->h_int);
   cudaFree(c->kry_d);
   cudaFreeHost(c->kry_h);
+  cudaFreeHost(c->coef_h);
   for (int q = 0; q < P2P_MAX; ++q)
     if (c->p2p_peer[q]) cudaIpcCloseMemHandle(c->p2p_peer[q]);
   cudaFree(c->p2p_base);
@@ -527,6 +537,16 @@ int xmhd_leja_start(xmhd_ctx* c, const double* u, const double* fu, double unorm
   return leja_run(c, st);
 }
 
+int xmhd_leja_start_async(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                          const double* v, double dt, double q, double theta, double tol,
+                          const double* xi, const double* coeffs, int ncoef) {
+  if (!c || !u || !fu || !v || !xi || !coeffs) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "use the strip driver for BC_HALO");
+  c->leja_u = u;
+  c->leja_fu = fu;
+  return leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+}
+
 int xmhd_leja_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_state* st) {
   if (!c || !coeffs) return fail(XMHD_BADARG, "null arg");
   int rc = upload_coeffs(c, coeffs, ncoef);
@@ -536,6 +556,48 @@ int xmhd_leja_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_sta
   CK(cudaMemcpyAsync(&c->ctl->ncoef, &c->ctl_h->ncoef, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(&c->ctl->status, &c->ctl_h->status, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   return leja_run(c, st);
+}
+
+// Host-paced driver primitives: enqueue iteration kernels without waiting,
+// extend the device coefficient table ahead of the terms that need it, sync.
+int xmhd_leja_launch(xmhd_ctx* c, int n, int peer) {
+  if (!c || n < 0 || n > 500) return fail(XMHD_BADARG, "bad launch count");
+  if (peer) {
+    int rc = p2p_check_ready(c);
+    if (rc) return rc;
+  }
+  StencilArgs a = leja_args(c);
+  if (peer) a.p2p = c->p2p;
+  for (int k = 0; k < n; ++k) {
+    if (peer) CK(launch_leja_peer(a, c->grid, c->stream));
+    else CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+    c->launches++;
+  }
+  return XMHD_OK;
+}
+
+int xmhd_leja_extend(xmhd_ctx* c, const double* coeffs, int from, int to) {
+  if (!c || !coeffs || from < 1 || to <= from || to > 500)
+    return fail(XMHD_BADARG, "bad coefficient extension");
+  // the staging ranges of one call's extensions are disjoint, so an earlier
+  // extension's copy still in flight is never overwritten
+  std::memcpy(c->coef_h + from, coeffs + from, sizeof(double) * (to - from));
+  CK(cudaMemcpyAsync(c->coeffs_d + from, c->coef_h + from, sizeof(double) * (to - from),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(launch_leja_extend(c->ctl, to, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_sync(xmhd_ctx* c, xmhd_leja_state* st) {
+  if (!c || !st) return fail(XMHD_BADARG, "null arg");
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  fill_state(*c->ctl_h, st);
+  c->p2p_epoch = c->ctl_h->epoch;
+  if (c->ctl_h->status == LJ_PEER_TIMEOUT)
+    return fail(XMHD_CUDA_ERROR, "peer-memory exchange timed out (a rank stopped)");
+  return XMHD_OK;
 }
 
 int xmhd_leja_hint(xmhd_ctx* c, int expected_iterations) {

@@ -177,6 +177,8 @@ int leja_emul_max_blocks(int nsm);
 // block per rank over args_dev (cooperative).
 cudaError_t launch_leja_p2p_init(const StencilArgs& a, cudaStream_t s);
 cudaError_t launch_leja_p2p_init_emul(const StencilArgs* args_dev, int nranks, cudaStream_t s);
+// Coefficient table grown to `to` entries (clears NEED_COEFFS when it applies).
+cudaError_t launch_leja_extend(LejaCtl* ctl, int to, cudaStream_t s);
 // Connectivity probe: write `value` into every peer board (slot 0, my row).
 cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s);
 

@@ -398,6 +398,14 @@ __global__ void leja_p2p_init_kernel(const StencilArgs a0, const StencilArgs* ar
   else c->status = LJ_PEER_TIMEOUT;
 }
 
+// The device coefficient table now holds `to` entries: leave NEED_COEFFS
+// if the loop stopped at the old end (stream order puts this between the
+// term that reached the boundary and the next one).
+__global__ void leja_extend_kernel(LejaCtl* ctl, int to) {
+  if (ctl->ncoef < to) ctl->ncoef = to;
+  if (ctl->status == LJ_NEED_COEFFS && ctl->m < ctl->ncoef) ctl->status = LJ_RUNNING;
+}
+
 // Connectivity probe: `value` into slot 0, row `rank`, of every rank's board.
 __global__ void p2p_probe_kernel(const P2PArgs x, double value) {
   const int q = threadIdx.x;
@@ -442,6 +450,11 @@ cudaError_t launch_leja_p2p_init_emul(const StencilArgs* args_dev, int nranks, c
   void* kargs[] = {(void*)&dummy, (void*)&args_dev};
   return cudaLaunchCooperativeKernel((const void*)leja_p2p_init_kernel<true>, dim3(nranks),
                                      dim3(32), kargs, 0, s);
+}
+
+cudaError_t launch_leja_extend(LejaCtl* ctl, int to, cudaStream_t s) {
+  leja_extend_kernel<<<1, 1, 0, s>>>(ctl, to);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s) {

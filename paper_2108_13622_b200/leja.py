@@ -184,6 +184,92 @@ def _ptr_d(a):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
+def _growth_plan(size, chunk=64):
+    """[(m, chunk)]: the chunk the reference fetches when the term index m reaches
+    the end of its coefficient table (leja.py:128-130), in order.  Stops where
+    the reference would index past the table (a cached table larger than the
+    doubled chunk is returned unchanged): the device then stops at that m."""
+    plan = []
+    while size < LEJA_MAX:
+        chunk = min(2 * chunk, LEJA_MAX)
+        if chunk <= size:
+            break
+        plan.append((size, chunk))
+        size = chunk
+    return plan
+
+
+def _cache_insert(l, q, theta, coeffs):
+    """The cache update _newton_coeffs performs on a miss (leja.py:96-99)."""
+    cache = _cache()
+    if len(cache) > 64:
+        cache.pop(next(iter(cache)))
+    cache[(l, q, theta)] = coeffs
+
+
+def drive_fused(lib, h, l, q, theta, coeffs, peer=False):
+    """Host-paced device Leja loop shared by the single-GPU and y-strip drivers.
+
+    Enqueues iteration kernels in batches sized by the degree of earlier calls
+    at a similar interval, and extends the device coefficient table ahead of
+    the term that first needs a grown chunk: the chunk is computed on a host
+    thread while the device iterates and its new entries are uploaded in
+    stream order (xmhd_leja_extend), so the loop never waits for the host at a
+    chunk boundary.  The reference's cache growth is replayed afterwards for
+    the boundaries the iteration actually crossed.  Returns the final state.
+    """
+    plan = _growth_plan(coeffs.size)
+    futs = {}
+
+    def fut(k):
+        if k < len(plan) and k not in futs:
+            futs[k] = _spec_pool.submit(_compute_coeffs, l, q, theta, plan[k][1])
+        return futs.get(k)
+
+    fut(0)
+    hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
+    batch = max(2, int(_degree_hint.get(hkey, 2)))
+    table_end, k, enq = coeffs.size, 0, 0
+    grown = []
+    st = _lib.LejaState()
+    target = batch
+    try:
+        while True:
+            while enq < min(target, LEJA_MAX - 1):
+                if k < len(plan) and enq + 1 >= plan[k][0]:
+                    arr = np.ascontiguousarray(fut(k).result())
+                    fut(k + 1)
+                    _lib.check(lib.xmhd_leja_extend(h, _ptr_d(arr), table_end, plan[k][1]),
+                               "xmhd_leja_extend")
+                    grown.append(arr)
+                    table_end = plan[k][1]
+                    k += 1
+                    continue
+                stop = min(target, LEJA_MAX - 1)
+                if k < len(plan):
+                    stop = min(stop, plan[k][0] - 1)
+                _lib.check(lib.xmhd_leja_launch(h, stop - enq, int(peer)), "xmhd_leja_launch")
+                enq = stop
+            _lib.check(lib.xmhd_leja_sync(h, ctypes.byref(st)), "xmhd_leja_sync")
+            if st.status != _lib.LEJA_RUNNING:
+                break
+            batch = min(2 * batch, 64)
+            target = enq + batch
+    finally:
+        for f in futs.values():
+            f.cancel()
+    for (m_b, _), arr in zip(plan, grown):
+        if st.iterations >= m_b:
+            _cache_insert(l, q, theta, arr)
+    if st.status == _lib.LEJA_NEED_COEFFS:
+        # only where the reference itself fails (see _growth_plan)
+        chunk = plan[-1][1] if plan else 64
+        _grow(l, q, theta, chunk, _cache().get((l, q, theta)), st.m)
+        raise RuntimeError("coefficient table ended early")   # not reached
+    _degree_hint[hkey] = int(st.iterations)
+    return st
+
+
 def apply_phi_leja(l, matvec, v, dt, shift, tol):
     """Approximate phi_l(J dt) v with J available only through `matvec` (leja.py:103-150).
 
@@ -209,28 +295,15 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
     mhd = lin.mhd
     lib = _lib.load()
     vd = _ops.as_device(v).reshape(-1)
-    chunk = 64
-    coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, chunk))
-    _speculate(l, q, theta, min(2 * chunk, LEJA_MAX))
+    coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, 64))
     st = _lib.LejaState()
     h = mhd.ctx.bind_stream()
-    # launch batching only: expected degree from earlier calls of this order at a
-    # similar interval scale (quarter-octave buckets of theta)
-    hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
-    lib.xmhd_leja_hint(h, int(_degree_hint.get(hkey, 2)))
-    rc = lib.xmhd_leja_start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
-                             float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
-                             float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
-                             int(coeffs.size), ctypes.byref(st))
-    _lib.check(rc, "xmhd_leja_start")
-    while st.status == _lib.LEJA_NEED_COEFFS:
-        chunk, grown = _grow(l, q, theta, chunk, coeffs, st.m)
-        coeffs = np.ascontiguousarray(grown)
-        _speculate(l, q, theta, min(2 * chunk, LEJA_MAX))
-        rc = lib.xmhd_leja_resume(h, _ptr_d(coeffs), int(coeffs.size), ctypes.byref(st))
-        _lib.check(rc, "xmhd_leja_resume")
-    _drop_speculation(l, q, theta)
-    _degree_hint[hkey] = int(st.iterations)
+    rc = lib.xmhd_leja_start_async(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
+                                   float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
+                                   float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
+                                   int(coeffs.size))
+    _lib.check(rc, "xmhd_leja_start_async")
+    st = drive_fused(lib, h, l, q, theta, coeffs)
     lin.rhs.calls += st.rhs_calls
     if st.status == _lib.LEJA_RHS_NONFINITE:
         # the reference raises from inside the matvec (mhd.py:225-231); rebuild

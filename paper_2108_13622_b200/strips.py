@@ -407,27 +407,13 @@ def leja_peer(mhd, lin, l, vd, dt, q, theta, tol, xi):
     mhd.exchange(lin.base_state, mhd.state_halo)
     mhd._set_halo(mhd.state_halo, mhd.dir_halo)
     h = mhd.ctx.bind_stream()
-    chunk = 64
-    coeffs = np.ascontiguousarray(leja._newton_coeffs(l, q, theta, chunk))
-    leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
-    hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
-    lib.xmhd_leja_hint(h, int(leja._degree_hint.get(hkey, 2)))
+    coeffs = np.ascontiguousarray(leja._newton_coeffs(l, q, theta, 64))
     rc = lib.xmhd_leja_p2p_start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
                                  float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
                                  float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
                                  int(coeffs.size))
     _lib.check(rc, "xmhd_leja_p2p_start")
-    st = _lib.LejaState()
-    _lib.check(lib.xmhd_leja_p2p_run(h, ctypes.byref(st)), "xmhd_leja_p2p_run")
-    while st.status == _lib.LEJA_NEED_COEFFS:
-        chunk, grown = leja._grow(l, q, theta, chunk, coeffs, st.m)
-        coeffs = np.ascontiguousarray(grown)
-        leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
-        _lib.check(lib.xmhd_leja_set_coeffs(h, _ptr_d(coeffs), int(coeffs.size)),
-                   "xmhd_leja_set_coeffs")
-        _lib.check(lib.xmhd_leja_p2p_run(h, ctypes.byref(st)), "xmhd_leja_p2p_run")
-    leja._degree_hint[hkey] = int(st.iterations)
-    return st
+    return leja.drive_fused(lib, h, l, q, theta, coeffs, peer=True)
 
 
 def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
@@ -440,7 +426,6 @@ def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
     backend = CudaStripBackend(mhd, lin)
     if mhd.peer_transport():
         st = leja_peer(mhd, lin, l, vd, dt, q, theta, tol, xi)
-        leja._drop_speculation(l, q, theta)
         return _finish(l, lin, mhd, backend, vd, v, st)
 
     def coeff_fn(chunk):
