@@ -84,6 +84,20 @@ int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f);
 int xmhd_jvp(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w,
              double* out, int* called, double* out_norm);
 
+/* Power iteration of estimate_alpha (linearize.py:113-135; replaces the loop at
+ * linearize.py:118-133 that the reference runs over jvp and np.linalg.norm).
+ * w0: start vector (read only; a zero w0 starts from ones as linearize.py:115-116).
+ * w: out, the last normalised iterate (SpectralEstimate.vector).  work: n-double
+ * scratch.  Stops when |mag - mags[-2]| or |mag - mags[-3]| <= tol*mag, or after
+ * maxit (<= 100) iterations.  mags[0..*nit): the magnitudes ||J w||;
+ * *rhs_calls: RHS evaluations; *status: 0 = alpha from max(mags[-3:]),
+ * 1 = magnitude < 1e-300 or non-finite (alpha 0, no vector).  Returns
+ * XMHD_NONFINITE when an RHS evaluation produced non-finite cells (the
+ * reference raises RhsBlowupError from inside jvp).  Single-domain contexts. */
+int xmhd_power(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w0,
+               double* w, double* work, int maxit, double tol, double* mags, int* nit,
+               int* rhs_calls, int* status);
+
 /* np.linalg.norm(x) (deterministic device reduction). */
 int xmhd_norm(xmhd_ctx* ctx, const double* x, long long n, double* out);
 

@@ -51,6 +51,7 @@ _SIGS = {
     "xmhd_set_halo": (_I, [_P, _P, _P, _P, _P]),
     "xmhd_rhs": (_I, [_P, _P, _P]),
     "xmhd_jvp": (_I, [_P, _P, _P, _D, _P, _P, _PI, _PD]),
+    "xmhd_power": (_I, [_P, _P, _P, _D, _P, _P, _P, _I, _D, _PD, _PI, _PI, _PI]),
     "xmhd_norm": (_I, [_P, _P, _L, _PD]),
     "xmhd_lincomb": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD, _PI]),
     "xmhd_divide": (_I, [_P, _P, _P, _D, _L, _PD]),

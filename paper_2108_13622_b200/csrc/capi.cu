@@ -49,6 +49,8 @@ struct xmhd_ctx {
   double* coef_h = nullptr;    // pinned [512]: staging of coefficient extensions
   double* kry_d = nullptr;     // [512] MGS coefficient slots (Krylov baseline)
   double* kry_h = nullptr;     // pinned [512]
+  PowerCtl* pctl = nullptr;    // device power iteration (allocated on first use)
+  PowerCtl* pctl_h = nullptr;  // pinned mirror
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -356,6 +358,8 @@ int xmhd_destroy(xmhd_ctx* c) {
   cudaFreeHost(c->h_int);
   cudaFree(c->kry_d);
   cudaFreeHost(c->kry_h);
+  cudaFree(c->pctl);
+  cudaFreeHost(c->pctl_h);
   cudaFreeHost(c->coef_h);
   for (int q = 0; q < P2P_MAX; ++q)
     if (c->p2p_peer[q]) cudaIpcCloseMemHandle(c->p2p_peer[q]);
@@ -443,6 +447,77 @@ int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const
   rc = fetch_bad(c, &bad);
   if (rc) return rc;
   return bad ? XMHD_NONFINITE : XMHD_OK;
+}
+
+// Device-resident power iteration of estimate_alpha (linearize.py:113-135).
+// Per iteration one fused JVP (MODE_JVP reading its FD step from the control
+// block, last block: ||J w||, magnitude list, stopping test) and one division
+// (w = J w / mag, ||w||, next FD step); the host enqueues batches of
+// iterations and reads the 1 KB control block once per batch.
+int xmhd_power(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w0,
+               double* w, double* work, int maxit, double tol, double* mags, int* nit,
+               int* rhs_calls, int* status) {
+  if (!c || !u || !fu || !w0 || !w || !work || !mags || !nit || !rhs_calls || !status)
+    return fail(XMHD_BADARG, "null arg");
+  if (maxit < 1 || maxit > POWER_MAXIT) return fail(XMHD_BADARG, "maxit out of range");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "y-strip contexts use the host power loop");
+  if (!c->pctl) {
+    CK(cudaMalloc(&c->pctl, sizeof(PowerCtl)));
+    CK(cudaMallocHost(&c->pctl_h, sizeof(PowerCtl)));
+  }
+  const long long n = NF * c->g.plane;
+  // w = w0 / ||w0||, a vector of ones when w0 == 0 (linearize.py:114-117)
+  CK(launch_norm(w0, n, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  double wn0 = c->h_dbl[0];
+  if (wn0 == 0.0) {
+    CK(launch_fill(work, n, 1.0, c->stream));
+    CK(launch_norm(work, n, redbuf(c), c->stream));
+    c->launches += 2;
+    rc = fetch_doubles(c, 1);
+    if (rc) return rc;
+    wn0 = c->h_dbl[0];
+  } else {
+    CK(cudaMemcpyAsync(work, w0, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  PowerCtl* h = c->pctl_h;
+  std::memset(h, 0, sizeof(PowerCtl));
+  h->status = PW_RUNNING;
+  h->maxit = maxit;
+  h->tol = tol;
+  h->unorm = unorm;
+  h->div = wn0;
+  h->force_ieee = c->force_ieee ? 1 : 0;
+  CK(cudaMemcpyAsync(c->pctl, h, sizeof(PowerCtl), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  CK(launch_power_divide(w, work, n, c->pctl, redbuf(c), c->stream));
+  c->launches++;
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.fu = fu;
+  a.dir = w;
+  a.out = work;
+  a.pctl = c->pctl;
+  int launched = 0, batch = 6;   // typical refreshes stop after 4-7 iterations
+  for (;;) {
+    for (int b = 0; b < batch && launched < maxit; ++b, ++launched) {
+      CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
+      CK(launch_power_divide(w, work, n, c->pctl, redbuf(c), c->stream));
+      c->launches += 2;
+    }
+    CK(cudaMemcpyAsync(h, c->pctl, sizeof(PowerCtl), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h->status != PW_RUNNING || launched >= maxit) break;
+    batch = 8;
+  }
+  if (h->status == PW_RUNNING) return fail(XMHD_CUDA_ERROR, "power iteration left RUNNING");
+  *nit = h->k;
+  *rhs_calls = h->rhs_calls;
+  for (int k = 0; k < h->k; ++k) mags[k] = h->mags[k];
+  *status = h->status == PW_DONE ? 0 : 1;
+  return h->status == PW_RHS_BAD ? XMHD_NONFINITE : XMHD_OK;
 }
 
 int xmhd_norm(xmhd_ctx* c, const double* x, long long n, double* out) {

@@ -43,6 +43,36 @@ enum LejaStatus {
   LJ_PEER_TIMEOUT = 6, // y-strips over peer memory: a peer never posted its sums
 };
 
+// Device-resident power iteration of estimate_alpha (linearize.py:113-135):
+// one fused JVP (J w, ||J w||) and one division kernel (w = J w / mag, ||w||,
+// next FD step) per iteration; both last blocks update this block, so the
+// host only enqueues kernels and reads the block back once per batch.
+constexpr int POWER_MAXIT = 100;   // linearize.py _POWER_MAXIT
+struct PowerCtl {
+  int status;       // PowerStatus
+  int k;            // magnitudes recorded
+  int maxit;
+  int rhs_calls;    // JVPs evaluated (zero directions excluded)
+  int stop;         // converged (or maxit): the next division is the last kernel
+  int pad_;
+  double unorm;     // ||u|| of the frozen linearization
+  double tol;       // relative change accepted against mags[-2] or mags[-3]
+  double div;       // divisor of the next division (||w0||, then mag)
+  double wn;        // ||w|| of the current iterate
+  double eps;       // FD step of the next JVP
+  Divisor epsd;
+  int force_ieee;
+  int pad2_;
+  double mags[POWER_MAXIT];
+};
+
+enum PowerStatus {
+  PW_RUNNING = 0,
+  PW_DONE = 1,      // converged or maxit: alpha = safety * max(mags[-3:])
+  PW_ZERO = 2,      // magnitude < 1e-300 or non-finite: alpha = 0, no vector
+  PW_RHS_BAD = 3,   // non-finite RHS inside the JVP: the reference raises
+};
+
 constexpr int P2P_MAX = 8;   // ranks of one NVLink / NVSwitch node
 
 // Peer-memory transport of the y-strip Leja loop.  The fused iteration kernel
@@ -88,6 +118,7 @@ struct StencilArgs {
   double* ext_sums;    // MODE_LEJA y-strips: [sum y'^2, sum p'^2, bad] of this rank
   int units_x, nunits, seg_rows;
   P2PArgs p2p;         // MODE_LEJA y-strips over peer memory
+  PowerCtl* pctl;      // MODE_JVP inside the device power iteration (eps from here)
 };
 
 #ifndef XB_SW
@@ -143,6 +174,12 @@ cudaError_t launch_leja_finalize(LejaCtl* ctl, const double* sums, const double*
 cudaError_t launch_leja_pack_halo(const LejaCtl* ctl, const double* y0, const double* y1, int nx,
                                   int ny, double* send_lo, double* send_hi, double* halo_lo,
                                   double* halo_hi, int mirror_lo, int mirror_hi, cudaStream_t s);
+// Power iteration: out = x / pctl->div (IEEE) and the control update from
+// ||out|| (next FD step, or the end of the iteration).  No-op unless RUNNING.
+cudaError_t launch_power_divide(double* out, const double* x, long long n, PowerCtl* pctl,
+                                RedBuf rb, cudaStream_t s);
+// x[i] = v.
+cudaError_t launch_fill(double* x, long long n, double v, cudaStream_t s);
 // result[0] = sum of squares (no sqrt; y-strip partial norms).
 cudaError_t launch_sumsq(const double* x, long long n, RedBuf rb, cudaStream_t s);
 // Generic Leja update for an arbitrary (host-supplied) matvec result w.
@@ -266,6 +303,49 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
                        ny < 1e-300 ? 1e-300 : ny);
   ctl->epsd = make_divisor_dev(ctl->eps);
   if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
+}
+
+// Power iteration, after the fused JVP reduced sum((J w)^2) (linearize.py:121-133).
+__device__ __forceinline__ void power_after_jvp(PowerCtl* pc, double sum, int bad) {
+  pc->rhs_calls += 1;
+  if (bad) {
+    pc->status = PW_RHS_BAD;
+    return;
+  }
+  const double mag = sqrt(sum);
+  if (mag < 1e-300 || !isfinite(mag)) {
+    pc->status = PW_ZERO;
+    return;
+  }
+  const int k = pc->k;
+  pc->mags[k] = mag;
+  pc->k = k + 1;
+  pc->div = mag;
+  const double lim = __dmul_rn(pc->tol, mag);
+  if ((k + 1 >= 3 && (fabs(__dsub_rn(mag, pc->mags[k - 1])) <= lim ||
+                      fabs(__dsub_rn(mag, pc->mags[k - 2])) <= lim)) ||
+      k + 1 >= pc->maxit)
+    pc->stop = 1;
+}
+
+// Power iteration, after w = x / div and its norm (linearize.py:115-116, 124;
+// the next jvp's eps, linearize.py:62-65).
+__device__ __forceinline__ void power_after_divide(PowerCtl* pc, double sum) {
+  const double kSqrtEps = 1.4901161193847656e-08;
+  const double wn = sqrt(sum);
+  pc->wn = wn;
+  if (pc->stop) {
+    pc->status = PW_DONE;
+    return;
+  }
+  if (wn == 0.0) {   // jvp of a zero vector is zero (no RHS call): magnitude 0
+    pc->status = PW_ZERO;
+    return;
+  }
+  pc->eps = __ddiv_rn(__dmul_rn(kSqrtEps, pc->unorm > 1.0 ? pc->unorm : 1.0),
+                      wn < 1e-300 ? 1e-300 : wn);
+  pc->epsd = make_divisor_dev(pc->eps);
+  if (pc->force_ieee) pc->epsd.kind = DIV_IEEE;
 }
 
 // Control-block start from sum(v^2) (leja.py:121-123): y = v, p = c0*v done by the caller.

@@ -234,6 +234,14 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     cm = __ldg(a.coeffs + m);
   }
 
+  if (MODE == MODE_JVP && a.pctl) {
+    // device power iteration: the FD step comes from the control block
+    const PowerCtl* pc = a.pctl;
+    if (pc->status != PW_RUNNING) return;
+    eps = pc->eps;
+    epsd = pc->epsd;
+  }
+
   double acc0 = 0.0, acc1 = 0.0;
   int bad = 0;
 
@@ -548,7 +556,9 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     const double sy = sum_partials(a.partials, nblk, 2, 0);
     const double sp = (MODE == MODE_LEJA) ? sum_partials(a.partials, nblk, 2, 1) : 0.0;
     if (t == 0) {
-      if (MODE == MODE_JVP) {
+      if (MODE == MODE_JVP && a.pctl) {
+        power_after_jvp(a.pctl, sy, *((volatile int*)a.bad));
+      } else if (MODE == MODE_JVP) {
         a.result[0] = sqrt(sy);
       } else if (MODE == MODE_LEJA && XR != XR_NONE) {
         // y-strips over peer memory: all-reduce the three sums, then every rank

@@ -130,6 +130,24 @@ __global__ void __launch_bounds__(VT) divide_kernel(double* __restrict__ out,
   if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = sqrt(tot[0]);
 }
 
+// One division of the device power iteration (linearize.py:115-116, 124):
+// out = x / div, then ||out|| and the next FD step in the last block.
+__global__ void __launch_bounds__(VT) power_divide_kernel(double* __restrict__ out,
+                                                          const double* __restrict__ x,
+                                                          long long n, PowerCtl* pc, RedBuf rb) {
+  if (pc->status != PW_RUNNING) return;
+  const double d = pc->div;
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    const double q = __ddiv_rn(__ldg(x + i), d);
+    out[i] = q;
+    acc[0] = __fma_rn(q, q, acc[0]);
+  }
+  double tot[1];
+  if (grid_reduce<1, false>(acc, rb, tot)) power_after_divide(pc, tot[0]);
+}
+
 __global__ void __launch_bounds__(VT) diffnorm_kernel(const double* __restrict__ a,
                                                       const double* __restrict__ b,
                                                       long long n, RedBuf rb) {
@@ -482,6 +500,23 @@ cudaError_t launch_lincomb(double* out, long long n, const double* const* v, con
 cudaError_t launch_divide(double* out, const double* x, double d, long long n, int want_norm,
                           RedBuf rb, cudaStream_t s) {
   divide_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, x, d, n, want_norm, rb);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(VT) fill_kernel(double* __restrict__ x, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT)
+    x[i] = v;
+}
+
+cudaError_t launch_fill(double* x, long long n, double v, cudaStream_t s) {
+  fill_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(x, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_power_divide(double* out, const double* x, long long n, PowerCtl* pctl,
+                                RedBuf rb, cudaStream_t s) {
+  power_divide_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, x, n, pctl, rb);
   return cudaGetLastError();
 }
 

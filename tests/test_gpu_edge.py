@@ -224,3 +224,88 @@ def test_checkpoint_roundtrip(tmp_path):
     assert path.read_bytes() == mhd_np.checkpoint_bytes(q, 0.05, 0.08, 1.25)
     loaded, t = xb.read_checkpoint(path)
     assert t == 1.25 and np.array_equal(loaded.data, q)
+
+
+def _host_power(xb, lin, w0, prev=None):
+    from paper_2108_13622_b200 import linearize
+    old = linearize._HOST_POWER
+    linearize._HOST_POWER = True
+    try:
+        if prev is not None:
+            return xb.estimate_alpha(lin, prev)
+        return xb.estimate_alpha(lin, None, rng=np.random.default_rng(w0))
+    finally:
+        linearize._HOST_POWER = old
+
+
+@pytest.mark.parametrize("refl,mu0", [(False, 1.0), (True, 0.7)])
+def test_device_power_iteration_matches_host_loop_and_oracle(refl, mu0):
+    """xmhd_power (one device-resident loop) against the host loop over the
+    fused JVP and the NumPy oracle (linearize.py:113-135): same iteration
+    count and RHS calls, alpha and the warm-start vector within rounding of
+    the norm summation order; then a warm-started refresh."""
+    from oracle import leja_np as olj
+    xb, q, op, lin, oop, olin = _mhd(refl=refl, mu0=mu0)
+    c0 = op.calls
+    dev = xb.estimate_alpha(lin, None, rng=np.random.default_rng(5))
+    c1 = op.calls
+    host = _host_power(xb, lin, 5)
+    c2 = op.calls
+    ocalls = oop.calls
+    ref = olj.power_alpha(olin, None, rng=np.random.default_rng(5))
+    assert c1 - c0 == c2 - c1 == oop.calls - ocalls == len(ref.mags)
+    assert len(dev.mags) == len(host.mags) == len(ref.mags)
+    assert abs(dev.alpha - ref.alpha) <= 1e-12 * ref.alpha
+    assert abs(dev.alpha - host.alpha) <= 1e-13 * host.alpha
+    assert rel(dev.vector, ref.vector) <= 1e-10
+    # warm start from the previous vector once the cache expires (linearize.py:108-109)
+    stale = xb.SpectralEstimate(alpha=dev.alpha, age_steps=dev.interval - 1, vector=dev.vector)
+    ostale = olj.Spectrum(ref.alpha, ref.interval - 1, ref.interval, ref.safety, ref.vector,
+                          ref.mags)
+    dev2 = xb.estimate_alpha(lin, stale)
+    ref2 = olj.power_alpha(olin, ostale)
+    assert len(dev2.mags) == len(ref2.mags)
+    assert abs(dev2.alpha - ref2.alpha) <= 1e-12 * ref2.alpha
+    assert torch.equal(stale.vector, dev.vector)    # the start vector is not mutated
+
+
+def test_device_power_zero_start_and_zero_operator():
+    """A zero start vector restarts from ones (linearize.py:115-116); a zero
+    Jacobian (uniform state, F = 0 and J w = 0) gives alpha 0 and no vector."""
+    from oracle import leja_np as olj
+    xb, q, op, lin, oop, olin = _mhd()
+    zero = xb.SpectralEstimate(alpha=1.0, age_steps=49,
+                               vector=torch.zeros(q.size, dtype=torch.float64, device="cuda"))
+    dev = xb.estimate_alpha(lin, zero)
+    ref = olj.power_alpha(olin, olj.Spectrum(1.0, 49, 50, 1.25, np.zeros(q.size), []))
+    assert len(dev.mags) == len(ref.mags)
+    assert abs(dev.alpha - ref.alpha) <= 1e-12 * ref.alpha
+    # uniform state: every JVP is exactly zero -> magnitude 0 -> alpha 0 after one RHS call
+    u = np.zeros((8, 12, 16))
+    u[0] = 1.0
+    u[7] = 2.0
+    st = xb.StateGrid(16, 12, 0.1, 0.1, torch.from_numpy(u).cuda())
+    op2 = xb.RhsOperator(xb.MhdRhs(st, xb.MHDParams(mu=0.01, eta=0.01, kappa=0.01)))
+    lin2 = xb.FrozenLinearization(op2, st.flat())
+    c = op2.calls
+    est = xb.estimate_alpha(lin2, None, rng=np.random.default_rng(0))
+    assert est.alpha == 0.0 and est.vector is None and op2.calls == c + 1
+
+
+def test_device_power_nonfinite_rhs_raises_like_reference():
+    """A NaN in the start vector makes u + eps*w non-finite: the power iteration raises
+    RhsBlowupError with the reference's message and cells (mhd.py:225-231)."""
+    from oracle import leja_np as olj, mhd_np
+    xb, q, op, lin, oop, olin = _mhd()
+    w = np.ones(q.size)
+    w[33] = np.nan      # ||w|| = nan: every iterate and eps are nan, F(u + eps*w) is not finite
+    prev_ref = olj.Spectrum(1.0, 49, 50, 1.25, w, [])
+    with pytest.raises(mhd_np.NonFiniteRhs) as ref_err:
+        olj.power_alpha(olin, prev_ref)
+    calls = op.calls
+    prev = xb.SpectralEstimate(alpha=1.0, age_steps=49, vector=torch.from_numpy(w).cuda())
+    with pytest.raises(xb.RhsBlowupError) as err:
+        xb.estimate_alpha(lin, prev)
+    assert str(err.value) == str(ref_err.value)
+    assert err.value.cells == ref_err.value.cells
+    assert op.calls == calls + 1
