@@ -40,8 +40,9 @@
 
 // L2 prefetch ahead of the per-thread loads (measured on B200, 2048^2 / 4096^2:
 // off 0.343 / 1.300 ms; rows 2 ahead + epilogue 1 ahead 0.313 / 1.243 ms;
-// epilogue 2 ahead 0.323; rows 5 ahead 0.352; bulk cp.async.bulk.prefetch
-// instead of per-line prefetches 0.339).
+// epilogue 2 ahead 0.323; rows 3 / 4 / 5 ahead 0.353 / 0.328 / 0.352; rows 3 +
+// epilogue 2 ahead 0.329; bulk cp.async.bulk.prefetch instead of per-line
+// prefetches 0.339).
 #ifndef XB_L2PF
 #define XB_L2PF 2   // row steps of the state / direction prefetch (0: no prefetch)
 #endif

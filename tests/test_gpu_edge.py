@@ -280,7 +280,8 @@ def test_device_power_zero_start_and_zero_operator():
     ref = olj.power_alpha(olin, olj.Spectrum(1.0, 49, 50, 1.25, np.zeros(q.size), []))
     assert len(dev.mags) == len(ref.mags)
     assert abs(dev.alpha - ref.alpha) <= 1e-12 * ref.alpha
-    # uniform state: every JVP is exactly zero -> magnitude 0 -> alpha 0 after one RHS call
+    # uniform state, uniform direction: u + eps*w is uniform, so F(u + eps*w) = F(u) = 0
+    # exactly, J w = 0, magnitude 0 -> alpha 0 and no vector after one RHS call
     u = np.zeros((8, 12, 16))
     u[0] = 1.0
     u[7] = 2.0
@@ -288,7 +289,9 @@ def test_device_power_zero_start_and_zero_operator():
     op2 = xb.RhsOperator(xb.MhdRhs(st, xb.MHDParams(mu=0.01, eta=0.01, kappa=0.01)))
     lin2 = xb.FrozenLinearization(op2, st.flat())
     c = op2.calls
-    est = xb.estimate_alpha(lin2, None, rng=np.random.default_rng(0))
+    ones = xb.SpectralEstimate(alpha=1.0, age_steps=49,
+                               vector=torch.ones(u.size, dtype=torch.float64, device="cuda"))
+    est = xb.estimate_alpha(lin2, ones)
     assert est.alpha == 0.0 and est.vector is None and op2.calls == c + 1
 
 
