@@ -57,6 +57,20 @@ typedef struct xmhd_leja_state {
   double ynorm;    /* ||y|| of the current Newton basis vector              */
 } xmhd_leja_state;
 
+/* Record of one asynchronous step (xmhd_async_*), read back once at its end. */
+#define XMHD_ASYNC_LEJA_MAX 32
+typedef struct xmhd_step_record {
+  int rhs_nonfinite;   /* an asynchronous RHS / JVP evaluation produced non-finite cells */
+  int jvp_calls;       /* RHS evaluations made by the asynchronous JVPs (zero w: none)   */
+  int nleja;           /* phi-actions recorded (xmhd_leja_finish_async calls)          */
+  int pad_;
+  double err_diff;     /* ||a - b|| of xmhd_diff_norms_async                          */
+  double err_ref;      /* ||b||                                                        */
+  double lc_norm;      /* ||out|| of the last xmhd_lincomb_async                       */
+  double lc_nonfinite; /* 1.0 when that combination has non-finite entries             */
+  xmhd_leja_state leja[XMHD_ASYNC_LEJA_MAX];
+} xmhd_step_record;
+
 /* Context for one (local) grid: the geometry + MHDParams captured by
  * RhsOperator(lambda flat: mhd_rhs(geometry.with_flat(flat), params))
  * (harness.py:129; mhd.py:39-48, 51-70).  `stream` is a cudaStream_t (0 = legacy). */
@@ -83,6 +97,32 @@ int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f);
  * *called = number of RHS evaluations (0 or 1); *out_norm = ||out|| (may be NULL). */
 int xmhd_jvp(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w,
              double* out, int* called, double* out_norm);
+
+/* Asynchronous single-domain steps: every call below only enqueues work on the
+ * context's stream; xmhd_async_fetch synchronises once and returns the step's
+ * record.  The host driver (integrators.step) replays the step through the
+ * synchronous entry points whenever the record shows an event the reference
+ * reacts to mid-step (a non-finite RHS raising RhsBlowupError, a phi-action
+ * needing more coefficients), so counters and results stay the reference's.
+ *   xmhd_async_begin        reset the record
+ *   xmhd_rhs_async          f = F(u) (mhd.py:127-232), non-finite cells -> record
+ *   xmhd_jvp_async          jvp (linearize.py:56-67) with ||w|| and eps on the device
+ *   xmhd_leja_loop          the whole Leja loop of the started phi-action in one
+ *                           cooperative launch (after xmhd_leja_start_async)
+ *   xmhd_leja_finish_async  p_out = the interpolant; its final state -> record
+ *   xmhd_lincomb_async      xmhd_lincomb with ||out|| and the non-finite flag -> record
+ *   xmhd_diff_norms_async   error_norm inputs (integrators.py:88-96) -> record */
+int xmhd_async_begin(xmhd_ctx* ctx);
+int xmhd_rhs_async(xmhd_ctx* ctx, const double* u, double* f);
+int xmhd_jvp_async(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                   const double* w, double* out);
+int xmhd_leja_loop(xmhd_ctx* ctx);
+int xmhd_leja_loop_available(xmhd_ctx* ctx);
+int xmhd_leja_finish_async(xmhd_ctx* ctx, double* p_out);
+int xmhd_lincomb_async(xmhd_ctx* ctx, double* out, long long n, const double* const* v,
+                       const double* coeffs, int nterms);
+int xmhd_diff_norms_async(xmhd_ctx* ctx, const double* a, const double* b, long long n);
+int xmhd_async_fetch(xmhd_ctx* ctx, xmhd_step_record* out);
 
 /* Power iteration of estimate_alpha (linearize.py:113-135; replaces the loop at
  * linearize.py:118-133 that the reference runs over jvp and np.linalg.norm).

@@ -34,6 +34,15 @@ class LejaState(ctypes.Structure):
                 ("ynorm", ctypes.c_double)]
 
 
+class StepRecord(ctypes.Structure):
+    """xmhd_step_record: the record of one asynchronous step."""
+    _fields_ = [("rhs_nonfinite", ctypes.c_int), ("jvp_calls", ctypes.c_int),
+                ("nleja", ctypes.c_int), ("pad_", ctypes.c_int),
+                ("err_diff", ctypes.c_double), ("err_ref", ctypes.c_double),
+                ("lc_norm", ctypes.c_double), ("lc_nonfinite", ctypes.c_double),
+                ("leja", LejaState * 32)]
+
+
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I = ctypes.c_int
@@ -51,6 +60,15 @@ _SIGS = {
     "xmhd_set_halo": (_I, [_P, _P, _P, _P, _P]),
     "xmhd_rhs": (_I, [_P, _P, _P]),
     "xmhd_jvp": (_I, [_P, _P, _P, _D, _P, _P, _PI, _PD]),
+    "xmhd_async_begin": (_I, [_P]),
+    "xmhd_rhs_async": (_I, [_P, _P, _P]),
+    "xmhd_jvp_async": (_I, [_P, _P, _P, _D, _P, _P]),
+    "xmhd_leja_loop": (_I, [_P]),
+    "xmhd_leja_loop_available": (_I, [_P]),
+    "xmhd_leja_finish_async": (_I, [_P, _P]),
+    "xmhd_lincomb_async": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I]),
+    "xmhd_diff_norms_async": (_I, [_P, _P, _P, _L]),
+    "xmhd_async_fetch": (_I, [_P, ctypes.POINTER(StepRecord)]),
     "xmhd_power": (_I, [_P, _P, _P, _D, _P, _P, _P, _I, _D, _PD, _PI, _PI, _PI]),
     "xmhd_norm": (_I, [_P, _P, _L, _PD]),
     "xmhd_lincomb": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD, _PI]),

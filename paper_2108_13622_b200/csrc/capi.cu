@@ -51,6 +51,13 @@ struct xmhd_ctx {
   double* kry_h = nullptr;     // pinned [512]
   PowerCtl* pctl = nullptr;    // device power iteration (allocated on first use)
   PowerCtl* pctl_h = nullptr;  // pinned mirror
+  // asynchronous steps (xmhd_async_*): device record + its pinned mirror, the
+  // control block of the device-side jvp prologue, phi-actions recorded so far
+  AsyncRec* arec = nullptr;
+  AsyncRec* arec_h = nullptr;
+  PowerCtl* jctl = nullptr;
+  int nleja_async = 0;
+  int loop_blocks = -1;        // co-resident blocks of the Leja loop kernel (-1: unknown)
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -238,7 +245,9 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.force_ieee = c->force_ieee ? 1 : 0;
   h.epoch = c->p2p_epoch;
   *c->ctl_h = h;
-  CK(cudaMemcpyAsync(c->ctl, c->ctl_h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
+  // staged from pageable memory at the call: back-to-back asynchronous
+  // phi-actions never race on the pinned mirror
+  CK(cudaMemcpyAsync(c->ctl, &h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
   CK(launch_leja_init(v, n, c->ybuf[0], c->pbuf[0], c->ctl, c->coeffs_d, redbuf(c), c->stream,
                       ext_sums));
@@ -360,6 +369,9 @@ int xmhd_destroy(xmhd_ctx* c) {
   cudaFreeHost(c->kry_h);
   cudaFree(c->pctl);
   cudaFreeHost(c->pctl_h);
+  cudaFree(c->arec);
+  cudaFreeHost(c->arec_h);
+  cudaFree(c->jctl);
   cudaFreeHost(c->coef_h);
   for (int q = 0; q < P2P_MAX; ++q)
     if (c->p2p_peer[q]) cudaIpcCloseMemHandle(c->p2p_peer[q]);
@@ -672,6 +684,132 @@ int xmhd_leja_sync(xmhd_ctx* c, xmhd_leja_state* st) {
   c->p2p_epoch = c->ctl_h->epoch;
   if (c->ctl_h->status == LJ_PEER_TIMEOUT)
     return fail(XMHD_CUDA_ERROR, "peer-memory exchange timed out (a rank stopped)");
+  return XMHD_OK;
+}
+
+// ---- asynchronous single-domain steps ------------------------------------
+// The whole Leja loop as one cooperative launch; no host read until the
+// caller synchronises (xmhd_leja_sync, or xmhd_async_fetch at a step end).
+int xmhd_leja_loop(xmhd_ctx* c) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "y-strips use the strip drivers");
+  if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
+  if (c->grid > c->loop_blocks)
+    return fail(XMHD_BADARG, "grid not co-resident: use xmhd_leja_launch batches");
+  StencilArgs a = leja_args(c);
+  CK(launch_leja_loop(a, c->grid, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_loop_available(xmhd_ctx* c) {
+  if (!c || c->g.bcy == BC_HALO) return 0;
+  if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
+  return c->grid <= c->loop_blocks ? 1 : 0;
+}
+
+static int ensure_async(xmhd_ctx* c) {
+  if (c->arec) return XMHD_OK;
+  CK(cudaMalloc(&c->arec, sizeof(AsyncRec)));
+  CK(cudaMallocHost(&c->arec_h, sizeof(AsyncRec)));
+  CK(cudaMalloc(&c->jctl, sizeof(PowerCtl)));
+  return XMHD_OK;
+}
+
+int xmhd_async_begin(xmhd_ctx* c) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  int rc = ensure_async(c);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(c->arec, 0, sizeof(AsyncRec), c->stream));
+  PowerCtl j;
+  std::memset(&j, 0, sizeof(j));
+  j.status = PW_RUNNING;
+  j.jvp_only = 1;
+  j.force_ieee = c->force_ieee ? 1 : 0;
+  CK(cudaMemcpyAsync(c->jctl, &j, sizeof(PowerCtl), cudaMemcpyHostToDevice, c->stream));
+  c->nleja_async = 0;
+  return XMHD_OK;
+}
+
+int xmhd_rhs_async(xmhd_ctx* c, const double* u, double* f) {
+  if (!c || !u || !f || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.out = f;
+  a.bad = &c->arec->bad;
+  CK(launch_stencil(MODE_RHS, a, c->grid, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_jvp_async(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w,
+                   double* out) {
+  if (!c || !u || !fu || !w || !out || !c->arec)
+    return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
+  const long long n = NF * c->g.plane;
+  CK(cudaMemsetAsync(out, 0, sizeof(double) * n, c->stream));   // zero w -> zero J w
+  CK(launch_jvp_prep(w, n, unorm, c->jctl, redbuf(c), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.dir = w;
+  a.fu = fu;
+  a.out = out;
+  a.pctl = c->jctl;
+  a.bad = &c->arec->bad;
+  CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
+  c->launches += 2;
+  return XMHD_OK;
+}
+
+int xmhd_leja_finish_async(xmhd_ctx* c, double* p_out) {
+  if (!c || !p_out || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
+  if (c->nleja_async >= ASYNC_LEJA_MAX) return fail(XMHD_BADARG, "too many phi-actions in one step");
+  const long long n = NF * c->g.plane;
+  CK(launch_leja_copy_result(p_out, c->pbuf, c->ctl, n, c->stream));
+  CK(cudaMemcpyAsync(&c->arec->leja[c->nleja_async], c->ctl, sizeof(LejaCtl),
+                     cudaMemcpyDeviceToDevice, c->stream));
+  c->nleja_async++;
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_lincomb_async(xmhd_ctx* c, double* out, long long n, const double* const* v,
+                       const double* cf, int nterms) {
+  if (!c || !out || !v || !cf || nterms < 1 || nterms > 4 || !c->arec)
+    return fail(XMHD_BADARG, "bad lincomb");
+  RedBuf rb = redbuf(c);
+  rb.result = c->arec->lc;
+  CK(launch_lincomb(out, n, v, cf, nterms, 1, rb, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_diff_norms_async(xmhd_ctx* c, const double* a, const double* b, long long n) {
+  if (!c || !a || !b || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
+  RedBuf rb = redbuf(c);
+  rb.result = c->arec->err;
+  CK(launch_diffnorm(a, b, n, rb, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_async_fetch(xmhd_ctx* c, xmhd_step_record* out) {
+  if (!c || !out || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
+  CK(cudaMemcpyAsync(&c->arec->jvp_calls, &c->jctl->rhs_calls, sizeof(int),
+                     cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->arec_h, c->arec, sizeof(AsyncRec), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const AsyncRec& r = *c->arec_h;
+  std::memset(out, 0, sizeof(*out));
+  out->rhs_nonfinite = r.bad;
+  out->jvp_calls = r.jvp_calls;
+  out->nleja = c->nleja_async;
+  out->err_diff = r.err[0];
+  out->err_ref = r.err[1];
+  out->lc_norm = r.lc[0];
+  out->lc_nonfinite = r.lc[1];
+  for (int k = 0; k < c->nleja_async; ++k) fill_state(r.leja[k], &out->leja[k]);
+  *c->ctl_h = r.leja[c->nleja_async ? c->nleja_async - 1 : 0];
   return XMHD_OK;
 }
 

@@ -54,7 +54,7 @@ struct PowerCtl {
   int maxit;
   int rhs_calls;    // JVPs evaluated (zero directions excluded)
   int stop;         // converged (or maxit): the next division is the last kernel
-  int pad_;
+  int jvp_only;     // plain asynchronous jvp: the JVP only counts its RHS call
   double unorm;     // ||u|| of the frozen linearization
   double tol;       // relative change accepted against mags[-2] or mags[-3]
   double div;       // divisor of the next division (||w0||, then mag)
@@ -202,6 +202,29 @@ cudaError_t launch_mgs(double* w, long long n, const double* v, const double* ci
 cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B, int m,
                                   double scale, RedBuf rb, cudaStream_t s);
 
+// The whole single-domain Leja loop in one cooperative launch (grid must be
+// co-resident: grid <= leja_loop_max_blocks).
+cudaError_t launch_leja_loop(const StencilArgs& a, int grid, cudaStream_t s);
+int leja_loop_max_blocks(int nsm);
+// p_out = pbuf[ctl->cur] (the interpolant of a finished call; no host read of cur).
+cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf, const LejaCtl* ctl,
+                                    long long n, cudaStream_t s);
+// jvp prologue on the device: sum(w^2) -> ||w||, eps and its divisor in jc
+// (status PW_RUNNING), or status PW_ZERO for a zero vector (linearize.py:62-65).
+cudaError_t launch_jvp_prep(const double* w, long long n, double unorm, PowerCtl* jc, RedBuf rb,
+                            cudaStream_t s);
+
+// Record of one asynchronous step (read back once, at its end).
+constexpr int ASYNC_LEJA_MAX = 32;
+struct AsyncRec {
+  int bad;          // an RHS / JVP evaluation produced non-finite cells
+  int jvp_calls;    // RHS evaluations of the asynchronous JVPs
+  int pad_[2];
+  double err[2];    // ||a - b||, ||b|| of the error norm
+  double lc[2];     // ||out||, non-finite flag of the flagged linear combination
+  LejaCtl leja[ASYNC_LEJA_MAX];   // final control block of each phi-action
+};
+
 // Kernels of the peer-memory strip driver (stencil.cu / vec.cu).
 cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s);
 // Emulation of P ranks on one GPU: ONE cooperative launch over all ranks'
@@ -308,6 +331,7 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
 // Power iteration, after the fused JVP reduced sum((J w)^2) (linearize.py:121-133).
 __device__ __forceinline__ void power_after_jvp(PowerCtl* pc, double sum, int bad) {
   pc->rhs_calls += 1;
+  if (pc->jvp_only) return;   // non-finite cells are recorded in the caller's flag
   if (bad) {
     pc->status = PW_RHS_BAD;
     return;

@@ -36,7 +36,10 @@
 #include <cfloat>
 #include <climits>
 #include <type_traits>
+#include <cooperative_groups.h>
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 // L2 prefetch ahead of the per-thread loads (measured on B200, 2048^2 / 4096^2:
 // off 0.343 / 1.300 ms; rows 2 ahead + epilogue 1 ahead 0.313 / 1.243 ms;
@@ -157,7 +160,15 @@ __device__ __forceinline__ double sum_partials(const double* p, int nblk, int st
 // Exchange kind of a MODE_LEJA launch: none (single domain, or y-strips over
 // NCCL with ext_sums), peer memory (one launch per rank), or P ranks emulated
 // in one cooperative launch on one GPU.
-enum { XR_NONE = 0, XR_PEER = 1, XR_EMUL = 2 };
+// XR_LOOP: the single-domain persistent loop (leja_loop_kernel), where y and p
+// are rewritten between terms inside one launch, so their loads bypass L1.
+enum { XR_NONE = 0, XR_PEER = 1, XR_EMUL = 2, XR_LOOP = 3 };
+
+// Load of data another block rewrites inside the same launch (XR_LOOP): L2 only.
+template <bool COH>
+__device__ __forceinline__ double ld_dir(const double* p) {
+  return COH ? __ldcg(p) : __ldg(p);
+}
 
 // y' of boundary row o of this strip into the ghost-row buffers it feeds
 // ([field][2][nx]): rows 0, 1 -> the rank below (its rows ny, ny+1) or, at a
@@ -184,6 +195,8 @@ __device__ __forceinline__ void push_ghost(double* dlo, int mlo, double* dhi, in
 template <int MODE, int KX, int KY, int XR>
 __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid,
                                              const int nblk) {
+  constexpr bool P2P = (XR == XR_PEER || XR == XR_EMUL);
+  constexpr bool COH = (XR == XR_LOOP);
   extern __shared__ __align__(16) double smem[];
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
   double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
@@ -212,18 +225,22 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   double* push_lo = nullptr;
   double* push_hi = nullptr;
   if (MODE == MODE_LEJA) {
-    const LejaCtl* c = a.ctl;
+    const volatile LejaCtl* c = a.ctl;   // rewritten by the last block of every term
     if (c->status != LJ_RUNNING) return;
     const int cur = c->cur, m = c->m;
-    if (XR != XR_NONE) {
+    if (P2P) {
       hlo_dir = a.p2p.halo_lo_dir[cur];
       hhi_dir = a.p2p.halo_hi_dir[cur];
       push_lo = a.p2p.dst_lo[cur ^ 1];
       push_hi = a.p2p.dst_hi[cur ^ 1];
     }
     eps = c->eps;
-    epsd = c->epsd;
-    thd = c->thetad;
+    epsd.d = c->epsd.d;
+    epsd.r = c->epsd.r;
+    epsd.kind = c->epsd.kind;
+    thd.d = c->thetad.d;
+    thd.r = c->thetad.r;
+    thd.kind = c->thetad.kind;
     zero_dir = c->zero_dir;
     dir = a.ybuf[cur];
     yout = a.ybuf[cur ^ 1];
@@ -250,13 +267,13 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
     const long long n = (long long)NF * g.plane;
     for (long long i = (long long)bid * SW + t; i < n; i += (long long)nblk * SW) {
-      const double y = dir[i];
+      const double y = ld_dir<COH>(dir + i);
       const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
-      const double pn = __dadd_rn(pin[i], __dmul_rn(cm, yn));
+      const double pn = __dadd_rn(ld_dir<COH>(pin + i), __dmul_rn(cm, yn));
       yout[i] = yn;
       pout[i] = pn;
-      if (XR != XR_NONE) {
+      if (P2P) {
         const int f = (int)(i / g.plane);
         const long long rem = i - (long long)f * g.plane;
         const int o = (int)(rem / g.nx), c = (int)(rem - (long long)o * g.nx);
@@ -298,7 +315,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-          if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+          if (MODE != MODE_RHS) nd[f] = ld_dir<COH>(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
         }
       }
 
@@ -372,8 +389,8 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
             const unsigned i = obase + (unsigned)f * plane;
             efu[f] = __ldg(a.fu + i);
             if (MODE == MODE_LEJA) {
-              ey[f] = __ldg(dir + i);
-              ep[f] = __ldg(pin + i);
+              ey[f] = ld_dir<COH>(dir + i);
+              ep[f] = ld_dir<COH>(pin + i);
             }
           }
         }
@@ -393,7 +410,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
               nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+              if (MODE != MODE_RHS) nd[f] = ld_dir<COH>(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
             }
           }
           Prim p;
@@ -517,7 +534,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
               const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
               yout[i] = yn;
               pout[i] = pn;
-              if (XR != XR_NONE)
+              if (P2P)
                 push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
                            g.nx, c_out, yn);
               acc0 = __fma_rn(yn, yn, acc0);
@@ -545,7 +562,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     a.partials[2 * bid + 1] = s1;
     // peer memory: this block's ghost-row stores to the neighbours must be
     // visible system-wide before the last block publishes the epoch
-    if (XR != XR_NONE) __threadfence_system();
+    if (P2P) __threadfence_system();
     else __threadfence();
     const unsigned prev = atomicAdd(a.ticket, 1u);
     am_last = (prev == (unsigned)nblk - 1);
@@ -561,7 +578,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         power_after_jvp(a.pctl, sy, *((volatile int*)a.bad));
       } else if (MODE == MODE_JVP) {
         a.result[0] = sqrt(sy);
-      } else if (MODE == MODE_LEJA && XR != XR_NONE) {
+      } else if (MODE == MODE_LEJA && P2P) {
         // y-strips over peer memory: all-reduce the three sums, then every rank
         // runs the identical control update
         LejaCtl* c = a.ctl;
@@ -607,6 +624,22 @@ template <int KX, int KY>
 __global__ void __launch_bounds__(SW, SW_MINB) leja_emul_kernel(const StencilArgs* args, int nblk) {
   const int rank = blockIdx.x / nblk;
   stencil_body<MODE_LEJA, KX, KY, XR_EMUL>(args[rank], blockIdx.x - rank * nblk, nblk);
+}
+
+// The whole Leja loop of one single-domain phi-action in ONE cooperative
+// launch: a term, a grid-wide barrier (y', p' and the control block complete),
+// the next term, until the control block leaves RUNNING (converged, blow-up,
+// non-finite RHS, 499 terms, or the end of the device coefficient table).
+// No host round trip per term: the host enqueues a whole phi-action and
+// everything after it without waiting.
+template <int KX, int KY>
+__global__ void __launch_bounds__(SW, SW_MINB) leja_loop_kernel(const StencilArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  for (;;) {
+    stencil_body<MODE_LEJA, KX, KY, XR_LOOP>(a, blockIdx.x, gridDim.x);
+    grid.sync();
+    if (((volatile const LejaCtl*)a.ctl)->status != LJ_RUNNING) break;
+  }
 }
 
 size_t stencil_smem_bytes() {
@@ -729,7 +762,36 @@ cudaError_t launch_emul_one(const StencilArgs* args_dev, int nranks, int nblk, c
                                      dim3(SW), kargs, stencil_smem_bytes(), s);
 }
 
+template <int KX, int KY>
+cudaError_t launch_loop_one(const StencilArgs& a, int grid, cudaStream_t s) {
+  static bool done = false;
+  cudaError_t err = smem_attr_once(leja_loop_kernel<KX, KY>, done);
+  if (err != cudaSuccess) return err;
+  void* kargs[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((const void*)leja_loop_kernel<KX, KY>, dim3(grid), dim3(SW),
+                                     kargs, stencil_smem_bytes(), s);
+}
+
 }  // namespace
+
+cudaError_t launch_leja_loop(const StencilArgs& a, int grid, cudaStream_t s) {
+  return with_div_kinds(a.g, [&](auto X, auto Y) {
+    return launch_loop_one<decltype(X)::value, decltype(Y)::value>(a, grid, s);
+  });
+}
+
+// Co-resident blocks of the loop kernel on the whole device.
+int leja_loop_max_blocks(int nsm) {
+  int n = 0;
+  static bool done = false;
+  if (smem_attr_once(leja_loop_kernel<DIV_MUL, DIV_MUL>, done) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, leja_loop_kernel<DIV_MUL, DIV_MUL>, SW,
+                                                    stencil_smem_bytes()) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n * nsm;
+}
 
 cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s) {
   return with_div_kinds(a.g, [&](auto X, auto Y) {

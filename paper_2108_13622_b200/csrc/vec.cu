@@ -514,6 +514,45 @@ cudaError_t launch_fill(double* x, long long n, double v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(VT) leja_copy_result_kernel(double* __restrict__ out,
+                                                              const double* p0, const double* p1,
+                                                              const LejaCtl* ctl, long long n) {
+  const double* __restrict__ src = ctl->cur ? p1 : p0;
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT)
+    out[i] = src[i];
+}
+
+cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf, const LejaCtl* ctl,
+                                    long long n, cudaStream_t s) {
+  leja_copy_result_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(p_out, pbuf[0], pbuf[1], ctl, n);
+  return cudaGetLastError();
+}
+
+// jvp prologue (linearize.py:62-65) without a host round trip.
+__global__ void __launch_bounds__(VT) jvp_prep_kernel(const double* __restrict__ w, long long n,
+                                                      double unorm, PowerCtl* jc, RedBuf rb) {
+  double acc[1] = {0.0};
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    const double v = __ldg(w + i);
+    acc[0] = __fma_rn(v, v, acc[0]);
+  }
+  double tot[1];
+  if (grid_reduce<1, false>(acc, rb, tot)) {
+    jc->stop = 0;
+    jc->status = PW_RUNNING;
+    jc->unorm = unorm;
+    power_after_divide(jc, tot[0]);   // wn == 0 -> PW_ZERO, else the FD step
+  }
+}
+
+cudaError_t launch_jvp_prep(const double* w, long long n, double unorm, PowerCtl* jc, RedBuf rb,
+                            cudaStream_t s) {
+  jvp_prep_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(w, n, unorm, jc, rb);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_power_divide(double* out, const double* x, long long n, PowerCtl* pctl,
                                 RedBuf rb, cudaStream_t s) {
   power_divide_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, x, n, pctl, rb);

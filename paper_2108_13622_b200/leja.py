@@ -16,6 +16,7 @@ a device kernel around the caller's matvec.
 """
 
 import ctypes
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -289,6 +290,83 @@ def apply_phi_leja(l, matvec, v, dt, shift, tol):
     return _apply_generic(l, matvec, v, dt, shift, tol, xi)
 
 
+# Grids up to this many cells run the Leja loop as one cooperative launch per
+# phi-action (xmhd_leja_loop); larger ones, where a term costs hundreds of
+# microseconds, keep the host-paced batches of drive_fused (which also extend
+# the coefficient table ahead of the device without stopping it).
+LOOP_MAX_CELLS = int(os.environ.get("XMHD_LOOP_MAX_CELLS", str(1 << 20)))
+
+
+def loop_available(mhd):
+    """True when phi-actions on this operator run as one device loop."""
+    ctx = mhd.ctx
+    ok = getattr(ctx, "loop_ok", None)
+    if ok is None:
+        ok = (ctx.nx * ctx.ny <= LOOP_MAX_CELLS and
+              bool(_lib.load().xmhd_leja_loop_available(ctx.h)))
+        ctx.loop_ok = ok
+    return ok
+
+
+def drive_loop(lib, h, l, q, theta, coeffs):
+    """Device loop with the reference's chunk growth (leja.py:128-130) at the
+    terms where the table ends: the loop stops with NEED_COEFFS, the grown
+    chunk's new entries are appended, and the loop resumes."""
+    st = _lib.LejaState()
+    chunk = 64
+    size = coeffs.size
+    while True:
+        _lib.check(lib.xmhd_leja_loop(h), "xmhd_leja_loop")
+        _lib.check(lib.xmhd_leja_sync(h, ctypes.byref(st)), "xmhd_leja_sync")
+        if st.status != _lib.LEJA_NEED_COEFFS:
+            return st
+        chunk, grown = _grow(l, q, theta, chunk, _cache().get((l, q, theta), coeffs), st.m)
+        arr = np.ascontiguousarray(grown)
+        _lib.check(lib.xmhd_leja_extend(h, _ptr_d(arr), size, arr.size), "xmhd_leja_extend")
+        size = arr.size
+
+
+def _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs):
+    rc = lib.xmhd_leja_start_async(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
+                                   float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
+                                   float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
+                                   int(coeffs.size))
+    _lib.check(rc, "xmhd_leja_start_async")
+
+
+def apply_phi_async(l, lin, v, dt, shift, tol):
+    """One phi-action enqueued without any host wait (asynchronous steps).
+
+    Only the first coefficient chunk is on the device: a call that reaches its
+    end stops with NEED_COEFFS, which the step's record reports and the caller
+    answers by replaying the step synchronously.  Returns the device vector
+    that receives the interpolant; its final state goes to the step record.
+    """
+    _check_order(l)
+    q, theta = shift.q, shift.theta
+    lib = _lib.load()
+    xi = np.ascontiguousarray(leja_points(LEJA_MAX))
+    vd = _ops.as_device(v).reshape(-1)
+    coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, 64))
+    h = lin.mhd.ctx.bind_stream()
+    _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs)
+    _lib.check(lib.xmhd_leja_loop(h), "xmhd_leja_loop")
+    p = torch.empty_like(vd)
+    _lib.check(lib.xmhd_leja_finish_async(h, _lib.ptr(p)), "xmhd_leja_finish_async")
+    return p
+
+
+def cache_snapshot():
+    """Copy of the coefficient cache (restored when an asynchronous step is replayed)."""
+    return dict(_cache())
+
+
+def cache_restore(snap):
+    cache = _cache()
+    cache.clear()
+    cache.update(snap)
+
+
 def _apply_fused(l, lin, v, dt, shift, tol, xi):
     from paper_2108_13622_b200.linearize import RhsBlowupError
     q, theta = shift.q, shift.theta
@@ -296,14 +374,12 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
     lib = _lib.load()
     vd = _ops.as_device(v).reshape(-1)
     coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, 64))
-    st = _lib.LejaState()
     h = mhd.ctx.bind_stream()
-    rc = lib.xmhd_leja_start_async(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
-                                   float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
-                                   float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
-                                   int(coeffs.size))
-    _lib.check(rc, "xmhd_leja_start_async")
-    st = drive_fused(lib, h, l, q, theta, coeffs)
+    _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs)
+    if loop_available(mhd):
+        st = drive_loop(lib, h, l, q, theta, coeffs)
+    else:
+        st = drive_fused(lib, h, l, q, theta, coeffs)
     lin.rhs.calls += st.rhs_calls
     if st.status == _lib.LEJA_RHS_NONFINITE:
         # the reference raises from inside the matvec (mhd.py:225-231); rebuild

@@ -1,0 +1,57 @@
+"""Device timeline of an adaptive run (torch.profiler / CUPTI): kernel busy time
+vs wall time, per-kernel totals, and the idle gaps between kernels.
+
+usage: prof_timeline.py {c0|c2} [t_final]
+"""
+import collections
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import paper_2108_13622_b200 as xb  # noqa: E402
+from paper_2108_13622_b200 import leja, scenarios as sc  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "c0"
+tf = float(sys.argv[2]) if len(sys.argv) > 2 else None
+if which == "c0":
+    s = sc.kh_setup(128) if tf is None else sc.kh_setup(128, t_final=tf)
+    warm = sc.kh_setup(128, t_final=0.02)
+    scheme = xb.Scheme.EXPRB43
+else:
+    s = sc.harris_setup(512) if tf is None else sc.harris_setup(512, t_final=tf)
+    warm = sc.harris_setup(512, t_final=0.02)
+    scheme = xb.Scheme.EXPRB54S4
+xb.run(xb.RunConfig(scenario=warm, scheme=scheme, tol=s.tol))
+leja._coeff_cache.clear()
+torch.cuda.synchronize()
+acts = [torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]
+with torch.profiler.profile(activities=acts) as prof:
+    t0 = time.perf_counter()
+    rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+ks = sorted(((e.time_range.start, e.time_range.end, e.name) for e in evs), key=lambda x: x[0])
+busy = 0.0
+last_end = None
+gaps = []
+per = collections.defaultdict(lambda: [0, 0.0])
+for st, en, name in ks:
+    busy += en - st
+    per[name.split("(")[0][:60]][0] += 1
+    per[name.split("(")[0][:60]][1] += en - st
+    if last_end is not None:
+        gaps.append(st - last_end)
+    last_end = en if last_end is None else max(last_end, en)
+span = (ks[-1][1] - ks[0][0]) if ks else 0
+print(f"{which}: wall {wall*1e3:.2f} ms (profiled), {rep.accepted} steps, {rep.rhs_evals} rhs; "
+      f"device events {len(ks)}, busy {busy/1e3:.2f} ms over span {span/1e3:.2f} ms")
+gaps.sort()
+if gaps:
+    n = len(gaps)
+    print(f"gaps: n={n} median {gaps[n//2]:.1f} us, p90 {gaps[int(n*0.9)]:.1f} us, "
+          f"sum {sum(gaps)/1e3:.2f} ms, sum>20us {sum(g for g in gaps if g > 20)/1e3:.2f} ms")
+for name, (c, t) in sorted(per.items(), key=lambda x: -x[1][1])[:15]:
+    print(f"  {name:60s} {c:6d} {t/1e3:9.3f} ms  avg {t/c:7.2f} us")

@@ -1,0 +1,159 @@
+"""Asynchronous steps and the one-launch Leja loop against the synchronous paths.
+
+The asynchronous step (integrators._step_async) enqueues a whole exponential
+step and reads one record; the Leja loop runs every Newton term of a
+phi-action inside one cooperative launch.  Both must be invisible to the
+reference's semantics: the same bits, counters, step sequence and cache
+state as the per-call synchronous driver (and hence the reference, which
+test_gpu_parity pins), including the mid-step events that force a replay.
+"""
+
+import contextlib
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@contextlib.contextmanager
+def mode(async_on=True, loop=True):
+    from paper_2108_13622_b200 import integrators, leja, mhd
+    old = (integrators.ASYNC, leja.LOOP_MAX_CELLS)
+    integrators.ASYNC = async_on
+    leja.LOOP_MAX_CELLS = (1 << 20) if loop else 0
+    for c in mhd._ctx_cache.values():
+        c.loop_ok = None
+    try:
+        yield
+    finally:
+        integrators.ASYNC, leja.LOOP_MAX_CELLS = old
+        for c in mhd._ctx_cache.values():
+            c.loop_ok = None
+
+
+def _run(setup, scheme, tol):
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import leja
+    leja._coeff_cache.clear()
+    rep = xb.run(xb.RunConfig(scenario=setup, scheme=scheme, tol=tol))
+    steps = [(s.dt, s.error, s.rhs_calls, s.phi_iterations, s.phi_applications, s.accepted)
+             for s in rep.steps]
+    return rep, steps, list(leja._coeff_cache)
+
+
+@pytest.mark.parametrize("which", ["kh", "harris"])
+def test_async_run_is_bitwise_the_synchronous_run(which):
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import integrators, scenarios as sc
+    if which == "kh":
+        setup, scheme, tol = sc.kh_setup(32, t_final=0.15), xb.Scheme.EXPRB43, 1e-4
+    else:
+        setup, scheme, tol = sc.harris_setup(32, t_final=0.6), xb.Scheme.EXPRB54S4, 1e-6
+    with mode(async_on=False, loop=False):      # per-term launches, host batches
+        ref, ref_steps, ref_keys = _run(setup, scheme, tol)
+    with mode(async_on=False, loop=True):       # one launch per phi-action
+        lp, lp_steps, lp_keys = _run(setup, scheme, tol)
+    r0 = integrators.replays
+    with mode(async_on=True, loop=True):        # one host wait per step
+        asy, asy_steps, asy_keys = _run(setup, scheme, tol)
+    assert ref.accepted >= 3
+    for other, steps, keys in ((lp, lp_steps, lp_keys), (asy, asy_steps, asy_keys)):
+        assert steps == ref_steps
+        assert keys == ref_keys
+        assert other.rhs_evals == ref.rhs_evals
+        assert other.phi_iterations == ref.phi_iterations
+        assert other.checksum == ref.checksum
+    assert integrators.replays == r0      # nothing in these runs needs a replay
+
+
+def _lin(n=24, seed=4):
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import scenarios as sc
+    s = sc.kh_setup(n)
+    q = sc.initial_fields(s)
+    q = q + 1e-3 * np.random.default_rng(seed).standard_normal(q.shape)
+    st = xb.StateGrid(n, n, s.dx, s.dy, torch.from_numpy(q).cuda())
+    op = xb.RhsOperator(xb.MhdRhs(st, xb.MHDParams(mu=s.mu, eta=s.eta, kappa=s.kappa)))
+    return xb, st, op
+
+
+def _same(a, b):
+    assert a.converged == b.converged
+    assert a.rhs_calls == b.rhs_calls
+    assert a.phi_iterations == b.phi_iterations
+    assert a.phi_applications == b.phi_applications
+    assert (a.error_estimate == b.error_estimate or
+            (np.isnan(a.error_estimate) and np.isnan(b.error_estimate)))
+    assert torch.equal(a.new_state, b.new_state)
+
+
+def test_async_step_replays_on_nonfinite_rhs():
+    """A stage that overflows makes F non-finite: the reference raises
+    RhsBlowupError mid-step and stops calling F; the asynchronous step sees
+    the flag in its record and replays synchronously (same counters)."""
+    from paper_2108_13622_b200 import integrators
+    xb, st, op = _lin()
+    u = st.flat()
+    res = {}
+    for async_on in (False, True):
+        with mode(async_on=async_on):
+            lin = xb.FrozenLinearization(op, u)
+            r0 = integrators.replays
+            res[async_on] = xb.step(xb.Scheme.EXPRB43, op, u, 1e300, alpha=0.0, tol=1e-4,
+                                    lin=lin)
+            if async_on:
+                assert integrators.replays == r0 + 1
+    assert not res[True].converged and res[True].error_estimate == np.inf
+    _same(res[True], res[False])
+
+
+def test_async_step_replays_when_a_phi_action_needs_a_second_chunk():
+    """A step whose phi-actions pass 64 Newton terms: the device loop stops at
+    the end of the first chunk, the record shows it, the step is replayed with
+    the reference's chunk growth and cache updates."""
+    from paper_2108_13622_b200 import integrators, leja
+    xb, st, op = _lin()
+    u = st.flat()
+    lin0 = xb.FrozenLinearization(op, u)
+    alpha = xb.estimate_alpha(lin0, None, rng=np.random.default_rng(0)).alpha
+    dt = 60.0 / alpha
+    res, keys = {}, {}
+    for async_on in (False, True):
+        with mode(async_on=async_on):
+            leja._coeff_cache.clear()
+            lin = xb.FrozenLinearization(op, u)
+            r0 = integrators.replays
+            res[async_on] = xb.step(xb.Scheme.EXPRB43, op, u, dt, alpha=alpha, tol=1e-6, lin=lin)
+            keys[async_on] = [(k, v.size) for k, v in leja._coeff_cache.items()]
+            if async_on:
+                assert integrators.replays == r0 + 1
+    assert res[False].phi_iterations > 64
+    _same(res[True], res[False])
+    assert keys[True] == keys[False]
+
+
+def test_loop_and_batched_phi_are_bitwise_equal():
+    """One cooperative launch per phi-action vs one launch per Newton term,
+    across a coefficient-chunk growth (degree > 64)."""
+    from paper_2108_13622_b200 import leja
+    xb, st, op = _lin(n=40)
+    lin = xb.FrozenLinearization(op, st.flat())
+    alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    v = torch.from_numpy(np.random.default_rng(9).standard_normal(st.flat().numel())).cuda()
+    out = {}
+    for loop in (False, True):
+        with mode(loop=loop):
+            leja._coeff_cache.clear()
+            for adt in (3.0, 80.0):
+                sh = xb.shift_and_scale(adt)
+                c = op.calls
+                r = xb.apply_phi_leja(1, xb.JacobianAction(lin), v, adt / alpha, sh, 1e-10)
+                out[(loop, adt)] = (r, op.calls - c)
+    for adt in (3.0, 80.0):
+        (a, ca), (b, cb) = out[(False, adt)], out[(True, adt)]
+        assert (a.iterations, a.converged, a.residual, ca) == (b.iterations, b.converged,
+                                                               b.residual, cb)
+        assert torch.equal(a.vector, b.vector)
+    assert out[(True, 80.0)][0].iterations > 64
