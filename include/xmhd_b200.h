@@ -118,6 +118,9 @@ int xmhd_jvp_async(xmhd_ctx* ctx, const double* u, const double* fu, double unor
                    const double* w, double* out);
 int xmhd_leja_loop(xmhd_ctx* ctx);
 int xmhd_leja_loop_available(xmhd_ctx* ctx);
+/* Loop kernel of xmhd_leja_loop: 0 = 2D tiles (default; XMHD_TILE=0 in the
+ * environment selects 1), 1 = the sliding-window iteration kernel in a loop. */
+int xmhd_set_loop_kind(xmhd_ctx* ctx, int kind);
 int xmhd_leja_finish_async(xmhd_ctx* ctx, double* p_out);
 int xmhd_lincomb_async(xmhd_ctx* ctx, double* out, long long n, const double* const* v,
                        const double* coeffs, int nterms);

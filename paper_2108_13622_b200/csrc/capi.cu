@@ -58,6 +58,9 @@ struct xmhd_ctx {
   PowerCtl* jctl = nullptr;
   int nleja_async = 0;
   int loop_blocks = -1;        // co-resident blocks of the Leja loop kernel (-1: unknown)
+  int tile_grid = -1;          // grid of the 2D-tile Leja loop (0: unavailable, -1: unknown)
+  int tile_minb = 2;           // its occupancy variant
+  int partial_slots = 0;       // doubles in `partials`
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -327,6 +330,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
   }
   c->red_grid = 4 * c->nsm;
   const int slots = (c->red_grid > c->grid ? c->red_grid : c->grid) * 8 + 64;
+  c->partial_slots = slots;
   if ((e = cudaMalloc(&c->partials, sizeof(double) * slots)) != cudaSuccess ||
       (e = cudaMalloc(&c->tickets, sizeof(unsigned) * 8)) != cudaSuccess ||
       (e = cudaMalloc(&c->result, sizeof(double) * 16)) != cudaSuccess ||
@@ -690,22 +694,45 @@ int xmhd_leja_sync(xmhd_ctx* c, xmhd_leja_state* st) {
 // ---- asynchronous single-domain steps ------------------------------------
 // The whole Leja loop as one cooperative launch; no host read until the
 // caller synchronises (xmhd_leja_sync, or xmhd_async_fetch at a step end).
+// Which loop kernel: the 2D-tile loop (default) or the sliding-window loop
+// (XMHD_TILE=0, A/B and tests).
+static void loop_plan(xmhd_ctx* c) {
+  if (c->tile_grid < 0) {
+    const char* e = std::getenv("XMHD_TILE");
+    const bool tile = !(e && std::atoi(e) == 0);
+    c->tile_grid = tile ? leja_tile_loop_grid(c->g, c->nsm, &c->tile_minb) : 0;
+    if (c->tile_grid * 6 > c->partial_slots) c->tile_grid = 0;
+  }
+  if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
+}
+
 int xmhd_leja_loop(xmhd_ctx* c) {
   if (!c) return fail(XMHD_BADARG, "null ctx");
   if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "y-strips use the strip drivers");
-  if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
-  if (c->grid > c->loop_blocks)
-    return fail(XMHD_BADARG, "grid not co-resident: use xmhd_leja_launch batches");
+  loop_plan(c);
   StencilArgs a = leja_args(c);
-  CK(launch_leja_loop(a, c->grid, c->stream));
+  if (c->tile_grid > 0) {
+    CK(launch_leja_tile_loop(a, c->tile_grid, c->tile_minb, c->stream));
+  } else {
+    if (c->grid > c->loop_blocks)
+      return fail(XMHD_BADARG, "grid not co-resident: use xmhd_leja_launch batches");
+    CK(launch_leja_loop(a, c->grid, c->stream));
+  }
   c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_set_loop_kind(xmhd_ctx* c, int kind) {
+  if (!c || kind < 0 || kind > 1) return fail(XMHD_BADARG, "bad loop kind");
+  c->tile_grid = -1;
+  if (kind == 1) c->tile_grid = 0;   // sliding-window loop
   return XMHD_OK;
 }
 
 int xmhd_leja_loop_available(xmhd_ctx* c) {
   if (!c || c->g.bcy == BC_HALO) return 0;
-  if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
-  return c->grid <= c->loop_blocks ? 1 : 0;
+  loop_plan(c);
+  return (c->tile_grid > 0 || c->grid <= c->loop_blocks) ? 1 : 0;
 }
 
 static int ensure_async(xmhd_ctx* c) {

@@ -206,6 +206,10 @@ cudaError_t launch_krylov_combine(double* out, long long n, const KrylovBasis& B
 // co-resident: grid <= leja_loop_max_blocks).
 cudaError_t launch_leja_loop(const StencilArgs& a, int grid, cudaStream_t s);
 int leja_loop_max_blocks(int nsm);
+// Small grids: the same loop over 2D tiles (grid = leja_tile_loop_grid; the
+// stencil partials buffer needs 6 doubles per block).
+cudaError_t launch_leja_tile_loop(const StencilArgs& a, int grid, int minb, cudaStream_t s);
+int leja_tile_loop_grid(const Geom& g, int nsm, int* minb);
 // p_out = pbuf[ctl->cur] (the interpolant of a finished call; no host read of cur).
 cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf, const LejaCtl* ctl,
                                     long long n, cudaStream_t s);

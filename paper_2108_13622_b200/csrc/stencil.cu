@@ -819,6 +819,352 @@ int leja_emul_max_blocks(int nsm) {
   return n * nsm;
 }
 
+// ---------------------------------------------------------------------------
+// Small-grid Leja loop: 2D tiles, all Newton terms in one cooperative launch.
+//
+// On grids of up to ~1M cells a term of the sliding-window kernel is latency
+// bound (a y-segment needs 4 warm-up rows, so a CTA spends 5 dependent row
+// steps on one output row).  Here a CTA computes a TX x TY tile in three
+// dependent phases over shared memory: (1) x = u + eps*y, primitives and
+// ideal fluxes on the tile plus its 2-cell halo, (2) the diffusive fluxes on
+// the level-1 ring, (3) the differenced RHS, the FD-JVP and the Newton update
+// for the tile.  Every per-cell value is the same IEEE operation sequence as
+// in stencil_body (same device functions, same association order), so F bits
+// are identical; only the order of the norm sums differs (fixed per grid).
+//
+// Terms are separated by one grid-wide barrier: each block publishes
+// [sum y'^2, sum p'^2, bad] into a parity-double-buffered slot, and after the
+// barrier EVERY block sums the slots in the same fixed order and runs the
+// reference's control update on its own shared-memory copy of the control
+// block (identical in all blocks), so no second barrier or last-block ticket
+// is needed.  Block 0 mirrors the control block to global memory.
+// Resident tile blocks per SM the register budget targets: 2 (210 registers,
+// the shortest chain when every block holds one tile: 8.8 us/term at 128^2)
+// or 3 (160 registers, more tiles in flight when blocks loop over several
+// tiles: 37.9 vs 41.5 us/term at 512^2; 4 blocks: 38.4).
+constexpr int TX = 16, TY = 8, TNT = TX * TY;        // outputs per tile = threads
+constexpr int EX = TX + 4, EY = TY + 4, NE = EX * EY;  // tile + 2-cell halo
+constexpr int FXW = TX + 2, NFXC = TY * FXW;           // FX / GX: rows [0,TY), cols [-1,TX]
+constexpr int FYH = TY + 2, NFYC = FYH * TX;           // FY / GY: rows [-1,TY], cols [0,TX)
+constexpr int GBW = TX + 2, NGB = (TY + 2) * GBW;      // level-1 box (corners skipped)
+
+struct TileSmem {
+  double pd[NPD][NE];
+  double fx[NFX][NFXC];
+  double fy[NFY][NFYC];
+  double gx[NG][NFXC];
+  double gy[NG][NFYC];
+};
+
+size_t tile_smem_bytes() { return sizeof(TileSmem); }
+
+namespace {
+
+// Row r (any integer) of the domain seen from a tile: rows beyond the 2-row
+// halo only feed outputs outside the grid, so they are clamped into it (the
+// loads stay in bounds); the halo itself follows row_source.
+__device__ __forceinline__ RowSrc tile_row(int r, const Geom& g, const double* u, const double* d,
+                                           const double* hlo_dir, const double* hhi_dir) {
+  r = min(max(r, -2), g.ny + 1);
+  return row_source(r, g, u, d, hlo_dir, hhi_dir);
+}
+
+}  // namespace
+
+template <int KX, int KY, int MINB>
+__global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const StencilArgs a) {
+  extern __shared__ __align__(16) double smem_raw[];
+  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
+  __shared__ LejaCtl lc;
+  __shared__ double red[3][TNT / 32];
+  cg::grid_group grid = cg::this_grid();
+  const Geom& g = a.g;
+  const int t = threadIdx.x;
+  const int bid = blockIdx.x, nblk = gridDim.x;
+  const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY, ntiles = ntx * nty;
+  const unsigned plane = (unsigned)g.plane;
+  if (t == 0) lc = *a.ctl;
+  __syncthreads();
+  int par = 0;
+  for (;;) {
+    if (lc.status != LJ_RUNNING) break;
+    const int cur = lc.cur, m = lc.m;
+    const double eps = lc.eps, dt = lc.dt, q = lc.q;
+    const Divisor epsd = lc.epsd, thd = lc.thetad;
+    const int zero_dir = lc.zero_dir;
+    const double* dir = a.ybuf[cur];
+    double* yout = a.ybuf[cur ^ 1];
+    const double* pin = a.pbuf[cur];
+    double* pout = a.pbuf[cur ^ 1];
+    const double xim = __ldg(a.xi + (m - 1));
+    const double cm = __ldg(a.coeffs + m);
+    double acc0 = 0.0, acc1 = 0.0;
+    int bad = 0;
+
+    if (zero_dir) {
+      // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
+      const long long n = (long long)NF * g.plane;
+      for (long long i = (long long)bid * TNT + t; i < n; i += (long long)nblk * TNT) {
+        const double y = __ldcg(dir + i);
+        const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
+                                    __dmul_rn(xim, y));
+        const double pn = __dadd_rn(__ldcg(pin + i), __dmul_rn(cm, yn));
+        yout[i] = yn;
+        pout[i] = pn;
+        acc0 = __fma_rn(yn, yn, acc0);
+        acc1 = __fma_rn(pn, pn, acc1);
+      }
+    } else {
+      for (int tile = bid; tile < ntiles; tile += nblk) {
+        const int X0 = (tile % ntx) * TX, Y0 = (tile / ntx) * TY;
+        // output cell of this thread and its epilogue operands (issued first)
+        const int oj = t / TX, oi = t - oj * TX;
+        const bool out_ok = (Y0 + oj < g.ny) && (X0 + oi < g.nx);
+        const unsigned obase = out_ok ? (unsigned)(Y0 + oj) * (unsigned)g.nx + (unsigned)(X0 + oi) : 0u;
+        double efu[NF], ey[NF], ep[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const unsigned i = obase + (unsigned)f * plane;
+          efu[f] = __ldg(a.fu + i);
+          ey[f] = __ldcg(dir + i);
+          ep[f] = __ldcg(pin + i);
+        }
+        // ---- phase 1: primitives and ideal fluxes on the tile + halo (2 cells / thread)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = t + h * TNT;
+          if (e < NE) {
+            const int ej = e / EX, ei = e - ej * EX;
+            const int j = ej - 2, i = ei - 2;
+            const RowSrc rs = tile_row(Y0 + j, g, a.u, dir, g.halo_lo_dir, g.halo_hi_dir);
+            int cs, flipx;
+            col_source(X0 + i, g, cs, flipx);
+            double x[NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const unsigned k = rs.off + (unsigned)cs + (unsigned)f * rs.fs;
+              x[f] = __dadd_rn(__ldg(rs.u + k), __dmul_rn(eps, __ldcg(rs.d + k)));
+            }
+            if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
+            if (rs.flip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+            Prim p;
+            primitives(x, g, p);
+            S.pd[PD_VX][e] = p.vx;
+            S.pd[PD_VY][e] = p.vy;
+            S.pd[PD_VZ][e] = p.vz;
+            S.pd[PD_BX][e] = p.bx;
+            S.pd[PD_BY][e] = p.by;
+            S.pd[PD_BZ][e] = p.bz;
+            S.pd[PD_T][e] = p.temp;
+            S.pd[PD_B2][e] = p.b2;
+            double fv[NFX];
+            if (j >= 0 && j < TY && i >= -1 && i <= TX) {
+              flux_x(p, g, fv);
+#pragma unroll
+              for (int k = 0; k < NFX; ++k) S.fx[k][j * FXW + i + 1] = fv[k];
+            }
+            if (j >= -1 && j <= TY && i >= 0 && i < TX) {
+              flux_y(p, g, fv);
+#pragma unroll
+              for (int k = 0; k < NFY; ++k) S.fy[k][(j + 1) * TX + i] = fv[k];
+            }
+          }
+        }
+        __syncthreads();
+        // ---- phase 2: diffusive fluxes on the level-1 ring (mhd.py:182-221)
+        if (g.diffusive) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = t + h * TNT;
+            if (e < NGB) {
+              const int bj = e / GBW, bi = e - bj * GBW;
+              const int j = bj - 1, i = bi - 1;
+              const bool in_gx = (j >= 0 && j < TY), in_gy = (i >= 0 && i < TX);
+              if (in_gx || in_gy) {
+                const int c = (j + 2) * EX + (i + 2);
+                double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
+#pragma unroll
+                for (int k = 0; k < NPD; ++k) {
+                  xl[k] = S.pd[k][c - 1];
+                  xr[k] = S.pd[k][c + 1];
+                  yd[k] = S.pd[k][c - EX];
+                  yu[k] = S.pd[k][c + EX];
+                  own[k] = S.pd[k][c];
+                }
+                double gxv[NG], gyv[NG];
+                diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyv);
+                if (in_gx) {
+#pragma unroll
+                  for (int k = 0; k < NG; ++k) S.gx[k][j * FXW + i + 1] = gxv[k];
+                }
+                if (in_gy) {
+#pragma unroll
+                  for (int k = 0; k < NG; ++k) S.gy[k][(j + 1) * TX + i] = gyv[k];
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();
+        // ---- phase 3: output cell (oj, oi): RHS in the reference's order + Newton update
+        if (out_ok) {
+          const int cx = oj * FXW + oi + 1;         // FX / GX index of the cell
+          const int cy = (oj + 1) * TX + oi;        // FY / GY index of the cell
+          double F[NF];
+#pragma unroll
+          for (int k = 0; k < NFX; ++k)
+            F[fx_field(k)] = -qdiv<KX>(__dsub_rn(S.fx[k][cx + 1], S.fx[k][cx - 1]), g.h2x);
+          F[BX] = -0.0;
+#pragma unroll
+          for (int k = 0; k < NFY; ++k) {
+            const int f = fy_field(k);
+            F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(S.fy[k][cy + TX], S.fy[k][cy - TX]), g.h2y));
+          }
+          F[BY] = __dsub_rn(F[BY], 0.0);
+          if (g.diffusive) {
+            double gr[NG], gl[NG], gu[NG], gd[NG];
+#pragma unroll
+            for (int k = 0; k < NG; ++k) {
+              gr[k] = S.gx[k][cx + 1];
+              gl[k] = S.gx[k][cx - 1];
+              gu[k] = S.gy[k][cy + TX];
+              gd[k] = S.gy[k][cy - TX];
+            }
+            F[RHO] = __dadd_rn(F[RHO], 0.0);
+            F[BX] = __dadd_rn(F[BX], 0.0);
+            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gr[0], gl[0]), g.h2x));
+            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gr[1], gl[1]), g.h2x));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gr[2], gl[2]), g.h2x));
+            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gr[3], gl[3]), g.h2x));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gr[4], gl[4]), g.h2x));
+            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gr[5], gl[5]), g.h2x));
+            F[RHO] = __dadd_rn(F[RHO], 0.0);
+            F[BY] = __dadd_rn(F[BY], 0.0);
+            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gu[0], gd[0]), g.h2y));
+            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gu[1], gd[1]), g.h2y));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gu[2], gd[2]), g.h2y));
+            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gu[3], gd[3]), g.h2y));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gu[4], gd[4]), g.h2y));
+            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gu[5], gd[5]), g.h2y));
+          }
+          unsigned ex = 0;
+#pragma unroll
+          for (int f = 0; f < NF; ++f) ex = max(ex, (unsigned)__double2hiint(F[f]) & 0x7ff00000u);
+          bad |= (ex == 0x7ff00000u);
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            const unsigned i = obase + (unsigned)f * plane;
+            const double w = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
+            const double y = ey[f];
+            const double yn = __dsub_rn(
+                qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
+                __dmul_rn(xim, y));
+            const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
+            yout[i] = yn;
+            pout[i] = pn;
+            acc0 = __fma_rn(yn, yn, acc0);
+            acc1 = __fma_rn(pn, pn, acc1);
+          }
+        }
+        __syncthreads();   // shared tiles are rewritten by the next tile
+      }
+    }
+
+    // ---- term end: publish [sum y'^2, sum p'^2, bad], barrier, every block reduces
+    {
+      double v0 = acc0, v1 = acc1, v2 = bad ? 1.0 : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+      }
+      const int w = t >> 5, l = t & 31;
+      if (l == 0) { red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; }
+      __syncthreads();
+      if (t == 0) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int k = 0; k < TNT / 32; ++k) { s0 += red[0][k]; s1 += red[1][k]; s2 += red[2][k]; }
+        double* slot = a.partials + ((size_t)par * nblk + bid) * 3;
+        slot[0] = s0;
+        slot[1] = s1;
+        slot[2] = s2;
+      }
+    }
+    grid.sync();
+    if (t < 32) {
+      const double* base = a.partials + (size_t)par * nblk * 3;
+      const double sy = sum_partials(base, nblk, 3, 0);
+      const double sp = sum_partials(base, nblk, 3, 1);
+      const double sb = sum_partials(base, nblk, 3, 2);
+      if (t == 0) {
+        leja_finalize(&lc, sy, sp, sb > 0.0, !zero_dir, cm);
+        if (bid == 0) *a.ctl = lc;
+      }
+    }
+    __syncthreads();
+    par ^= 1;
+  }
+}
+
+namespace {
+
+template <int KX, int KY, int MINB>
+cudaError_t launch_tile_loop_one(const StencilArgs& a, int grid, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaError_t err = cudaFuncSetAttribute(leja_tile_loop_kernel<KX, KY, MINB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)tile_smem_bytes());
+    if (err != cudaSuccess) return err;
+    done = true;
+  }
+  void* kargs[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((const void*)leja_tile_loop_kernel<KX, KY, MINB>, dim3(grid),
+                                     dim3(TNT), kargs, tile_smem_bytes(), s);
+}
+
+template <int MINB>
+int tile_blocks_per_sm() {
+  int n = 0;
+  if (cudaFuncSetAttribute(leja_tile_loop_kernel<DIV_MUL, DIV_MUL, MINB>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tile_smem_bytes()) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &n, leja_tile_loop_kernel<DIV_MUL, DIV_MUL, MINB>, TNT, tile_smem_bytes()) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+}  // namespace
+
+// minb: 2 or 3 (leja_tile_loop_grid's choice).
+cudaError_t launch_leja_tile_loop(const StencilArgs& a, int grid, int minb, cudaStream_t s) {
+  return with_div_kinds(a.g, [&](auto X, auto Y) {
+    return minb == 3 ? launch_tile_loop_one<decltype(X)::value, decltype(Y)::value, 3>(a, grid, s)
+                     : launch_tile_loop_one<decltype(X)::value, decltype(Y)::value, 2>(a, grid, s);
+  });
+}
+
+// Grid of the tile loop (one block per tile, capped at the co-resident blocks)
+// and its occupancy variant: 2 blocks / SM when every block holds one tile,
+// else 3 (more tiles in flight).  0 when the kernel cannot be resident.
+int leja_tile_loop_grid(const Geom& g, int nsm, int* minb) {
+  const long long ntiles = (long long)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
+  const int n2 = tile_blocks_per_sm<2>();
+  int mb = 2, n = n2;
+  if (ntiles > (long long)n2 * nsm) {
+    const int n3 = tile_blocks_per_sm<3>();
+    if (n3 > n2) { mb = 3; n = n3; }
+  }
+  if (n < 1) return 0;
+  *minb = mb;
+  const long long cap = (long long)n * nsm;
+  return (int)(ntiles < cap ? ntiles : cap);
+}
+
 cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s) {
   switch (mode) {
     case MODE_RHS: return launch_mode<MODE_RHS>(a, grid, s);
