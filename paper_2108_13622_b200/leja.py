@@ -252,7 +252,11 @@ def drive_fused(lib, h, l, q, theta, coeffs, peer=False):
                 _lib.check(lib.xmhd_leja_launch(h, stop - enq, int(peer)), "xmhd_leja_launch")
                 enq = stop
             _lib.check(lib.xmhd_leja_sync(h, ctypes.byref(st)), "xmhd_leja_sync")
-            if st.status != _lib.LEJA_RUNNING:
+            # a batch that ended exactly at a chunk boundary leaves the device
+            # waiting for the extension the loop above enqueues next
+            waiting = (st.status == _lib.LEJA_NEED_COEFFS and k < len(plan) and
+                       st.m == plan[k][0])
+            if st.status != _lib.LEJA_RUNNING and not waiting:
                 break
             batch = min(2 * batch, 64)
             target = enq + batch

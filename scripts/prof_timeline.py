@@ -15,7 +15,14 @@ from paper_2108_13622_b200 import leja, scenarios as sc  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c0"
 tf = float(sys.argv[2]) if len(sys.argv) > 2 else None
-if which == "c0":
+if which == "c3":
+    tf, steps = None, (int(sys.argv[2]) if len(sys.argv) > 2 else 5)
+if which == "c3":
+    s = sc.CONFIGS[3]()
+    s.max_accepted = steps
+    warm = sc.kh_setup(4096, tol=1e-5, t_final=1e9, max_accepted=1)
+    scheme = xb.Scheme.EXPRB43
+elif which == "c0":
     s = sc.kh_setup(128) if tf is None else sc.kh_setup(128, t_final=tf)
     warm = sc.kh_setup(128, t_final=0.02)
     scheme = xb.Scheme.EXPRB43
@@ -23,13 +30,13 @@ else:
     s = sc.harris_setup(512) if tf is None else sc.harris_setup(512, t_final=tf)
     warm = sc.harris_setup(512, t_final=0.02)
     scheme = xb.Scheme.EXPRB54S4
-xb.run(xb.RunConfig(scenario=warm, scheme=scheme, tol=s.tol))
+xb.run(xb.RunConfig(scenario=warm, scheme=scheme, tol=s.tol, max_accepted=warm.max_accepted))
 leja._coeff_cache.clear()
 torch.cuda.synchronize()
 acts = [torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]
 with torch.profiler.profile(activities=acts) as prof:
     t0 = time.perf_counter()
-    rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol))
+    rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol, max_accepted=s.max_accepted))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]

@@ -199,3 +199,28 @@ def test_loop_kernels_against_per_term_launches(n):
                        sh.theta, 1e-10, olj.CoeffCache())
     assert t.iterations == ref.iterations
     assert np.linalg.norm(t.vector.cpu().numpy() - ref.vector) <= 1e-10 * np.linalg.norm(ref.vector)
+
+
+def test_batched_driver_when_a_batch_ends_at_a_chunk_boundary():
+    """Host-paced batches (large grids): a batch that ends exactly at term 63
+    leaves the device at the end of the first coefficient chunk; the driver
+    must extend the table and continue, like the reference's growth."""
+    from paper_2108_13622_b200 import leja
+    xb, st, op = _lin(n=40)
+    lin = xb.FrozenLinearization(op, st.flat())
+    alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    v = torch.from_numpy(np.random.default_rng(9).standard_normal(st.flat().numel())).cuda()
+    adt = 80.0
+    sh = xb.shift_and_scale(adt)
+    out = {}
+    for key, kw in (("loop", dict(loop=True, tile=False)), ("batch", dict(loop=False))):
+        with mode(**kw):
+            leja._coeff_cache.clear()
+            leja._degree_hint.clear()
+            if key == "batch":
+                theta = sh.theta
+                leja._degree_hint[(1, int(round(4.0 * np.log2(theta))))] = 63
+            out[key] = xb.apply_phi_leja(1, xb.JacobianAction(lin), v, adt / alpha, sh, 1e-10)
+    a, b = out["loop"], out["batch"]
+    assert a.iterations > 64 and a.iterations == b.iterations and a.converged == b.converged
+    assert torch.equal(a.vector, b.vector)
