@@ -141,6 +141,11 @@ int xmhd_power(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, c
                double* w, double* work, int maxit, double tol, double* mags, int* nit,
                int* rhs_calls, int* status);
 
+/* FrozenLinearization (linearize.py:46-53): fu = F(u) and *unorm = ||u|| with one
+ * host synchronisation; XMHD_NONFINITE when F(u) has non-finite cells.
+ * Single-domain contexts. */
+int xmhd_linearize(xmhd_ctx* ctx, const double* u, double* fu, double* unorm);
+
 /* np.linalg.norm(x) (deterministic device reduction). */
 int xmhd_norm(xmhd_ctx* ctx, const double* x, long long n, double* out);
 

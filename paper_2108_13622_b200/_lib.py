@@ -71,6 +71,7 @@ _SIGS = {
     "xmhd_diff_norms_async": (_I, [_P, _P, _P, _L]),
     "xmhd_async_fetch": (_I, [_P, ctypes.POINTER(StepRecord)]),
     "xmhd_power": (_I, [_P, _P, _P, _D, _P, _P, _P, _I, _D, _PD, _PI, _PI, _PI]),
+    "xmhd_linearize": (_I, [_P, _P, _P, _PD]),
     "xmhd_norm": (_I, [_P, _P, _L, _PD]),
     "xmhd_lincomb": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD, _PI]),
     "xmhd_divide": (_I, [_P, _P, _P, _D, _L, _PD]),
@@ -187,7 +188,14 @@ def host_doubles(arr):
     return a, a.ctypes.data_as(_PD)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def current_stream_handle():
+    """cudaStream_t of torch's current stream on the current device (the raw
+    accessor skips the Stream object: this runs once per native call)."""
+    if _raw_stream is not None:
+        return ctypes.c_void_p(_raw_stream(torch.cuda.current_device()))
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
@@ -208,7 +216,10 @@ class Context:
         self.h = h
 
     def bind_stream(self):
-        self.lib.xmhd_set_stream(self.h, current_stream_handle())
+        st = current_stream_handle()
+        if st.value != getattr(self, "_stream", -1):
+            self.lib.xmhd_set_stream(self.h, st)
+            self._stream = st.value
         return self.h
 
     def plan(self):

@@ -18,19 +18,27 @@ _util = {}
 _util_lock = threading.Lock()
 
 
+_util_tls = threading.local()
+
+
 def util_ctx():
     """A geometry-free context used for reductions on arbitrary vectors.
 
     One per (device, host thread): its reduction scratch must not be shared by
     concurrently enqueued work.
     """
-    key = (torch.cuda.current_device(), threading.get_ident())
+    dev = torch.cuda.current_device()
+    mine = getattr(_util_tls, "ctx", None)
+    if mine is not None and mine[0] == dev:
+        return mine[1]
+    key = (dev, threading.get_ident())
     with _util_lock:
         c = _util.get(key)
         if c is None:
             c = _lib.Context(2, 2, 1.0, 1.0, 0.0, 0.0, 0.0, 5.0 / 3.0, 1.0,
                              _lib.BC_PERIODIC, _lib.BC_PERIODIC)
             _util[key] = c
+    _util_tls.ctx = (dev, c)
     return c
 
 

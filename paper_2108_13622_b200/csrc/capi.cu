@@ -61,6 +61,8 @@ struct xmhd_ctx {
   int tile_grid = -1;          // grid of the 2D-tile Leja loop (0: unavailable, -1: unknown)
   int tile_minb = 2;           // its occupancy variant
   int partial_slots = 0;       // doubles in `partials`
+  double xi_h[500];            // host copy of the Leja points on the device
+  bool xi_valid = false;
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -235,7 +237,12 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   if (rc) return rc;
   rc = upload_coeffs(c, coeffs, ncoef);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(c->xi_d, xi, sizeof(double) * 500, cudaMemcpyHostToDevice, c->stream));
+  // the Leja points never change between calls: upload only what differs
+  if (!c->xi_valid || std::memcmp(c->xi_h, xi, sizeof(double) * 500) != 0) {
+    std::memcpy(c->xi_h, xi, sizeof(double) * 500);
+    CK(cudaMemcpyAsync(c->xi_d, xi, sizeof(double) * 500, cudaMemcpyHostToDevice, c->stream));
+    c->xi_valid = true;
+  }
   LejaCtl h;
   std::memset(&h, 0, sizeof(h));
   h.ncoef = ncoef;
@@ -534,6 +541,25 @@ int xmhd_power(xmhd_ctx* c, const double* u, const double* fu, double unorm, con
   for (int k = 0; k < h->k; ++k) mags[k] = h->mags[k];
   *status = h->status == PW_DONE ? 0 : 1;
   return h->status == PW_RHS_BAD ? XMHD_NONFINITE : XMHD_OK;
+}
+
+// FrozenLinearization (linearize.py:46-53) in one host round trip:
+// fu = F(u) and ||u|| enqueued back to back, then one read of both.
+int xmhd_linearize(xmhd_ctx* c, const double* u, double* fu, double* unorm) {
+  if (!c || !u || !fu || !unorm) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "y-strips reduce ||u|| across ranks");
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.out = fu;
+  CK(launch_stencil(MODE_RHS, a, c->grid, c->stream));
+  CK(launch_norm(u, NF * c->g.plane, redbuf(c), c->stream));
+  c->launches += 2;
+  CK(cudaMemcpyAsync(c->h_int, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_dbl, c->result, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *unorm = c->h_dbl[0];
+  return c->h_int[0] ? XMHD_NONFINITE : XMHD_OK;
 }
 
 int xmhd_norm(xmhd_ctx* c, const double* x, long long n, double* out) {

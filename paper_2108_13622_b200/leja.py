@@ -111,7 +111,7 @@ def _compute_coeffs(l, q, theta, count):
 # current chunk, a host thread computes the next chunk (a pure function of
 # (l, q, theta, count), so the values are the ones an on-demand computation
 # would produce).  The cache below still follows the reference's policy.
-_spec_pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="leja-coeffs")
+_spec_pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="leja-coeffs")
 _spec = {}
 _degree_hint = {}
 
@@ -227,9 +227,15 @@ def drive_fused(lib, h, l, q, theta, coeffs, peer=False):
             futs[k] = _spec_pool.submit(_compute_coeffs, l, q, theta, plan[k][1])
         return futs.get(k)
 
-    fut(0)
     hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
     batch = max(2, int(_degree_hint.get(hkey, 2)))
+    # every chunk the expected degree will reach is computed from the start, in
+    # parallel (the divided differences release the GIL), so a slow host core
+    # never makes the device wait at a chunk boundary
+    fut(0)
+    for kk in range(1, len(plan)):
+        if plan[kk][0] <= batch + batch // 4 + 8:
+            fut(kk)
     table_end, k, enq = coeffs.size, 0, 0
     grown = []
     st = _lib.LejaState()
