@@ -9,7 +9,9 @@ coefficient cache cleared per step so the host coefficient work is included.
           resident in HBM (state vectors 268 MB each >> 126 MB L2: no flush).
   e2e   : same metric through the public API with pinned HOST buffers: per step
           u and the 4 right-hand vectors are copied H2D and the 4 results D2H.
-  roofline : the fused Leja iteration kernel, 384 algorithmic B per cell
+  roofline : the fused Leja iteration kernel, 352 algorithmic B per cell per term
+          (read u, y, F(u), p; write y' every term and p' every other term:
+          deferred interpolant stores; 384 with XMHD_PDEFER=0)
           (read u, y, F(u), p; write y', p'), timed with CUDA events on its stream.
   cpu_baseline : the NumPy oracle (the reference's own algorithm, oracle/) on a
           bounded sample of the same workload on this host.
@@ -38,7 +40,8 @@ sys.path.insert(0, REPO)
 METRIC = "RHS/Jv cell-updates/s (fp64 GB/s vs HBM peak); wall-s per EXPRB step"
 SWEEP = (1.0, 10.0, 100.0, 300.0)
 LEJA_TOL = 1e-10
-BYTES_PER_CELL_ITER = 384.0
+# algorithmic bytes per cell per Newton term
+BYTES_PER_CELL_ITER = 384.0 if os.environ.get("XMHD_PDEFER", "1") == "0" else 352.0
 
 
 def parse():

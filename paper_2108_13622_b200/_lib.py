@@ -66,6 +66,7 @@ _SIGS = {
     "xmhd_leja_loop": (_I, [_P]),
     "xmhd_leja_loop_available": (_I, [_P]),
     "xmhd_set_loop_kind": (_I, [_P, _I]),
+    "xmhd_set_leja_defer": (_I, [_P, _I]),
     "xmhd_leja_finish_async": (_I, [_P, _P]),
     "xmhd_lincomb_async": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I]),
     "xmhd_diff_norms_async": (_I, [_P, _P, _P, _L]),

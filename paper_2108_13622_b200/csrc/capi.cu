@@ -63,6 +63,7 @@ struct xmhd_ctx {
   int partial_slots = 0;       // doubles in `partials`
   double xi_h[500];            // host copy of the Leja points on the device
   bool xi_valid = false;
+  bool leja_defer = true;      // deferred interpolant stores (XMHD_PDEFER=0: off)
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -232,7 +233,7 @@ int upload_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
 
 int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double dt, double q,
                double theta, double tol, const double* xi, const double* coeffs, int ncoef,
-               double* ext_sums = nullptr) {
+               double* ext_sums = nullptr, bool generic = false) {
   int rc = ensure_ws(c, n);
   if (rc) return rc;
   rc = upload_coeffs(c, coeffs, ncoef);
@@ -254,6 +255,7 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.thetad = make_divisor(theta, c->force_ieee);
   h.force_ieee = c->force_ieee ? 1 : 0;
   h.epoch = c->p2p_epoch;
+  h.defer = (c->leja_defer && !generic) ? 1 : 0;   // the generic update stores every term
   *c->ctl_h = h;
   // staged from pageable memory at the call: back-to-back asynchronous
   // phi-actions never race on the pinned mirror
@@ -299,6 +301,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
   xmhd_ctx* c = new xmhd_ctx();
   const bool ieee = std::getenv("XMHD_DIV_IEEE") && std::atoi(std::getenv("XMHD_DIV_IEEE"));
   c->force_ieee = ieee;
+  if (const char* e = std::getenv("XMHD_PDEFER")) c->leja_defer = std::atoi(e) != 0;
   Geom& g = c->g;
   std::memset(&g, 0, sizeof(g));
   g.nx = nx;
@@ -748,6 +751,12 @@ int xmhd_leja_loop(xmhd_ctx* c) {
   return XMHD_OK;
 }
 
+int xmhd_set_leja_defer(xmhd_ctx* c, int on) {
+  if (!c) return fail(XMHD_BADARG, "null ctx");
+  c->leja_defer = on != 0;
+  return XMHD_OK;
+}
+
 int xmhd_set_loop_kind(xmhd_ctx* c, int kind) {
   if (!c || kind < 0 || kind > 1) return fail(XMHD_BADARG, "bad loop kind");
   c->tile_grid = -1;
@@ -818,7 +827,7 @@ int xmhd_leja_finish_async(xmhd_ctx* c, double* p_out) {
   if (!c || !p_out || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
   if (c->nleja_async >= ASYNC_LEJA_MAX) return fail(XMHD_BADARG, "too many phi-actions in one step");
   const long long n = NF * c->g.plane;
-  CK(launch_leja_copy_result(p_out, c->pbuf, c->ctl, n, c->stream));
+  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
   CK(cudaMemcpyAsync(&c->arec->leja[c->nleja_async], c->ctl, sizeof(LejaCtl),
                      cudaMemcpyDeviceToDevice, c->stream));
   c->nleja_async++;
@@ -877,8 +886,8 @@ int xmhd_leja_result(xmhd_ctx* c, double* p_out) {
   int rc = sync_ctl(c);
   if (rc) return rc;
   const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
-  CK(cudaMemcpyAsync(p_out, c->pbuf[c->ctl_h->cur], sizeof(double) * n,
-                     cudaMemcpyDeviceToDevice, c->stream));
+  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
+  c->launches++;
   return XMHD_OK;
 }
 
@@ -896,7 +905,7 @@ int xmhd_leja_generic_start(xmhd_ctx* c, const double* v, long long n, double dt
                             double theta, double tol, const double* xi, const double* coeffs,
                             int ncoef, xmhd_leja_state* st) {
   if (!c || !v || !xi || !coeffs || n < 1) return fail(XMHD_BADARG, "bad arg");
-  int rc = leja_setup(c, v, n, 1.0, dt, q, theta, tol, xi, coeffs, ncoef);
+  int rc = leja_setup(c, v, n, 1.0, dt, q, theta, tol, xi, coeffs, ncoef, nullptr, true);
   if (rc) return rc;
   c->gen_n = n;
   rc = sync_ctl(c);

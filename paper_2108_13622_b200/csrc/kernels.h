@@ -31,6 +31,16 @@ struct LejaCtl {
   int force_ieee;   // testing: plain IEEE division for eps as well
   int pad2_;
   unsigned long long epoch;   // y-strips over peer memory: last exchange epoch
+  // Deferred interpolant update: with `defer` set, every other term leaves
+  // p' = p + c_m*y_m in registers (for ||p'||) without storing it; the next
+  // term adds c_m*y_m (its own direction) before its own update and stores.
+  // Same two roundings per element as the reference's p = p + c*y per term
+  // (bitwise-identical p and norms), 352 instead of 384 B per cell per term.
+  int pcur;         // buffer holding the last stored interpolant
+  int ppend;        // 1: the interpolant is pbuf[pcur] + pend_coef * ybuf[cur]
+  int defer;        // the iteration kernels of this call defer every other store
+  int pad3_;
+  double pend_coef; // coefficient of the pending term
 };
 
 enum LejaStatus {
@@ -210,9 +220,11 @@ int leja_loop_max_blocks(int nsm);
 // stencil partials buffer needs 6 doubles per block).
 cudaError_t launch_leja_tile_loop(const StencilArgs& a, int grid, int minb, cudaStream_t s);
 int leja_tile_loop_grid(const Geom& g, int nsm, int* minb);
-// p_out = pbuf[ctl->cur] (the interpolant of a finished call; no host read of cur).
-cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf, const LejaCtl* ctl,
-                                    long long n, cudaStream_t s);
+// p_out = the interpolant of a finished call: pbuf[pcur], plus pend_coef *
+// ybuf[cur] when a term is pending (no host read of the control block).
+cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf,
+                                    const double* const* ybuf, const LejaCtl* ctl, long long n,
+                                    cudaStream_t s);
 // jvp prologue on the device: sum(w^2) -> ||w||, eps and its divisor in jc
 // (status PW_RUNNING), or status PW_ZERO for a zero vector (linearize.py:62-65).
 cudaError_t launch_jvp_prep(const double* w, long long n, double unorm, PowerCtl* jc, RedBuf rb,
@@ -307,6 +319,13 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
   const double np = sqrt(sp);
   const double res = __ddiv_rn(__dmul_rn(fabs(cm), ny), fmax(1.0, np));
   ctl->cur ^= 1;
+  if (ctl->defer && !ctl->ppend) {   // this term kept p' in registers
+    ctl->ppend = 1;
+    ctl->pend_coef = cm;
+  } else {                           // this term stored p'
+    ctl->pcur ^= 1;
+    ctl->ppend = 0;
+  }
   ctl->residual = res;
   ctl->ynorm = ny;
   ctl->pnorm = np;
@@ -389,6 +408,8 @@ __device__ __forceinline__ void leja_init_ctl(LejaCtl* ctl, double sumsq) {
   if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
   ctl->m = 1;
   ctl->cur = 0;
+  ctl->pcur = 0;
+  ctl->ppend = 0;
   ctl->iters = 0;
   ctl->rhs_calls = 0;
   ctl->small_prev = 0;

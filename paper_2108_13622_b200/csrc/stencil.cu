@@ -221,6 +221,8 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   const double* pin = nullptr;
   double* pout = nullptr;
   double dt = 0.0, q = 0.0, xim = 0.0, cm = 0.0;
+  double pcoef = 0.0;          // coefficient of a pending interpolant term
+  int ppend = 0, pstore = 1;   // a term is pending / this term stores p'
   int zero_dir = 0;
   const double* hlo_dir = g.halo_lo_dir;
   const double* hhi_dir = g.halo_hi_dir;
@@ -246,8 +248,12 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     zero_dir = c->zero_dir;
     dir = a.ybuf[cur];
     yout = a.ybuf[cur ^ 1];
-    pin = a.pbuf[cur];
-    pout = a.pbuf[cur ^ 1];
+    const int pc = c->pcur;
+    pin = a.pbuf[pc];
+    pout = a.pbuf[pc ^ 1];
+    ppend = c->ppend;
+    pcoef = c->pend_coef;
+    pstore = !(c->defer && !ppend);
     dt = c->dt;
     q = c->q;
     xim = __ldg(a.xi + (m - 1));
@@ -272,9 +278,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       const double y = ld_dir<COH>(dir + i);
       const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
-      const double pn = __dadd_rn(ld_dir<COH>(pin + i), __dmul_rn(cm, yn));
+      double pb = ld_dir<COH>(pin + i);
+      if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));   // the pending term first
+      const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
       yout[i] = yn;
-      pout[i] = pn;
+      if (pstore) pout[i] = pn;
       if (P2P) {
         const int f = (int)(i / g.plane);
         const long long rem = i - (long long)f * g.plane;
@@ -534,9 +542,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
               const double yn = __dsub_rn(
                   qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                   __dmul_rn(xim, y));
-              const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
+              double pb = ep[f];
+              if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));   // pending term first
+              const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
               yout[i] = yn;
-              pout[i] = pn;
+              if (pstore) pout[i] = pn;
               if (P2P)
                 push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
                            g.nx, c_out, yn);
@@ -897,8 +907,11 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
     const int zero_dir = lc.zero_dir;
     const double* dir = a.ybuf[cur];
     double* yout = a.ybuf[cur ^ 1];
-    const double* pin = a.pbuf[cur];
-    double* pout = a.pbuf[cur ^ 1];
+    const double* pin = a.pbuf[lc.pcur];
+    double* pout = a.pbuf[lc.pcur ^ 1];
+    const int ppend = lc.ppend;
+    const double pcoef = lc.pend_coef;
+    const bool pstore = !(lc.defer && !ppend);
     const double xim = __ldg(a.xi + (m - 1));
     const double cm = __ldg(a.coeffs + m);
     double acc0 = 0.0, acc1 = 0.0;
@@ -911,9 +924,11 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
         const double y = __ldcg(dir + i);
         const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                     __dmul_rn(xim, y));
-        const double pn = __dadd_rn(__ldcg(pin + i), __dmul_rn(cm, yn));
+        double pb = __ldcg(pin + i);
+        if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+        const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
         yout[i] = yn;
-        pout[i] = pn;
+        if (pstore) pout[i] = pn;
         acc0 = __fma_rn(yn, yn, acc0);
         acc1 = __fma_rn(pn, pn, acc1);
       }
@@ -1062,9 +1077,11 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
             const double yn = __dsub_rn(
                 qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                 __dmul_rn(xim, y));
-            const double pn = __dadd_rn(ep[f], __dmul_rn(cm, yn));
+            double pb = ep[f];
+            if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+            const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
             yout[i] = yn;
-            pout[i] = pn;
+            if (pstore) pout[i] = pn;
             acc0 = __fma_rn(yn, yn, acc0);
             acc1 = __fma_rn(pn, pn, acc1);
           }

@@ -338,11 +338,11 @@ __global__ void __launch_bounds__(VT) leja_update_kernel(const double* __restric
                                                          const double* __restrict__ xi,
                                                          RedBuf rb) {
   if (ctl->status != LJ_RUNNING) return;
-  const int cur = ctl->cur, m = ctl->m;
+  const int cur = ctl->cur, m = ctl->m, pc = ctl->pcur;   // generic calls never defer
   const double* y = cur ? y1 : y0;
   double* yo = cur ? y0 : y1;
-  const double* p = cur ? p1 : p0;
-  double* po = cur ? p0 : p1;
+  const double* p = pc ? p1 : p0;
+  double* po = pc ? p0 : p1;
   const double dt = ctl->dt, q = ctl->q, theta = ctl->theta;
   const double xim = xi[m - 1], cm = coeffs[m];
   double acc[2] = {0.0, 0.0};
@@ -516,16 +516,22 @@ cudaError_t launch_fill(double* x, long long n, double v, cudaStream_t s) {
 
 __global__ void __launch_bounds__(VT) leja_copy_result_kernel(double* __restrict__ out,
                                                               const double* p0, const double* p1,
+                                                              const double* y0, const double* y1,
                                                               const LejaCtl* ctl, long long n) {
-  const double* __restrict__ src = ctl->cur ? p1 : p0;
+  const double* __restrict__ src = ctl->pcur ? p1 : p0;
+  const double* __restrict__ y = ctl->cur ? y1 : y0;
+  const int pend = ctl->ppend;
+  const double c = ctl->pend_coef;
   for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
        i += (long long)gridDim.x * VT)
-    out[i] = src[i];
+    out[i] = pend ? __dadd_rn(src[i], __dmul_rn(c, y[i])) : src[i];   // p + c*y (leja.py:140)
 }
 
-cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf, const LejaCtl* ctl,
-                                    long long n, cudaStream_t s) {
-  leja_copy_result_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(p_out, pbuf[0], pbuf[1], ctl, n);
+cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf,
+                                    const double* const* ybuf, const LejaCtl* ctl, long long n,
+                                    cudaStream_t s) {
+  leja_copy_result_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(p_out, pbuf[0], pbuf[1], ybuf[0],
+                                                               ybuf[1], ctl, n);
   return cudaGetLastError();
 }
 

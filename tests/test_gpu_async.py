@@ -224,3 +224,43 @@ def test_batched_driver_when_a_batch_ends_at_a_chunk_boundary():
     a, b = out["loop"], out["batch"]
     assert a.iterations > 64 and a.iterations == b.iterations and a.converged == b.converged
     assert torch.equal(a.vector, b.vector)
+
+
+@pytest.mark.parametrize("kw", [dict(loop=False), dict(loop=True, tile=False),
+                                dict(loop=True, tile=True)], ids=["batch", "slide", "tile"])
+def test_deferred_interpolant_stores_are_bitwise(kw):
+    """Every other Newton term keeps p' in registers and the next term stores
+    both additions in the reference's order: the interpolant, the residuals
+    and the iteration counts are bitwise those of a store per term, for
+    converged calls ending on either parity, a chunk growth, and a blow-up
+    (which returns the interpolant before the failing term)."""
+    from paper_2108_13622_b200 import _lib, leja, mhd
+    xb, st, op = _lin(n=40)
+    lin = xb.FrozenLinearization(op, st.flat())
+    alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    v = torch.from_numpy(np.random.default_rng(9).standard_normal(st.flat().numel())).cuda()
+    cases = [(1, 1.0, 1.0), (1, 3.0, 1.0), (3, 7.0, 1.0), (1, 80.0, 1.0), (1, 50.0, 1e-3)]
+    out = {}
+    try:
+        for defer in (0, 1):
+            for c in mhd._ctx_cache.values():
+                _lib.load().xmhd_set_leja_defer(c.h, defer)
+            with mode(**kw):
+                for l, adt, shrink in cases:
+                    leja._coeff_cache.clear()
+                    sh = xb.shift_and_scale(shrink * adt)
+                    r = xb.apply_phi_leja(l, xb.JacobianAction(lin), v, adt / alpha, sh, 1e-10)
+                    out[(defer, l, adt, shrink)] = r
+    finally:
+        for c in mhd._ctx_cache.values():
+            _lib.load().xmhd_set_leja_defer(c.h, 1)
+    parities = set()
+    for l, adt, shrink in cases:
+        a, b = out[(0, l, adt, shrink)], out[(1, l, adt, shrink)]
+        assert (a.iterations, a.converged, a.residual) == (b.iterations, b.converged, b.residual)
+        assert torch.equal(a.vector, b.vector)
+        if a.converged:
+            parities.add(a.iterations % 2)
+    assert parities == {0, 1}
+    assert not out[(1, 1, 50.0, 1e-3)].converged          # blow-up case
+    assert out[(1, 1, 80.0, 1.0)].iterations > 64          # chunk growth
