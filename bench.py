@@ -9,10 +9,10 @@ coefficient cache cleared per step so the host coefficient work is included.
           resident in HBM (state vectors 268 MB each >> 126 MB L2: no flush).
   e2e   : same metric through the public API with pinned HOST buffers: per step
           u and the 4 right-hand vectors are copied H2D and the 4 results D2H.
-  roofline : the fused Leja iteration kernel, 352 algorithmic B per cell per term
-          (read u, y, F(u), p; write y' every term and p' every other term:
-          deferred interpolant stores; 384 with XMHD_PDEFER=0)
-          (read u, y, F(u), p; write y', p'), timed with CUDA events on its stream.
+  roofline : the fused Leja iteration kernel, timed with CUDA events on its
+          stream.  Algorithmic bytes per cell per Newton term:
+          352 (deferred interpolant stores: every term reads u, y, F(u), p and
+          writes y'; every other term also writes p'), 384 with XMHD_PDEFER=0.
   cpu_baseline : the NumPy oracle (the reference's own algorithm, oracle/) on a
           bounded sample of the same workload on this host.
 
@@ -41,7 +41,8 @@ METRIC = "RHS/Jv cell-updates/s (fp64 GB/s vs HBM peak); wall-s per EXPRB step"
 SWEEP = (1.0, 10.0, 100.0, 300.0)
 LEJA_TOL = 1e-10
 # algorithmic bytes per cell per Newton term
-BYTES_PER_CELL_ITER = 384.0 if os.environ.get("XMHD_PDEFER", "1") == "0" else 352.0
+def bytes_per_cell_term(world):
+    return 384.0 if os.environ.get("XMHD_PDEFER", "1") == "0" else 352.0
 
 
 def parse():
@@ -319,7 +320,8 @@ def main():
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
     kern_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
     local_cells = u_dev.numel() // 8
-    achieved = BYTES_PER_CELL_ITER * local_cells / (kern_ms * 1e-3) / 1e9
+    bpc = bytes_per_cell_term(world)
+    achieved = bpc * local_cells / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
 
     # ---- end to end through the public API with pinned host buffers
@@ -381,12 +383,12 @@ def main():
                        "parallelism": f"y-strips x{world} (NCCL halo + allreduce)"
                                       if world > 1 else "single-gpu",
                        "stencil_plan": plan},
-            "gbs_algorithmic": value * BYTES_PER_CELL_ITER / 1e9,
+            "gbs_algorithmic": value * bpc / 1e9,
             "jv_per_s": value / n_cells,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
-                         "kernel_ms": kern_ms, "bytes_per_cell": BYTES_PER_CELL_ITER,
+                         "kernel_ms": kern_ms, "bytes_per_cell": bpc,
                          "traffic": ncu_traffic(args.n, local_cells)},
             "e2e": e2e,
             "gpu_launches": launches,

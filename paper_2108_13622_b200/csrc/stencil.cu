@@ -60,7 +60,10 @@ namespace cg = cooperative_groups;
 // prefetch to L2 only (neutral), GY ring in shared memory (-35%), L1 cache
 // hints (-10%), double2 shared-memory rings (neutral), 256-thread strips with
 // one CTA per SM (XB_SW=256: -20%, barrier stalls hit all 8 warps at once),
-// one-correction bodies for eps / theta when exact (neutral), 64-thread strips
+// one-correction bodies for eps / theta when exact (neutral), a "lookahead"
+// interpolant schedule in which every other term neither reads nor stores p
+// (320 B/cell/term, but the mode branches cost more than the traffic saved:
+// 0.338 vs 0.305 ms at 2048^2 on the same box), 64-thread strips
 // (0.327 vs 0.315 ms), the row loop unrolled by 3 so the PD / GY register
 // rings need no copies (-30% MOVs, but 0.337 ms: code size and scheduling).
 
