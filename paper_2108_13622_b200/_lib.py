@@ -16,7 +16,7 @@ from paper_2108_13622_b200 import build as _build
 OK, NONFINITE, BADARG, CUDA_ERROR = 0, 1, 2, 3
 BC_PERIODIC, BC_REFLECTING, BC_HALO = 0, 1, 2
 (LEJA_RUNNING, LEJA_CONVERGED, LEJA_BLOWUP, LEJA_RHS_NONFINITE, LEJA_NEED_COEFFS,
- LEJA_EXHAUSTED, LEJA_PEER_TIMEOUT) = range(7)
+ LEJA_EXHAUSTED, LEJA_PEER_TIMEOUT, LEJA_MODE_ERROR) = range(8)
 
 
 class NativeUnavailable(RuntimeError):

@@ -64,6 +64,7 @@ struct xmhd_ctx {
   double xi_h[500];            // host copy of the Leja points on the device
   bool xi_valid = false;
   bool leja_defer = true;      // deferred interpolant stores (XMHD_PDEFER=0: off)
+  int leja_next_term = 1;      // Newton term index of the next iteration launch
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
@@ -170,6 +171,17 @@ void fill_state(const LejaCtl& h, xmhd_leja_state* st) {
   st->ynorm = h.ynorm;
 }
 
+// One fused Leja term launch: the kernel variant compiled for the term's
+// interpolant mode (single-domain lookahead pairs), else the generic one.
+int launch_term(xmhd_ctx* c, const StencilArgs& a) {
+  const int defer = c->ctl_h->defer;
+  const int pm = (defer == 2) ? leja_pmode(c->leja_next_term, 2) : PM_ANY;
+  CK(launch_leja_term(a, c->grid, pm, c->stream));
+  c->leja_next_term++;
+  c->launches++;
+  return XMHD_OK;
+}
+
 int sync_ctl(xmhd_ctx* c) {
   CK(cudaMemcpyAsync(c->ctl_h, c->ctl, sizeof(LejaCtl), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -194,17 +206,23 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   // first batch: the caller's degree hint (xmhd_leja_hint; the host keys it by
   // phi order and interval scale), so most calls need a single sync
   const int done = c->ctl_h->iters;
+  if (c->ctl_h->m > 0) c->leja_next_term = c->ctl_h->m;   // resume after a stop
   int batch = c->hint_iters - done;
   if (batch < 2) batch = 2;
   if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
     for (int k = 0; k < batch; ++k) {
-      if (peer) CK(launch_leja_peer(a, c->grid, c->stream));
-      else CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
-      c->launches++;
+      if (peer) {
+        CK(launch_leja_peer(a, c->grid, c->stream));
+        c->launches++;
+      } else {
+        int rc = launch_term(c, a);
+        if (rc) return rc;
+      }
     }
     int rc = sync_ctl(c);
     if (rc) return rc;
+    c->leja_next_term = c->ctl_h->m;   // kernels launched past a stop exited
     if (c->ctl_h->status != LJ_RUNNING) break;
     batch = batch * 2 < c->batch_max ? batch * 2 : c->batch_max;
   }
@@ -255,7 +273,10 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.thetad = make_divisor(theta, c->force_ieee);
   h.force_ieee = c->force_ieee ? 1 : 0;
   h.epoch = c->p2p_epoch;
-  h.defer = (c->leja_defer && !generic) ? 1 : 0;   // the generic update stores every term
+  // the generic update stores every term; y-strips keep p (their all-reduce
+  // carries two sums); a single domain defers with lookahead
+  h.defer = (!c->leja_defer || generic) ? 0 : (c->g.bcy == BC_HALO ? 1 : 2);
+  c->leja_next_term = 1;
   *c->ctl_h = h;
   // staged from pageable memory at the call: back-to-back asynchronous
   // phi-actions never race on the pinned mirror
@@ -689,9 +710,13 @@ int xmhd_leja_launch(xmhd_ctx* c, int n, int peer) {
   StencilArgs a = leja_args(c);
   if (peer) a.p2p = c->p2p;
   for (int k = 0; k < n; ++k) {
-    if (peer) CK(launch_leja_peer(a, c->grid, c->stream));
-    else CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
-    c->launches++;
+    if (peer) {
+      CK(launch_leja_peer(a, c->grid, c->stream));
+      c->launches++;
+    } else {
+      int rc = launch_term(c, a);
+      if (rc) return rc;
+    }
   }
   return XMHD_OK;
 }
@@ -714,6 +739,10 @@ int xmhd_leja_sync(xmhd_ctx* c, xmhd_leja_state* st) {
   int rc = sync_ctl(c);
   if (rc) return rc;
   fill_state(*c->ctl_h, st);
+  if (c->ctl_h->status == LJ_MODE_ERROR)
+    return fail(XMHD_CUDA_ERROR, "Leja kernel variant / interpolant mode mismatch");
+  if (c->ctl_h->status == LJ_RUNNING || c->ctl_h->status == LJ_NEED_COEFFS)
+    c->leja_next_term = c->ctl_h->m;
   c->p2p_epoch = c->ctl_h->epoch;
   if (c->ctl_h->status == LJ_PEER_TIMEOUT)
     return fail(XMHD_CUDA_ERROR, "peer-memory exchange timed out (a rank stopped)");
@@ -730,7 +759,7 @@ static void loop_plan(xmhd_ctx* c) {
     const char* e = std::getenv("XMHD_TILE");
     const bool tile = !(e && std::atoi(e) == 0);
     c->tile_grid = tile ? leja_tile_loop_grid(c->g, c->nsm, &c->tile_minb) : 0;
-    if (c->tile_grid * 6 > c->partial_slots) c->tile_grid = 0;
+    if (c->tile_grid * 8 > c->partial_slots) c->tile_grid = 0;
   }
   if (c->loop_blocks < 0) c->loop_blocks = leja_loop_max_blocks(c->nsm);
 }
@@ -964,12 +993,16 @@ int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, do
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));  // warm-up term
+  rc = launch_term(c, a);  // warm-up term
+  if (rc) return rc;
   CK(cudaEventRecord(e0, c->stream));
-  for (int k = 0; k < n_iter; ++k) CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
+  for (int k = 0; k < n_iter; ++k) {
+    rc = launch_term(c, a);
+    if (rc) return rc;
+  }
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaEventSynchronize(e1));
-  c->launches += n_iter + 2;
+  c->launches += 1;
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e0, e1));
   cudaEventDestroy(e0);

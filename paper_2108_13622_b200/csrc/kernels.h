@@ -36,12 +36,36 @@ struct LejaCtl {
   // term adds c_m*y_m (its own direction) before its own update and stores.
   // Same two roundings per element as the reference's p = p + c*y per term
   // (bitwise-identical p and norms), 352 instead of 384 B per cell per term.
+  // defer == 2 (single domain, "lookahead"): an odd term neither reads nor
+  // stores p (y' and ||y'|| only, 256 B/cell); the even term after it reads
+  // p, forms p_m = p + c_m*y_m and ||p_m|| (resolving the odd term's
+  // residual first, in the reference's order) and then its own update, and
+  // stores (384 B/cell): 320 B per term.  A call that converged on the odd
+  // term discards the even one (no iteration, no RHS call counted).
   int pcur;         // buffer holding the last stored interpolant
   int ppend;        // 1: the interpolant is pbuf[pcur] + pend_coef * ybuf[cur]
-  int defer;        // the iteration kernels of this call defer every other store
-  int pad3_;
+  int defer;        // 0: store every term; 1: every other term; 2: with lookahead
+  int pmode;        // LejaPMode of the next term (= leja_pmode(m, defer))
   double pend_coef; // coefficient of the pending term
+  double pend_ynorm;// ||y|| of a term whose residual is not resolved yet
 };
+
+// What a term does with the interpolant.
+enum LejaPMode {
+  PM_ANY = -1,    // (kernel template) read the mode from the control block
+  PM_STORE = 0,   // read p (+ pending term), add c*y', store
+  PM_KEEP = 1,    // read p, add c*y' in registers for ||p'||, no store (defer 1)
+  PM_SKIP = 2,    // neither read nor store p: y' and ||y'|| only (defer 2)
+  PM_LOOK = 3,    // read p, add the pending term (||.|| of it), add c*y', store
+};
+
+// The mode of term m: a pure function of m, so the host launches the kernel
+// variant compiled for it (and the kernel checks it against the device's).
+__host__ __device__ __forceinline__ int leja_pmode(int m, int defer) {
+  if (defer == 2) return m >= 499 ? PM_STORE : ((m & 1) ? PM_SKIP : PM_LOOK);
+  if (defer == 1) return (m & 1) ? PM_KEEP : PM_STORE;
+  return PM_STORE;
+}
 
 enum LejaStatus {
   LJ_RUNNING = 0,
@@ -51,6 +75,7 @@ enum LejaStatus {
   LJ_NEED_COEFFS = 4,  // m reached the coefficient chunk size (leja.py:128-130)
   LJ_EXHAUSTED = 5,    // 499 terms without convergence (leja.py:149-150)
   LJ_PEER_TIMEOUT = 6, // y-strips over peer memory: a peer never posted its sums
+  LJ_MODE_ERROR = 7,   // a kernel variant launched for another interpolant mode
 };
 
 // Device-resident power iteration of estimate_alpha (linearize.py:113-135):
@@ -140,6 +165,8 @@ constexpr int SOUT = SW - 4;     // output columns per strip
 size_t stencil_smem_bytes();
 void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows, int& grid);
 cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s);
+// One Newton term with the variant compiled for its interpolant mode (LejaPMode).
+cudaError_t launch_leja_term(const StencilArgs& a, int grid, int pmode, cudaStream_t s);
 
 // Vector kernels (vec.cu).
 struct RedBuf {
@@ -298,11 +325,43 @@ __device__ __forceinline__ bool p2p_allreduce3(const P2PArgs& x, unsigned long l
   return true;
 }
 
+// Next FD step and zero-direction flag from ||y|| (linearize.py:62-65).
+__device__ __forceinline__ void leja_next_eps(LejaCtl* ctl, double ny) {
+  const double kSqrtEps = 1.4901161193847656e-08;  // linearize.py:15
+  ctl->zero_dir = (ny == 0.0);
+  ctl->eps = __ddiv_rn(__dmul_rn(kSqrtEps, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
+                       ny < 1e-300 ? 1e-300 : ny);
+  ctl->epsd = make_divisor_dev(ctl->eps);
+  if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
+}
+
 // Control update after one Newton term (leja.py:134-148); run by one thread
 // of the last CTA of the iteration kernel, after the deterministic reduction.
-__device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp, int bad,
-                                              int counted, double cm) {
-  const double kSqrtEps = 1.4901161193847656e-08;  // linearize.py:15
+// sy = sum y'^2, sp = sum p'^2 of this term; sp_prev = sum p_{m-1}^2 of the
+// pending term a PM_LOOK term resolves first.
+__device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp, double sp_prev,
+                                              int bad, int counted, double cm) {
+  const int mode = ctl->pmode;
+  if (mode == PM_LOOK) {
+    // the previous (odd) term's residual (leja.py:141-145), in the reference's order
+    const double np_prev = sqrt(sp_prev);
+    const double res_prev = __ddiv_rn(__dmul_rn(fabs(ctl->pend_coef), ctl->pend_ynorm),
+                                      fmax(1.0, np_prev));
+    ctl->residual = res_prev;
+    ctl->pnorm = np_prev;
+    if (res_prev <= ctl->tol) {
+      if (ctl->small_prev) {
+        // converged on the odd term: this term never happened (no iteration,
+        // no RHS call); the interpolant is pbuf[pcur] + pend_coef * ybuf[cur]
+        ctl->m -= 1;
+        ctl->status = LJ_CONVERGED;
+        return;
+      }
+      ctl->small_prev = 1;
+    } else {
+      ctl->small_prev = 0;
+    }
+  }
   ctl->iters += 1;
   if (counted) ctl->rhs_calls += 1;
   if (bad) {  // mhd.py:225-231 raised inside the matvec
@@ -312,17 +371,32 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
   }
   const double ny = sqrt(sy);
   if (!isfinite(ny) || ny > ctl->blowup) {
+    // the reference returns the interpolant before this term: pbuf[pcur]
+    // (+ the pending term, whose y is still ybuf[cur])
     ctl->residual = CUDART_INF;
     ctl->status = LJ_BLOWUP;
+    return;
+  }
+  if (mode == PM_SKIP) {
+    // residual unresolved until the next term has ||p_m||
+    ctl->cur ^= 1;
+    ctl->ppend = 1;
+    ctl->pend_coef = cm;
+    ctl->pend_ynorm = ny;
+    ctl->ynorm = ny;
+    ctl->m += 1;   // <= 498
+    ctl->pmode = leja_pmode(ctl->m, ctl->defer);
+    if (ctl->m >= ctl->ncoef) ctl->status = LJ_NEED_COEFFS;
+    leja_next_eps(ctl, ny);
     return;
   }
   const double np = sqrt(sp);
   const double res = __ddiv_rn(__dmul_rn(fabs(cm), ny), fmax(1.0, np));
   ctl->cur ^= 1;
-  if (ctl->defer && !ctl->ppend) {   // this term kept p' in registers
+  if (mode == PM_KEEP) {   // this term kept p' in registers
     ctl->ppend = 1;
     ctl->pend_coef = cm;
-  } else {                           // this term stored p'
+  } else {                 // this term stored p'
     ctl->pcur ^= 1;
     ctl->ppend = 0;
   }
@@ -344,11 +418,8 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
     return;
   }
   if (ctl->m >= ctl->ncoef) ctl->status = LJ_NEED_COEFFS;
-  ctl->zero_dir = (ny == 0.0);
-  ctl->eps = __ddiv_rn(__dmul_rn(kSqrtEps, ctl->unorm > 1.0 ? ctl->unorm : 1.0),
-                       ny < 1e-300 ? 1e-300 : ny);
-  ctl->epsd = make_divisor_dev(ctl->eps);
-  if (ctl->force_ieee) ctl->epsd.kind = DIV_IEEE;
+  ctl->pmode = leja_pmode(ctl->m, ctl->defer);
+  leja_next_eps(ctl, ny);
 }
 
 // Power iteration, after the fused JVP reduced sum((J w)^2) (linearize.py:121-133).
@@ -410,6 +481,7 @@ __device__ __forceinline__ void leja_init_ctl(LejaCtl* ctl, double sumsq) {
   ctl->cur = 0;
   ctl->pcur = 0;
   ctl->ppend = 0;
+  ctl->pmode = leja_pmode(1, ctl->defer);
   ctl->iters = 0;
   ctl->rhs_calls = 0;
   ctl->small_prev = 0;

@@ -60,10 +60,9 @@ namespace cg = cooperative_groups;
 // prefetch to L2 only (neutral), GY ring in shared memory (-35%), L1 cache
 // hints (-10%), double2 shared-memory rings (neutral), 256-thread strips with
 // one CTA per SM (XB_SW=256: -20%, barrier stalls hit all 8 warps at once),
-// one-correction bodies for eps / theta when exact (neutral), a "lookahead"
-// interpolant schedule in which every other term neither reads nor stores p
-// (320 B/cell/term, but the mode branches cost more than the traffic saved:
-// 0.338 vs 0.305 ms at 2048^2 on the same box), 64-thread strips
+// one-correction bodies for eps / theta when exact (neutral), the lookahead
+// interpolant schedule with runtime mode branches in one kernel (0.338 vs
+// 0.305 ms at 2048^2: hence one compiled variant per mode), 64-thread strips
 // (0.327 vs 0.315 ms), the row loop unrolled by 3 so the PD / GY register
 // rings need no copies (-30% MOVs, but 0.337 ms: code size and scheduling).
 
@@ -197,7 +196,7 @@ __device__ __forceinline__ void push_ghost(double* dlo, int mlo, double* dhi, in
 // One launch of the fused stencil.  bid / nblk: this block's index among the
 // nblk blocks working on this rank's grid (the launch grid, except in the
 // one-launch emulation of several ranks).
-template <int MODE, int KX, int KY, int XR>
+template <int MODE, int KX, int KY, int XR, int PM = PM_ANY>
 __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid,
                                              const int nblk) {
   constexpr bool P2P = (XR == XR_PEER || XR == XR_EMUL);
@@ -225,7 +224,8 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   double* pout = nullptr;
   double dt = 0.0, q = 0.0, xim = 0.0, cm = 0.0;
   double pcoef = 0.0;          // coefficient of a pending interpolant term
-  int ppend = 0, pstore = 1;   // a term is pending / this term stores p'
+  int ppend = 0;               // a term is pending (pbuf[pcur] + pcoef * y)
+  int pm_rt = PM_STORE;        // LejaPMode of this term (control block)
   int zero_dir = 0;
   const double* hlo_dir = g.halo_lo_dir;
   const double* hhi_dir = g.halo_hi_dir;
@@ -256,7 +256,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     pout = a.pbuf[pc ^ 1];
     ppend = c->ppend;
     pcoef = c->pend_coef;
-    pstore = !(c->defer && !ppend);
+    pm_rt = c->pmode;
+    if (PM != PM_ANY && pm_rt != PM) {   // variant launched for another mode
+      if (bid == 0 && threadIdx.x == 0) a.ctl->status = LJ_MODE_ERROR;
+      return;
+    }
     dt = c->dt;
     q = c->q;
     xim = __ldg(a.xi + (m - 1));
@@ -271,8 +275,14 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     epsd = pc->epsd;
   }
 
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;   // sums of y'^2, p'^2, pending p^2
   int bad = 0;
+  // interpolant handling of this term: compile-time for the PM variants
+  const int pmode = (PM == PM_ANY) ? pm_rt : PM;
+  const bool pread = (pmode != PM_SKIP);
+  const bool pstore = (pmode == PM_STORE || pmode == PM_LOOK);
+  const bool padd = (PM == PM_LOOK) ? true : (PM == PM_SKIP ? false : (ppend != 0));
+  const bool pnorm2 = (pmode == PM_LOOK);
 
   if (MODE == MODE_LEJA && zero_dir) {
     // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
@@ -281,11 +291,17 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       const double y = ld_dir<COH>(dir + i);
       const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
-      double pb = ld_dir<COH>(pin + i);
-      if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));   // the pending term first
-      const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
       yout[i] = yn;
-      if (pstore) pout[i] = pn;
+      double pn = 0.0;
+      if (pread) {
+        double pb = ld_dir<COH>(pin + i);
+        if (padd) {   // the pending term first
+          pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+          if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+        }
+        pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+        if (pstore) pout[i] = pn;
+      }
       if (P2P) {
         const int f = (int)(i / g.plane);
         const long long rem = i - (long long)f * g.plane;
@@ -384,7 +400,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
           }
           if (do_epi) {
 #pragma unroll
-            for (int k = t; k < (MODE == MODE_LEJA ? 24 : 8) * LPR; k += SW) {
+            for (int k = t; k < (MODE == MODE_LEJA ? (pread ? 24 : 16) : 8) * LPR; k += SW) {
               const double* base = (k < 8 * LPR) ? a.fu : (k < 16 * LPR ? dir : pin);
               const int ff = (k / LPR) & 7, sg = k % LPR;
               const int cc = min(max(X0 - 2 + sg * 16, 0), g.nx - 1);
@@ -404,7 +420,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
             efu[f] = __ldg(a.fu + i);
             if (MODE == MODE_LEJA) {
               ey[f] = ld_dir<COH>(dir + i);
-              ep[f] = ld_dir<COH>(pin + i);
+              if (pread) ep[f] = ld_dir<COH>(pin + i);
             }
           }
         }
@@ -545,11 +561,17 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
               const double yn = __dsub_rn(
                   qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                   __dmul_rn(xim, y));
-              double pb = ep[f];
-              if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));   // pending term first
-              const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
               yout[i] = yn;
-              if (pstore) pout[i] = pn;
+              double pn = 0.0;
+              if (pread) {
+                double pb = ep[f];
+                if (padd) {   // the pending term first
+                  pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+                  if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+                }
+                pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+                if (pstore) pout[i] = pn;
+              }
               if (P2P)
                 push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
                            g.nx, c_out, yn);
@@ -571,11 +593,14 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   if (bad) atomicOr(a.bad, 1);
   if (MODE == MODE_RHS) return;
 
+  constexpr bool NEED_S2 = (MODE == MODE_LEJA) && (PM == PM_ANY || PM == PM_LOOK);
   const double s0 = block_sum(acc0, red);
-  const double s1 = (MODE == MODE_LEJA) ? block_sum(acc1, red) : 0.0;
+  const double s1 = (MODE == MODE_LEJA && PM != PM_SKIP) ? block_sum(acc1, red) : 0.0;
+  const double s2 = NEED_S2 ? block_sum(acc2, red) : 0.0;
   if (t == 0) {
-    a.partials[2 * bid] = s0;
-    a.partials[2 * bid + 1] = s1;
+    a.partials[3 * bid] = s0;
+    a.partials[3 * bid + 1] = s1;
+    a.partials[3 * bid + 2] = s2;
     // peer memory: this block's ghost-row stores to the neighbours must be
     // visible system-wide before the last block publishes the epoch
     if (P2P) __threadfence_system();
@@ -587,8 +612,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   if (!am_last) return;
   __threadfence();
   if (t < 32) {
-    const double sy = sum_partials(a.partials, nblk, 2, 0);
-    const double sp = (MODE == MODE_LEJA) ? sum_partials(a.partials, nblk, 2, 1) : 0.0;
+    const double sy = sum_partials(a.partials, nblk, 3, 0);
+    const double sp = (MODE == MODE_LEJA && PM != PM_SKIP) ? sum_partials(a.partials, nblk, 3, 1)
+                                                            : 0.0;
+    const double sp2 = NEED_S2 ? sum_partials(a.partials, nblk, 3, 2) : 0.0;
     if (t == 0) {
       if (MODE == MODE_JVP && a.pctl) {
         power_after_jvp(a.pctl, sy, *((volatile int*)a.bad));
@@ -603,7 +630,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         const unsigned long long ep = c->epoch + 1;
         c->epoch = ep;
         if (p2p_allreduce3(a.p2p, ep, v, tot))
-          leja_finalize(c, tot[0], tot[1], tot[2] > 0.0, !zero_dir, cm);
+          leja_finalize(c, tot[0], tot[1], 0.0, tot[2] > 0.0, !zero_dir, cm);   // defer <= 1
         else
           c->status = LJ_PEER_TIMEOUT;
       } else if (a.ext_sums) {
@@ -614,7 +641,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         a.ext_sums[2] = *((volatile int*)a.bad) ? 1.0 : 0.0;
       } else {
         const int flag = *((volatile int*)a.bad);
-        leja_finalize(a.ctl, sy, sp, flag, !zero_dir, cm);
+        leja_finalize(a.ctl, sy, sp, sp2, flag, !zero_dir, cm);
       }
       if (MODE == MODE_JVP) a.result[1] = sy;   // local sum of squares (y-strips)
       *a.ticket = 0u;
@@ -622,9 +649,9 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   }
 }
 
-template <int MODE, int KX, int KY>
+template <int MODE, int KX, int KY, int PM = PM_ANY>
 __global__ void __launch_bounds__(SW, SW_MINB) stencil_kernel(const StencilArgs a) {
-  stencil_body<MODE, KX, KY, XR_NONE>(a, blockIdx.x, gridDim.x);
+  stencil_body<MODE, KX, KY, XR_NONE, PM>(a, blockIdx.x, gridDim.x);
 }
 
 // Fused Leja iteration of one y-strip with the peer-memory exchange.
@@ -710,18 +737,18 @@ void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_ro
 
 namespace {
 
-template <int MODE, int KX, int KY>
+template <int MODE, int KX, int KY, int PM = PM_ANY>
 cudaError_t launch_one(const StencilArgs& a, int grid, cudaStream_t s) {
   static bool attr_done = false;
   const size_t smem = stencil_smem_bytes();
   if (!attr_done) {
-    cudaError_t err = cudaFuncSetAttribute(stencil_kernel<MODE, KX, KY>,
+    cudaError_t err = cudaFuncSetAttribute(stencil_kernel<MODE, KX, KY, PM>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
     if (err != cudaSuccess) return err;
     attr_done = true;
   }
-  stencil_kernel<MODE, KX, KY><<<grid, SW, smem, s>>>(a);
+  stencil_kernel<MODE, KX, KY, PM><<<grid, SW, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -743,10 +770,10 @@ cudaError_t with_div_kinds(const Geom& g, F&& f) {
   return f(K1{}, K1{});
 }
 
-template <int MODE>
+template <int MODE, int PM = PM_ANY>
 cudaError_t launch_mode(const StencilArgs& a, int grid, cudaStream_t s) {
   return with_div_kinds(a.g, [&](auto X, auto Y) {
-    return launch_one<MODE, decltype(X)::value, decltype(Y)::value>(a, grid, s);
+    return launch_one<MODE, decltype(X)::value, decltype(Y)::value, PM>(a, grid, s);
   });
 }
 
@@ -892,7 +919,7 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
   extern __shared__ __align__(16) double smem_raw[];
   TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
   __shared__ LejaCtl lc;
-  __shared__ double red[3][TNT / 32];
+  __shared__ double red[4][TNT / 32];
   cg::grid_group grid = cg::this_grid();
   const Geom& g = a.g;
   const int t = threadIdx.x;
@@ -914,10 +941,11 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
     double* pout = a.pbuf[lc.pcur ^ 1];
     const int ppend = lc.ppend;
     const double pcoef = lc.pend_coef;
-    const bool pstore = !(lc.defer && !ppend);
+    const int pmode = lc.pmode;
+    const bool pread = (pmode != PM_SKIP), pstore = (pmode == PM_STORE || pmode == PM_LOOK);
     const double xim = __ldg(a.xi + (m - 1));
     const double cm = __ldg(a.coeffs + m);
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
     int bad = 0;
 
     if (zero_dir) {
@@ -927,13 +955,18 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
         const double y = __ldcg(dir + i);
         const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                     __dmul_rn(xim, y));
-        double pb = __ldcg(pin + i);
-        if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
-        const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
         yout[i] = yn;
-        if (pstore) pout[i] = pn;
         acc0 = __fma_rn(yn, yn, acc0);
-        acc1 = __fma_rn(pn, pn, acc1);
+        if (pread) {
+          double pb = __ldcg(pin + i);
+          if (ppend) {
+            pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+            if (pmode == PM_LOOK) acc2 = __fma_rn(pb, pb, acc2);
+          }
+          const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+          if (pstore) pout[i] = pn;
+          acc1 = __fma_rn(pn, pn, acc1);
+        }
       }
     } else {
       for (int tile = bid; tile < ntiles; tile += nblk) {
@@ -948,7 +981,7 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
           const unsigned i = obase + (unsigned)f * plane;
           efu[f] = __ldg(a.fu + i);
           ey[f] = __ldcg(dir + i);
-          ep[f] = __ldcg(pin + i);
+          if (pread) ep[f] = __ldcg(pin + i);
         }
         // ---- phase 1: primitives and ideal fluxes on the tile + halo (2 cells / thread)
 #pragma unroll
@@ -1080,48 +1113,57 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
             const double yn = __dsub_rn(
                 qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
                 __dmul_rn(xim, y));
-            double pb = ep[f];
-            if (ppend) pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
-            const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
             yout[i] = yn;
-            if (pstore) pout[i] = pn;
             acc0 = __fma_rn(yn, yn, acc0);
-            acc1 = __fma_rn(pn, pn, acc1);
+            if (pread) {
+              double pb = ep[f];
+              if (ppend) {
+                pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+                if (pmode == PM_LOOK) acc2 = __fma_rn(pb, pb, acc2);
+              }
+              const double pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+              if (pstore) pout[i] = pn;
+              acc1 = __fma_rn(pn, pn, acc1);
+            }
           }
         }
         __syncthreads();   // shared tiles are rewritten by the next tile
       }
     }
 
-    // ---- term end: publish [sum y'^2, sum p'^2, bad], barrier, every block reduces
+    // ---- term end: publish [sum y'^2, sum p'^2, sum pending p^2, bad], barrier,
+    // every block reduces
     {
-      double v0 = acc0, v1 = acc1, v2 = bad ? 1.0 : 0.0;
+      double v[4] = {acc0, acc1, acc2, bad ? 1.0 : 0.0};
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-      }
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
       const int w = t >> 5, l = t & 31;
-      if (l == 0) { red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; }
+      if (l == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) red[k][w] = v[k];
+      }
       __syncthreads();
       if (t == 0) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-        for (int k = 0; k < TNT / 32; ++k) { s0 += red[0][k]; s1 += red[1][k]; s2 += red[2][k]; }
-        double* slot = a.partials + ((size_t)par * nblk + bid) * 3;
-        slot[0] = s0;
-        slot[1] = s1;
-        slot[2] = s2;
+        double* slot = a.partials + ((size_t)par * nblk + bid) * 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double sk = 0.0;
+          for (int j = 0; j < TNT / 32; ++j) sk += red[k][j];
+          slot[k] = sk;
+        }
       }
     }
     grid.sync();
     if (t < 32) {
-      const double* base = a.partials + (size_t)par * nblk * 3;
-      const double sy = sum_partials(base, nblk, 3, 0);
-      const double sp = sum_partials(base, nblk, 3, 1);
-      const double sb = sum_partials(base, nblk, 3, 2);
+      const double* base = a.partials + (size_t)par * nblk * 4;
+      const double sy = sum_partials(base, nblk, 4, 0);
+      const double sp = sum_partials(base, nblk, 4, 1);
+      const double sp2 = sum_partials(base, nblk, 4, 2);
+      const double sb = sum_partials(base, nblk, 4, 3);
       if (t == 0) {
-        leja_finalize(&lc, sy, sp, sb > 0.0, !zero_dir, cm);
+        leja_finalize(&lc, sy, sp, sp2, sb > 0.0, !zero_dir, cm);
         if (bid == 0) *a.ctl = lc;
       }
     }
@@ -1186,6 +1228,16 @@ int leja_tile_loop_grid(const Geom& g, int nsm, int* minb) {
   *minb = mb;
   const long long cap = (long long)n * nsm;
   return (int)(ntiles < cap ? ntiles : cap);
+}
+
+// One Newton term with the kernel variant compiled for its interpolant mode
+// (leja_pmode of the term: lookahead pairs on one domain).
+cudaError_t launch_leja_term(const StencilArgs& a, int grid, int pmode, cudaStream_t s) {
+  switch (pmode) {
+    case PM_SKIP: return launch_mode<MODE_LEJA, PM_SKIP>(a, grid, s);
+    case PM_LOOK: return launch_mode<MODE_LEJA, PM_LOOK>(a, grid, s);
+    default: return launch_mode<MODE_LEJA>(a, grid, s);
+  }
 }
 
 cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s) {

@@ -291,7 +291,7 @@ __global__ void leja_init_finalize_kernel(LejaCtl* ctl, const double* sums) {
 __global__ void leja_finalize_kernel(LejaCtl* ctl, const double* sums,
                                      const double* __restrict__ coeffs) {
   if (ctl->status != LJ_RUNNING) return;
-  leja_finalize(ctl, sums[0], sums[1], sums[2] > 0.0, !ctl->zero_dir, coeffs[ctl->m]);
+  leja_finalize(ctl, sums[0], sums[1], 0.0, sums[2] > 0.0, !ctl->zero_dir, coeffs[ctl->m]);
 }
 
 // Halo rows of the current Newton basis vector (y-strips): rows 0,1 go to the
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(VT) leja_update_kernel(const double* __restric
     acc[1] = __fma_rn(pn, pn, acc[1]);
   }
   double tot[2];
-  if (grid_reduce<2, false>(acc, rb, tot)) leja_finalize(ctl, tot[0], tot[1], 0, 0, cm);
+  if (grid_reduce<2, false>(acc, rb, tot)) leja_finalize(ctl, tot[0], tot[1], 0.0, 0, 0, cm);
 }
 
 // One modified Gram-Schmidt update of the Arnoldi loop (krylov.py:60-67):

@@ -277,7 +277,9 @@ def drive_fused(lib, h, l, q, theta, coeffs, peer=False):
         chunk = plan[-1][1] if plan else 64
         _grow(l, q, theta, chunk, _cache().get((l, q, theta)), st.m)
         raise RuntimeError("coefficient table ended early")   # not reached
-    _degree_hint[hkey] = int(st.iterations)
+    # + 1: on one domain a term's convergence is resolved by the next launch
+    # (deferred interpolant with lookahead, csrc/kernels.h)
+    _degree_hint[hkey] = int(st.iterations) + 1
     return st
 
 
