@@ -390,6 +390,8 @@ def main():
             "jv_per_s": value / n_cells,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_kind,
+                         # the same term at the reference's 384 B/cell traffic
+                         "frac_at_384B": 384.0 * local_cells / (kern_ms * 1e-3) / 1e9 / peak,
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
                          "kernel_ms": kern_ms, "bytes_per_cell": bpc,
                          "traffic": ncu_traffic(args.n, local_cells)},

@@ -926,7 +926,15 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
   const int bid = blockIdx.x, nblk = gridDim.x;
   const int ntx = (g.nx + TX - 1) / TX, nty = (g.ny + TY - 1) / TY, ntiles = ntx * nty;
   const unsigned plane = (unsigned)g.plane;
-  if (t == 0) lc = *a.ctl;
+  if (t == 0) {
+    lc = *a.ctl;
+    // small grids are not bandwidth-bound: a fresh call stores p every term
+    // (no interpolant schedule, the lean reduction path below)
+    if (lc.m == 1 && !lc.ppend) {
+      lc.defer = 0;
+      lc.pmode = PM_STORE;
+    }
+  }
   __syncthreads();
   int par = 0;
   for (;;) {
@@ -1157,11 +1165,23 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
     }
     grid.sync();
     if (t < 32) {
+      // the four sums in one pass over the slots (fixed order: lanes stride
+      // the blocks, then one shuffle tree per sum)
       const double* base = a.partials + (size_t)par * nblk * 4;
-      const double sy = sum_partials(base, nblk, 4, 0);
-      const double sp = sum_partials(base, nblk, 4, 1);
-      const double sp2 = sum_partials(base, nblk, 4, 2);
-      const double sb = sum_partials(base, nblk, 4, 3);
+      double r4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int b = t; b < nblk; b += 32) {
+        const double2 lo = __ldcg(reinterpret_cast<const double2*>(base + 4 * b));
+        const double2 hi = __ldcg(reinterpret_cast<const double2*>(base + 4 * b + 2));
+        r4[0] += lo.x;
+        r4[1] += lo.y;
+        r4[2] += hi.x;
+        r4[3] += hi.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r4[k] += __shfl_xor_sync(0xffffffffu, r4[k], o);
+      const double sy = r4[0], sp = r4[1], sp2 = r4[2], sb = r4[3];
       if (t == 0) {
         leja_finalize(&lc, sy, sp, sp2, sb > 0.0, !zero_dir, cm);
         if (bid == 0) *a.ctl = lc;
