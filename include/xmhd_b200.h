@@ -132,6 +132,22 @@ int xmhd_lincomb_async(xmhd_ctx* ctx, double* out, long long n, const double* co
 int xmhd_diff_norms_async(xmhd_ctx* ctx, const double* a, const double* b, long long n);
 int xmhd_async_fetch(xmhd_ctx* ctx, xmhd_step_record* out);
 
+/* One exponential Rosenbrock step enqueued natively with the operations and
+ * order of the asynchronous Python step (integrators.py:156-199): scheme
+ * XMHD_SCHEME_EXPRB43 (5 phi-actions) or XMHD_SCHEME_EXPRB54S4 (10).
+ * phi_param: per phi-action, in call order, [dt_eff, q, theta] as the host
+ * computed them (shift_and_scale); tables: per phi-action the first 64 Newton
+ * coefficients (the host's _newton_coeffs, keeping the reference's cache);
+ * tiny_alpha: alpha < 1e-14, phi_l(0) v = v / l! without Leja.  work:
+ * XMHD_STEP_WORK * n doubles of scratch; u_new: the higher-order solution.
+ * Starts a step record (xmhd_async_begin); read it with xmhd_async_fetch. */
+#define XMHD_SCHEME_EXPRB43 0
+#define XMHD_SCHEME_EXPRB54S4 1
+#define XMHD_STEP_WORK 20
+int xmhd_step_async(xmhd_ctx* ctx, int scheme, const double* u, const double* fu, double unorm,
+                    long long n, double dt, const double* phi_param, const double* tables,
+                    int tiny_alpha, double tol, const double* xi, double* work, double* u_new);
+
 /* Power iteration of estimate_alpha (linearize.py:113-135; replaces the loop at
  * linearize.py:118-133 that the reference runs over jvp and np.linalg.norm).
  * w0: start vector (read only; a zero w0 starts from ones as linearize.py:115-116).

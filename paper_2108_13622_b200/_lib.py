@@ -71,6 +71,7 @@ _SIGS = {
     "xmhd_lincomb_async": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I]),
     "xmhd_diff_norms_async": (_I, [_P, _P, _P, _L]),
     "xmhd_async_fetch": (_I, [_P, ctypes.POINTER(StepRecord)]),
+    "xmhd_step_async": (_I, [_P, _I, _P, _P, _D, _L, _D, _PD, _PD, _I, _D, _PD, _P, _P]),
     "xmhd_power": (_I, [_P, _P, _P, _D, _P, _P, _P, _I, _D, _PD, _PI, _PI, _PI]),
     "xmhd_linearize": (_I, [_P, _P, _P, _PD]),
     "xmhd_norm": (_I, [_P, _P, _L, _PD]),

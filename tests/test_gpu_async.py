@@ -264,3 +264,29 @@ def test_deferred_interpolant_stores_are_bitwise(kw):
     assert parities == {0, 1}
     assert not out[(1, 1, 50.0, 1e-3)].converged          # blow-up case
     assert out[(1, 1, 80.0, 1.0)].iterations > 64          # chunk growth
+
+
+@pytest.mark.parametrize("which", ["kh", "harris"])
+def test_native_step_is_bitwise_the_python_issued_step(which):
+    """xmhd_step_async (csrc/steps.cpp) enqueues the operations of
+    _step_exprb43 / _step_exprb54s4 in the same order: the same run bit for
+    bit as the asynchronous step issued from Python."""
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import integrators, scenarios as sc
+    if which == "kh":
+        setup, scheme, tol = sc.kh_setup(32, t_final=0.15), xb.Scheme.EXPRB43, 1e-4
+    else:
+        setup, scheme, tol = sc.harris_setup(32, t_final=0.6), xb.Scheme.EXPRB54S4, 1e-6
+    out = {}
+    old = integrators.NATIVE_STEP
+    try:
+        for native in (False, True):
+            integrators.NATIVE_STEP = native
+            with mode(async_on=True, loop=True):
+                out[native] = _run(setup, scheme, tol)
+    finally:
+        integrators.NATIVE_STEP = old
+    (a, sa, ka), (b, sb, kb) = out[False], out[True]
+    assert sa == sb and ka == kb
+    assert (a.rhs_evals, a.phi_iterations, a.checksum) == (b.rhs_evals, b.phi_iterations,
+                                                           b.checksum)
