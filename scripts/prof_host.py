@@ -14,7 +14,10 @@ import paper_2108_13622_b200 as xb  # noqa: E402
 from paper_2108_13622_b200 import leja, scenarios as sc  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c0"
-if which == "c0":
+if which == "c3":
+    mk = lambda tf=None: sc.kh_setup(4096, tol=1e-5, t_final=1e9, max_accepted=(2 if tf else 20))  # noqa: E731
+    scheme = xb.Scheme.EXPRB43
+elif which == "c0":
     mk = lambda tf=None: sc.kh_setup(128) if tf is None else sc.kh_setup(128, t_final=tf)  # noqa: E731
     scheme = xb.Scheme.EXPRB43
 else:
@@ -22,11 +25,12 @@ else:
     scheme = xb.Scheme.EXPRB54S4
 tf = float(sys.argv[2]) if len(sys.argv) > 2 else None
 s = mk(tf)
-xb.run(xb.RunConfig(scenario=mk(0.02), scheme=scheme, tol=s.tol))   # warm
+xb.run(xb.RunConfig(scenario=mk(0.02), scheme=scheme, tol=s.tol,
+                    max_accepted=mk(0.02).max_accepted))   # warm
 leja._coeff_cache.clear()
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol))
+rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol, max_accepted=s.max_accepted))
 torch.cuda.synchronize()
 wall = time.perf_counter() - t0
 print(f"{which}: wall {wall:.4f} s, {rep.accepted} accepted, {rep.rhs_evals} rhs, "
@@ -35,7 +39,7 @@ print(f"{which}: wall {wall:.4f} s, {rep.accepted} accepted, {rep.rhs_evals} rhs
 leja._coeff_cache.clear()
 pr = cProfile.Profile()
 pr.enable()
-rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol))
+rep = xb.run(xb.RunConfig(scenario=s, scheme=scheme, tol=s.tol, max_accepted=s.max_accepted))
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(30)
 pstats.Stats(pr).sort_stats("cumtime").print_stats(30)

@@ -60,5 +60,13 @@ if gaps:
     n = len(gaps)
     print(f"gaps: n={n} median {gaps[n//2]:.1f} us, p90 {gaps[int(n*0.9)]:.1f} us, "
           f"sum {sum(gaps)/1e3:.2f} ms, sum>20us {sum(g for g in gaps if g > 20)/1e3:.2f} ms")
+big = []
+prev = None
+for st, en, name in ks:
+    if prev is not None and st - prev[1] > 1000:
+        big.append((st - prev[1], prev[2].split("(")[0][:50], name.split("(")[0][:50]))
+    prev = (st, en, name) if prev is None or en > prev[1] else prev
+for g, a, b in sorted(big, reverse=True)[:12]:
+    print(f"  gap {g/1e3:8.2f} ms after {a} before {b}")
 for name, (c, t) in sorted(per.items(), key=lambda x: -x[1][1])[:15]:
     print(f"  {name:60s} {c:6d} {t/1e3:9.3f} ms  avg {t/c:7.2f} us")
