@@ -63,7 +63,7 @@ typedef struct xmhd_step_record {
   int rhs_nonfinite;   /* an asynchronous RHS / JVP evaluation produced non-finite cells */
   int jvp_calls;       /* RHS evaluations made by the asynchronous JVPs (zero w: none)   */
   int nleja;           /* phi-actions recorded (xmhd_leja_finish_async calls)          */
-  int pad_;
+  int lin_nonfinite;   /* F(u) of the last xmhd_linearize_async had non-finite cells    */
   double err_diff;     /* ||a - b|| of xmhd_diff_norms_async                          */
   double err_ref;      /* ||b||                                                        */
   double lc_norm;      /* ||out|| of the last xmhd_lincomb_async                       */
@@ -166,6 +166,16 @@ int xmhd_power(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, c
  * host synchronisation; XMHD_NONFINITE when F(u) has non-finite cells.
  * Single-domain contexts. */
 int xmhd_linearize(xmhd_ctx* ctx, const double* u, double* fu, double* unorm);
+
+/* The same without a host wait, for a caller that knows ||u|| (the harness:
+ * the previous step's flagged combination already reduced it, bit for bit):
+ * fu = F(u); its non-finite flag is read by xmhd_linearize_check (one sync)
+ * or arrives with the next step record (lin_nonfinite). */
+int xmhd_linearize_async(xmhd_ctx* ctx, const double* u, double* fu);
+int xmhd_linearize_check(xmhd_ctx* ctx, int* nonfinite);
+
+/* max |div B| (mhd.py:235-240) into a device double, no host wait. */
+int xmhd_divb_async(xmhd_ctx* ctx, const double* u, double* out_dev);
 
 /* np.linalg.norm(x) (deterministic device reduction). */
 int xmhd_norm(xmhd_ctx* ctx, const double* x, long long n, double* out);

@@ -37,7 +37,7 @@ class LejaState(ctypes.Structure):
 class StepRecord(ctypes.Structure):
     """xmhd_step_record: the record of one asynchronous step."""
     _fields_ = [("rhs_nonfinite", ctypes.c_int), ("jvp_calls", ctypes.c_int),
-                ("nleja", ctypes.c_int), ("pad_", ctypes.c_int),
+                ("nleja", ctypes.c_int), ("lin_nonfinite", ctypes.c_int),
                 ("err_diff", ctypes.c_double), ("err_ref", ctypes.c_double),
                 ("lc_norm", ctypes.c_double), ("lc_nonfinite", ctypes.c_double),
                 ("leja", LejaState * 32)]
@@ -74,6 +74,9 @@ _SIGS = {
     "xmhd_step_async": (_I, [_P, _I, _P, _P, _D, _L, _D, _PD, _PD, _I, _D, _PD, _P, _P]),
     "xmhd_power": (_I, [_P, _P, _P, _D, _P, _P, _P, _I, _D, _PD, _PI, _PI, _PI]),
     "xmhd_linearize": (_I, [_P, _P, _P, _PD]),
+    "xmhd_linearize_async": (_I, [_P, _P, _P]),
+    "xmhd_linearize_check": (_I, [_P, _PI]),
+    "xmhd_divb_async": (_I, [_P, _P, _P]),
     "xmhd_norm": (_I, [_P, _P, _L, _PD]),
     "xmhd_lincomb": (_I, [_P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD, _PI]),
     "xmhd_divide": (_I, [_P, _P, _P, _D, _L, _PD]),

@@ -586,6 +586,40 @@ int xmhd_linearize(xmhd_ctx* c, const double* u, double* fu, double* unorm) {
   return c->h_int[0] ? XMHD_NONFINITE : XMHD_OK;
 }
 
+// FrozenLinearization without a host wait, ||u|| known to the caller: fu = F(u)
+// with its non-finite flag in a slot of its own (bad[1]), read by
+// xmhd_linearize_check or with the next step record.
+int xmhd_linearize_async(xmhd_ctx* c, const double* u, double* fu) {
+  if (!c || !u || !fu) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "single-domain contexts only");
+  CK(cudaMemsetAsync(c->bad + 1, 0, sizeof(int), c->stream));
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.out = fu;
+  a.bad = c->bad + 1;
+  CK(launch_stencil(MODE_RHS, a, c->grid, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_linearize_check(xmhd_ctx* c, int* nonfinite) {
+  if (!c || !nonfinite) return fail(XMHD_BADARG, "null arg");
+  CK(cudaMemcpyAsync(c->h_int + 1, c->bad + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *nonfinite = c->h_int[1];
+  return XMHD_OK;
+}
+
+// max |div B| of u into a device double (no host wait; harness.py:209-211).
+int xmhd_divb_async(xmhd_ctx* c, const double* u, double* out_dev) {
+  if (!c || !u || !out_dev) return fail(XMHD_BADARG, "null arg");
+  RedBuf rb = redbuf(c);
+  rb.result = out_dev;
+  CK(launch_divb_max(c->g, u, nullptr, rb, c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
 int xmhd_norm(xmhd_ctx* c, const double* x, long long n, double* out) {
   if (!c || !x || !out) return fail(XMHD_BADARG, "null arg");
   CK(launch_norm(x, n, redbuf(c), c->stream));
@@ -888,11 +922,14 @@ int xmhd_async_fetch(xmhd_ctx* c, xmhd_step_record* out) {
   if (!c || !out || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
   CK(cudaMemcpyAsync(&c->arec->jvp_calls, &c->jctl->rhs_calls, sizeof(int),
                      cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->arec->pad_[0], c->bad + 1, sizeof(int), cudaMemcpyDeviceToDevice,
+                     c->stream));
   CK(cudaMemcpyAsync(c->arec_h, c->arec, sizeof(AsyncRec), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const AsyncRec& r = *c->arec_h;
   std::memset(out, 0, sizeof(*out));
   out->rhs_nonfinite = r.bad;
+  out->lin_nonfinite = r.pad_[0];
   out->jvp_calls = r.jvp_calls;
   out->nleja = c->nleja_async;
   out->err_diff = r.err[0];
