@@ -290,3 +290,43 @@ def test_native_step_is_bitwise_the_python_issued_step(which):
     assert sa == sb and ka == kb
     assert (a.rhs_evals, a.phi_iterations, a.checksum) == (b.rhs_evals, b.phi_iterations,
                                                            b.checksum)
+
+
+def test_deferred_linearization_raises_like_the_constructor():
+    """FrozenLinearization with a known ||u|| enqueues F(u) without waiting;
+    a non-finite F(u) raises the reference's RhsBlowupError (same message and
+    cells) from check(), from estimate_alpha and from step()."""
+    xb, st, op = _lin(n=24)
+    u = st.flat().clone()
+    u[5 * 24 * 24 + 7] = float("nan")
+    with pytest.raises(xb.RhsBlowupError) as eager:
+        xb.FrozenLinearization(op, u)
+    for use in ("check", "alpha", "step"):
+        lin = xb.FrozenLinearization(op, u, base_norm=1.0)
+        with pytest.raises(xb.RhsBlowupError) as lazy:
+            if use == "check":
+                lin.check()
+            elif use == "alpha":
+                xb.estimate_alpha(lin, None, rng=np.random.default_rng(0))
+            else:
+                xb.step(xb.Scheme.EXPRB43, op, u, 1e-3, alpha=10.0, tol=1e-4, lin=lin)
+        assert str(lazy.value) == str(eager.value)
+        assert lazy.value.cells == eager.value.cells
+
+
+def test_lazy_divb_and_norm_match_the_eager_run():
+    """The harness's deferred div B log and carried state norm give the run
+    of the eager path (div B read every step, ||u|| reduced by the
+    linearization): same report, same bits."""
+    import paper_2108_13622_b200 as xb
+    from paper_2108_13622_b200 import harness, scenarios as sc
+    setup = sc.kh_setup(32, t_final=0.15)
+    lazy = xb.run(xb.RunConfig(scenario=setup, tol=1e-4))
+    old = harness._Domain.divb_async_ok
+    try:
+        harness._Domain.divb_async_ok = False
+        eager = xb.run(xb.RunConfig(scenario=setup, tol=1e-4))
+    finally:
+        harness._Domain.divb_async_ok = old
+    assert lazy.max_divb == eager.max_divb
+    assert lazy.checksum == eager.checksum and lazy.rhs_evals == eager.rhs_evals
