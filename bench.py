@@ -11,9 +11,9 @@ coefficient cache cleared per step so the host coefficient work is included.
           u and the 4 right-hand vectors are copied H2D and the 4 results D2H.
   roofline : the fused Leja iteration kernel, timed with CUDA events on its
           stream.  Algorithmic bytes per cell per Newton term:
-          320 on one GPU (lookahead interpolant schedule: an odd term reads u,
-          y, F(u) and writes y' = 256 B, the even term reads u, y, F(u), p and
-          writes y', p' = 384 B), 352 on y-strips, 384 with XMHD_PDEFER=0.
+          320 (lookahead interpolant schedule: an odd term reads u, y, F(u)
+          and writes y' = 256 B, the even term reads u, y, F(u), p and writes
+          y', p' = 384 B), 384 with XMHD_PDEFER=0.
   cpu_baseline : the NumPy oracle (the reference's own algorithm, oracle/) on a
           bounded sample of the same workload on this host.
 
@@ -43,9 +43,7 @@ SWEEP = (1.0, 10.0, 100.0, 300.0)
 LEJA_TOL = 1e-10
 # algorithmic bytes per cell per Newton term
 def bytes_per_cell_term(world):
-    if os.environ.get("XMHD_PDEFER", "1") == "0":
-        return 384.0
-    return 320.0 if world == 1 else 352.0
+    return 384.0 if os.environ.get("XMHD_PDEFER", "1") == "0" else 320.0
 
 
 def parse():

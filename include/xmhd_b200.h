@@ -122,9 +122,11 @@ int xmhd_leja_loop_available(xmhd_ctx* ctx);
  * environment selects 1), 1 = the sliding-window iteration kernel in a loop. */
 int xmhd_set_loop_kind(xmhd_ctx* ctx, int kind);
 /* Deferred interpolant stores of the fused Leja kernels (default on; XMHD_PDEFER=0
- * in the environment turns them off): every other Newton term keeps p + c*y in
- * registers for ||p|| and the next term stores both additions, in the
- * reference's order (same bits), so a term streams 352 instead of 384 B/cell. */
+ * in the environment turns them off): an odd Newton term neither reads nor
+ * stores p, the even term after it forms p + c*y (and its norm, resolving the
+ * odd term's residual first) before its own update and stores, in the
+ * reference's order (same bits): 320 instead of 384 B/cell per term.  A call
+ * that converged on the odd term discards the even one (not counted). */
 int xmhd_set_leja_defer(xmhd_ctx* ctx, int on);
 int xmhd_leja_finish_async(xmhd_ctx* ctx, double* p_out);
 int xmhd_lincomb_async(xmhd_ctx* ctx, double* out, long long n, const double* const* v,

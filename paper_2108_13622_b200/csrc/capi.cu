@@ -173,10 +173,11 @@ void fill_state(const LejaCtl& h, xmhd_leja_state* st) {
 
 // One fused Leja term launch: the kernel variant compiled for the term's
 // interpolant mode (single-domain lookahead pairs), else the generic one.
-int launch_term(xmhd_ctx* c, const StencilArgs& a) {
+int launch_term(xmhd_ctx* c, const StencilArgs& a, bool peer = false) {
   const int defer = c->ctl_h->defer;
   const int pm = (defer == 2) ? leja_pmode(c->leja_next_term, 2) : PM_ANY;
-  CK(launch_leja_term(a, c->grid, pm, c->stream));
+  if (peer) CK(launch_leja_peer(a, c->grid, pm, c->stream));
+  else CK(launch_leja_term(a, c->grid, pm, c->stream));
   c->leja_next_term++;
   c->launches++;
   return XMHD_OK;
@@ -212,13 +213,8 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
     for (int k = 0; k < batch; ++k) {
-      if (peer) {
-        CK(launch_leja_peer(a, c->grid, c->stream));
-        c->launches++;
-      } else {
-        int rc = launch_term(c, a);
-        if (rc) return rc;
-      }
+      int rc = launch_term(c, a, peer);
+      if (rc) return rc;
     }
     int rc = sync_ctl(c);
     if (rc) return rc;
@@ -275,7 +271,7 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.epoch = c->p2p_epoch;
   // the generic update stores every term; y-strips keep p (their all-reduce
   // carries two sums); a single domain defers with lookahead
-  h.defer = (!c->leja_defer || generic) ? 0 : (c->g.bcy == BC_HALO ? 1 : 2);
+  h.defer = (!c->leja_defer || generic) ? 0 : 2;   // the generic update stores every term
   c->leja_next_term = 1;
   *c->ctl_h = h;
   // staged from pageable memory at the call: back-to-back asynchronous
@@ -744,13 +740,8 @@ int xmhd_leja_launch(xmhd_ctx* c, int n, int peer) {
   StencilArgs a = leja_args(c);
   if (peer) a.p2p = c->p2p;
   for (int k = 0; k < n; ++k) {
-    if (peer) {
-      CK(launch_leja_peer(a, c->grid, c->stream));
-      c->launches++;
-    } else {
-      int rc = launch_term(c, a);
-      if (rc) return rc;
-    }
+    int rc = launch_term(c, a, peer != 0);
+    if (rc) return rc;
   }
   return XMHD_OK;
 }
@@ -1192,9 +1183,7 @@ int xmhd_leja_strip_iterate(xmhd_ctx* c, double* sums) {
     return fail(XMHD_BADARG, "halo rows (state and direction) not set");
   StencilArgs a = leja_args(c);
   a.ext_sums = sums;
-  CK(launch_stencil(MODE_LEJA, a, c->grid, c->stream));
-  c->launches++;
-  return XMHD_OK;
+  return launch_term(c, a);
 }
 
 int xmhd_leja_strip_finalize(xmhd_ctx* c, const double* sums) {
@@ -1209,6 +1198,10 @@ int xmhd_leja_query(xmhd_ctx* c, xmhd_leja_state* st) {
   int rc = sync_ctl(c);
   if (rc) return rc;
   fill_state(*c->ctl_h, st);
+  if (c->ctl_h->status == LJ_MODE_ERROR)
+    return fail(XMHD_CUDA_ERROR, "Leja kernel variant / interpolant mode mismatch");
+  if (c->ctl_h->status == LJ_RUNNING || c->ctl_h->status == LJ_NEED_COEFFS)
+    c->leja_next_term = c->ctl_h->m;   // terms launched past a stop exited
   return XMHD_OK;
 }
 
@@ -1451,8 +1444,13 @@ int xmhd_leja_p2p_emul_run(xmhd_ctx* const* ctxs, int nranks, xmhd_leja_state* s
   if (nblk > cap) nblk = cap;
   if (nblk < 1) return fail(XMHD_BADARG, "too many emulated ranks for one cooperative launch");
   const StencilArgs a0 = leja_args(ctxs[0]);
+  rc = sync_ctl(ctxs[0]);
+  if (rc) return rc;
   for (;;) {
-    CK(launch_leja_emul(dev, a0, nranks, nblk, ctxs[0]->stream));
+    // one term per launch: its interpolant mode from the (synced) term index
+    const LejaCtl& h0 = *ctxs[0]->ctl_h;
+    const int pm = (h0.defer == 2) ? leja_pmode(h0.m, 2) : PM_ANY;
+    CK(launch_leja_emul(dev, a0, nranks, nblk, pm, ctxs[0]->stream));
     for (int r = 0; r < nranks; ++r) ctxs[r]->launches++;
     for (int r = 0; r < nranks; ++r) {
       rc = sync_ctl(ctxs[r]);

@@ -269,11 +269,11 @@ struct AsyncRec {
 };
 
 // Kernels of the peer-memory strip driver (stencil.cu / vec.cu).
-cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_leja_peer(const StencilArgs& a, int grid, int pmode, cudaStream_t s);
 // Emulation of P ranks on one GPU: ONE cooperative launch over all ranks'
 // blocks (args: device array of P StencilArgs; nblk blocks per rank).
 cudaError_t launch_leja_emul(const StencilArgs* args_dev, const StencilArgs& a0, int nranks,
-                             int nblk, cudaStream_t s);
+                             int nblk, int pmode, cudaStream_t s);
 int leja_emul_max_blocks(int nsm);
 // Start of a peer-memory strip Leja call: exchange of sum(v^2) (ext_sums[0])
 // and leja_init_ctl on the global sum.  Real ranks: one block; emulation: one
@@ -286,18 +286,19 @@ cudaError_t launch_leja_extend(LejaCtl* ctl, int to, cudaStream_t s);
 cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s);
 
 #ifdef __CUDACC__
-// All-reduce of 3 doubles over the ranks through peer memory (one thread).
+// All-reduce of 4 doubles over the ranks through peer memory (one thread).
 // Every rank adds the same P entries in rank order, so all ranks obtain the
 // same bits.  Slot = epoch parity: a rank can only reuse a slot after every
 // rank has consumed it (it must first pass the exchange of epoch+1).
-__device__ __forceinline__ bool p2p_allreduce3(const P2PArgs& x, unsigned long long epoch,
-                                               const double v[3], double out[3]) {
+__device__ __forceinline__ bool p2p_allreduce4(const P2PArgs& x, unsigned long long epoch,
+                                               const double v[4], double out[4]) {
   const int P = x.nranks, me = x.rank, slot = (int)(epoch & 1ull);
   for (int q = 0; q < P; ++q) {
     volatile double* b = x.board[q] + (slot * P2P_MAX + me) * 4;
     b[0] = v[0];
     b[1] = v[1];
     b[2] = v[2];
+    b[3] = v[3];
   }
   __threadfence_system();
   for (int q = 0; q < P; ++q) {
@@ -314,14 +315,9 @@ __device__ __forceinline__ bool p2p_allreduce3(const P2PArgs& x, unsigned long l
   }
   __threadfence_system();
   volatile const double* mb = x.board[me] + slot * P2P_MAX * 4;
-  out[0] = mb[0];
-  out[1] = mb[1];
-  out[2] = mb[2];
-  for (int q = 1; q < P; ++q) {
-    out[0] = __dadd_rn(out[0], mb[q * 4]);
-    out[1] = __dadd_rn(out[1], mb[q * 4 + 1]);
-    out[2] = __dadd_rn(out[2], mb[q * 4 + 2]);
-  }
+  for (int k = 0; k < 4; ++k) out[k] = mb[k];
+  for (int q = 1; q < P; ++q)
+    for (int k = 0; k < 4; ++k) out[k] = __dadd_rn(out[k], mb[q * 4 + k]);
   return true;
 }
 

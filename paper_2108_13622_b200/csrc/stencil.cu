@@ -625,12 +625,12 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         // y-strips over peer memory: all-reduce the three sums, then every rank
         // runs the identical control update
         LejaCtl* c = a.ctl;
-        const double v[3] = {sy, sp, *((volatile int*)a.bad) ? 1.0 : 0.0};
-        double tot[3];
+        const double v[4] = {sy, sp, sp2, *((volatile int*)a.bad) ? 1.0 : 0.0};
+        double tot[4];
         const unsigned long long ep = c->epoch + 1;
         c->epoch = ep;
-        if (p2p_allreduce3(a.p2p, ep, v, tot))
-          leja_finalize(c, tot[0], tot[1], 0.0, tot[2] > 0.0, !zero_dir, cm);   // defer <= 1
+        if (p2p_allreduce4(a.p2p, ep, v, tot))
+          leja_finalize(c, tot[0], tot[1], tot[2], tot[3] > 0.0, !zero_dir, cm);
         else
           c->status = LJ_PEER_TIMEOUT;
       } else if (a.ext_sums) {
@@ -638,7 +638,8 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         // after the cross-rank allreduce (leja_finalize_kernel)
         a.ext_sums[0] = sy;
         a.ext_sums[1] = sp;
-        a.ext_sums[2] = *((volatile int*)a.bad) ? 1.0 : 0.0;
+        a.ext_sums[2] = sp2;
+        a.ext_sums[3] = *((volatile int*)a.bad) ? 1.0 : 0.0;
       } else {
         const int flag = *((volatile int*)a.bad);
         leja_finalize(a.ctl, sy, sp, sp2, flag, !zero_dir, cm);
@@ -655,18 +656,18 @@ __global__ void __launch_bounds__(SW, SW_MINB) stencil_kernel(const StencilArgs 
 }
 
 // Fused Leja iteration of one y-strip with the peer-memory exchange.
-template <int KX, int KY>
+template <int KX, int KY, int PM = PM_ANY>
 __global__ void __launch_bounds__(SW, SW_MINB) leja_peer_kernel(const StencilArgs a) {
-  stencil_body<MODE_LEJA, KX, KY, XR_PEER>(a, blockIdx.x, gridDim.x);
+  stencil_body<MODE_LEJA, KX, KY, XR_PEER, PM>(a, blockIdx.x, gridDim.x);
 }
 
 // P ranks in one cooperative launch on one GPU (tests): blocks
 // [r*nblk, (r+1)*nblk) run rank r with args[r]; the ranks' last blocks meet
 // in p2p_allreduce3, which the cooperative launch makes safe (co-resident).
-template <int KX, int KY>
+template <int KX, int KY, int PM = PM_ANY>
 __global__ void __launch_bounds__(SW, SW_MINB) leja_emul_kernel(const StencilArgs* args, int nblk) {
   const int rank = blockIdx.x / nblk;
-  stencil_body<MODE_LEJA, KX, KY, XR_EMUL>(args[rank], blockIdx.x - rank * nblk, nblk);
+  stencil_body<MODE_LEJA, KX, KY, XR_EMUL, PM>(args[rank], blockIdx.x - rank * nblk, nblk);
 }
 
 // The whole Leja loop of one single-domain phi-action in ONE cooperative
@@ -786,23 +787,24 @@ cudaError_t smem_attr_once(K kernel, bool& done) {
   return err;
 }
 
-template <int KX, int KY>
+template <int KX, int KY, int PM>
 cudaError_t launch_peer_one(const StencilArgs& a, int grid, cudaStream_t s) {
   static bool done = false;
-  cudaError_t err = smem_attr_once(leja_peer_kernel<KX, KY>, done);
+  cudaError_t err = smem_attr_once(leja_peer_kernel<KX, KY, PM>, done);
   if (err != cudaSuccess) return err;
-  leja_peer_kernel<KX, KY><<<grid, SW, stencil_smem_bytes(), s>>>(a);
+  leja_peer_kernel<KX, KY, PM><<<grid, SW, stencil_smem_bytes(), s>>>(a);
   return cudaGetLastError();
 }
 
-template <int KX, int KY>
+template <int KX, int KY, int PM>
 cudaError_t launch_emul_one(const StencilArgs* args_dev, int nranks, int nblk, cudaStream_t s) {
   static bool done = false;
-  cudaError_t err = smem_attr_once(leja_emul_kernel<KX, KY>, done);
+  cudaError_t err = smem_attr_once(leja_emul_kernel<KX, KY, PM>, done);
   if (err != cudaSuccess) return err;
   void* kargs[] = {(void*)&args_dev, (void*)&nblk};
-  return cudaLaunchCooperativeKernel((const void*)leja_emul_kernel<KX, KY>, dim3(nranks * nblk),
-                                     dim3(SW), kargs, stencil_smem_bytes(), s);
+  return cudaLaunchCooperativeKernel((const void*)leja_emul_kernel<KX, KY, PM>,
+                                     dim3(nranks * nblk), dim3(SW), kargs, stencil_smem_bytes(),
+                                     s);
 }
 
 template <int KX, int KY>
@@ -836,16 +838,26 @@ int leja_loop_max_blocks(int nsm) {
   return n * nsm;
 }
 
-cudaError_t launch_leja_peer(const StencilArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_leja_peer(const StencilArgs& a, int grid, int pmode, cudaStream_t s) {
   return with_div_kinds(a.g, [&](auto X, auto Y) {
-    return launch_peer_one<decltype(X)::value, decltype(Y)::value>(a, grid, s);
+    constexpr int KX = decltype(X)::value, KY = decltype(Y)::value;
+    switch (pmode) {
+      case PM_SKIP: return launch_peer_one<KX, KY, PM_SKIP>(a, grid, s);
+      case PM_LOOK: return launch_peer_one<KX, KY, PM_LOOK>(a, grid, s);
+      default: return launch_peer_one<KX, KY, PM_ANY>(a, grid, s);
+    }
   });
 }
 
 cudaError_t launch_leja_emul(const StencilArgs* args_dev, const StencilArgs& a0, int nranks,
-                             int nblk, cudaStream_t s) {
+                             int nblk, int pmode, cudaStream_t s) {
   return with_div_kinds(a0.g, [&](auto X, auto Y) {
-    return launch_emul_one<decltype(X)::value, decltype(Y)::value>(args_dev, nranks, nblk, s);
+    constexpr int KX = decltype(X)::value, KY = decltype(Y)::value;
+    switch (pmode) {
+      case PM_SKIP: return launch_emul_one<KX, KY, PM_SKIP>(args_dev, nranks, nblk, s);
+      case PM_LOOK: return launch_emul_one<KX, KY, PM_LOOK>(args_dev, nranks, nblk, s);
+      default: return launch_emul_one<KX, KY, PM_ANY>(args_dev, nranks, nblk, s);
+    }
   });
 }
 

@@ -291,7 +291,7 @@ __global__ void leja_init_finalize_kernel(LejaCtl* ctl, const double* sums) {
 __global__ void leja_finalize_kernel(LejaCtl* ctl, const double* sums,
                                      const double* __restrict__ coeffs) {
   if (ctl->status != LJ_RUNNING) return;
-  leja_finalize(ctl, sums[0], sums[1], 0.0, sums[2] > 0.0, !ctl->zero_dir, coeffs[ctl->m]);
+  leja_finalize(ctl, sums[0], sums[1], sums[2], sums[3] > 0.0, !ctl->zero_dir, coeffs[ctl->m]);
 }
 
 // Halo rows of the current Newton basis vector (y-strips): rows 0,1 go to the
@@ -408,11 +408,11 @@ __global__ void leja_p2p_init_kernel(const StencilArgs a0, const StencilArgs* ar
   if (threadIdx.x != 0) return;
   const StencilArgs& a = EMUL ? args[blockIdx.x] : a0;
   LejaCtl* c = a.ctl;
-  const double v[3] = {a.ext_sums[0], 0.0, 0.0};
-  double tot[3];
+  const double v[4] = {a.ext_sums[0], 0.0, 0.0, 0.0};
+  double tot[4];
   const unsigned long long ep = c->epoch + 1;
   c->epoch = ep;
-  if (p2p_allreduce3(a.p2p, ep, v, tot)) leja_init_ctl(c, tot[0]);
+  if (p2p_allreduce4(a.p2p, ep, v, tot)) leja_init_ctl(c, tot[0]);
   else c->status = LJ_PEER_TIMEOUT;
 }
 

@@ -309,7 +309,8 @@ class CudaStripBackend:
         self.lib = _lib.load()
         self.h = mhd.ctx.bind_stream()
         dev = lin.base_state.device
-        self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        # [sum y'^2, sum p'^2, sum pending p^2, non-finite] of this rank
+        self.sums = torch.zeros(4, dtype=torch.float64, device=dev)
 
     def start(self, v, dt, q, theta, tol, xi, coeffs):
         mhd = self.mhd
