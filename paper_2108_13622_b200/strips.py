@@ -19,7 +19,7 @@ synchronisation:
 and synchronises once per batch of terms.  That is the NCCL transport.  On one
 NVLink / NVSwitch node the default is the peer-memory transport instead: the
 fused kernel itself stores its boundary rows of y' into the neighbours'
-ghost-row buffers (CUDA IPC mappings) and all-reduces the three sums through
+ghost-row buffers (CUDA IPC mappings) and all-reduces the four term sums through
 per-rank boards in peer memory, so a Newton term is ONE kernel launch per rank
 with no host call and no collective (``XMHD_STRIP_TRANSPORT=nccl`` selects the
 NCCL path).  u's halo rows are exchanged once per phi-call (u is frozen).  Every other norm of the host layer (FD step, error
