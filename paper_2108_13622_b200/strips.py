@@ -13,7 +13,7 @@ synchronisation:
     pack the boundary rows of the current y          (device kernel)
     2-row halo exchange with both y-neighbours        (torch.distributed P2P: NCCL/NVLink)
     fused FD-JVP + Newton term on the strip           (stencil kernel, BC_HALO rows)
-    allreduce of [sum y'^2, sum p'^2, non-finite]     (one 24-byte NCCL allreduce)
+    allreduce of [sum y'^2, sum p'^2, sum pending p^2, non-finite] (one 32-byte NCCL allreduce)
     control update from the global sums               (1-thread kernel, identical on all ranks)
 
 and synchronises once per batch of terms.  That is the NCCL transport.  On one
