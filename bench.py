@@ -151,11 +151,15 @@ def dist_setup():
 
 
 def cpu_sample(n, iters=3, adt=10.0):
-    """The NumPy oracle (reference algorithm) on `iters` Leja iterations of the workload."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    """The NumPy oracle (reference algorithm) on `iters` Leja iterations of the workload.
+
+    Threading as the reference gets it: NumPy's elementwise ufuncs (nearly all
+    of the work) run on one core; OpenBLAS's ddot (the norms) may use every
+    core of the host (not limited here)."""
+    threads = os.cpu_count() or 1
     try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(1)
+        from threadpoolctl import threadpool_info
+        threads = max([threads] + [int(i.get("num_threads", 1)) for i in threadpool_info()])
     except Exception:
         pass
     from oracle import leja_np as olj, mhd_np
@@ -183,11 +187,12 @@ def cpu_sample(n, iters=3, adt=10.0):
         p = p + c[m] * y
         _ = abs(c[m]) * ny / max(1.0, np.linalg.norm(p))
     wall = time.perf_counter() - t0
-    return {"value": iters * n * n / wall, "unit": "cell-updates/s", "cores": 1,
+    return {"value": iters * n * n / wall, "unit": "cell-updates/s", "cores": threads,
             "kind": "port",
             "sample": f"{iters} Leja iterations (FD-JVP + Newton update + 2 norms) of the "
-                      f"config-1 phi_1 call at {n}^2, alpha*dt={adt:g}, NumPy oracle, "
-                      f"OPENBLAS_NUM_THREADS=1, {wall:.1f} s"}
+                      f"config-1 phi_1 call at {n}^2, alpha*dt={adt:g}, NumPy oracle (the "
+                      f"reference's algorithm and ufunc sequence): ufuncs on 1 core, BLAS "
+                      f"norms on up to {threads} threads, {wall:.1f} s"}
 
 
 def workload_name(n):
@@ -205,6 +210,7 @@ def reference_arm(args, rank):
         if k >= args.warmup:
             samples.append(r["value"])
     value = float(np.mean(samples))
+    cores = r["cores"]
     wall = time.perf_counter() - t0
     line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": args.gpus,
             "steps": iters, "warmup": args.warmup, "ms_per_step": 1e3 * args.n ** 2 / value,
@@ -212,14 +218,16 @@ def reference_arm(args, rank):
             "data": "synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes "
                     "per field; v seeded unit Gaussian)", "impl": "reference",
             "config": {"workload": workload_name(args.n), "grid": args.n,
-                       "parallelism": "cpu (reference NumPy path, one host thread)",
+                       "parallelism": "cpu (reference NumPy path: ufuncs on one core, BLAS "
+                                      "norms multi-threaded)",
                        "sample": "each step = 1 Leja term (FD-JVP + Newton update + 2 norms) "
                                  "of the alpha*dt=10 call; the metric is per cell-update, so "
                                  "the sweep's rate is the per-term rate"},
-            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": 1,
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores,
                              "kind": "port",
                              "sample": f"1 Leja iteration per step at {args.n}^2 via the NumPy "
-                                       f"oracle (single-threaded ufuncs), total {wall:.1f} s"},
+                                       f"oracle (ufuncs on one core, BLAS norms on up to "
+                                       f"{cores} threads), total {wall:.1f} s"},
             "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
