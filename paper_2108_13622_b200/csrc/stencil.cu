@@ -34,6 +34,7 @@
 // per-cell density share one correctly rounded reciprocal (__drcp_rn) and are
 // completed by the two-correction Markstein sequence (exact for any divisor).
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <type_traits>
 #include <cooperative_groups.h>
@@ -893,6 +894,9 @@ int leja_emul_max_blocks(int nsm) {
 // reference's control update on its own shared-memory copy of the control
 // block (identical in all blocks), so no second barrier or last-block ticket
 // is needed.  Block 0 mirrors the control block to global memory.
+// Measured and dropped: loading the next tile's phase-1 inputs during phases
+// 2-3 of the current one (512^2: 40.3 us/term at 2 blocks/SM, 45.7 at 3 with
+// spills, vs 38.2 without).
 // Resident tile blocks per SM the register budget targets: 2 (210 registers,
 // the shortest chain when every block holds one tile: 8.8 us/term at 128^2)
 // or 3 (160 registers, more tiles in flight when blocks loop over several
@@ -1252,7 +1256,11 @@ int leja_tile_loop_grid(const Geom& g, int nsm, int* minb) {
   const long long ntiles = (long long)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
   const int n2 = tile_blocks_per_sm<2>();
   int mb = 2, n = n2;
-  if (ntiles > (long long)n2 * nsm) {
+  const char* force = std::getenv("XMHD_TILE_MINB");   // A/B knob: 2 or 3
+  if (force && std::atoi(force) == 3) {
+    const int n3 = tile_blocks_per_sm<3>();
+    if (n3 > 0) { mb = 3; n = n3; }
+  } else if (!force && ntiles > (long long)n2 * nsm) {
     const int n3 = tile_blocks_per_sm<3>();
     if (n3 > n2) { mb = 3; n = n3; }
   }
