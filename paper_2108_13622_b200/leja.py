@@ -152,6 +152,34 @@ def _newton_coeffs(l, q, theta, count):
     return coeffs
 
 
+def newton_coeffs_many(keys, count=64):
+    """_newton_coeffs for a sequence of (l, q, theta) in call order, the cache
+    misses computed concurrently on the coefficient pool (the divided
+    differences release the GIL); the cache sees the same lookups and inserts,
+    in the same order, as one _newton_coeffs call per key."""
+    cache = _cache()
+    futs = {}
+    for key in keys:
+        hit = cache.get(key)
+        if (hit is None or hit.size < count) and key not in futs:
+            spec = _spec.pop(key + (count,), None)
+            futs[key] = spec if spec is not None else _spec_pool.submit(_compute_coeffs, *key,
+                                                                        count)
+    out = []
+    for key in keys:
+        hit = cache.get(key)
+        if hit is not None and hit.size >= count:
+            out.append(hit)
+            continue
+        fut = futs.pop(key, None)
+        coeffs = fut.result() if fut is not None else _compute_coeffs(*key, count)
+        if len(cache) > 64:
+            cache.pop(next(iter(cache)))
+        cache[key] = coeffs
+        out.append(coeffs)
+    return out
+
+
 class JacobianAction:
     """The matvec w -> jvp(lin, w) of a frozen linearization.
 

@@ -122,3 +122,21 @@ def test_compute_without_gpu_fails_loudly():
     st = xb.StateGrid.zeros(4, 4, 0.1, 0.1)
     with pytest.raises(xb.NativeUnavailable):
         xb.mhd_rhs(st, xb.MHDParams(0.0, 0.0, 0.0))
+
+
+def test_newton_coeffs_many_matches_sequential_calls(lib):
+    """The batched coefficient lookup (concurrent misses) leaves the cache and
+    returns the tables exactly as one _newton_coeffs call per key would,
+    including repeated keys and FIFO eviction at 65 entries."""
+    import numpy as np
+    from paper_2108_13622_b200 import leja
+    keys = [(1, -0.5 * a, 0.25 * a) for a in np.linspace(0.3, 9.0, 70)]
+    keys = keys[:3] + [keys[1]] + keys[3:] + [keys[0]]
+    leja._coeff_cache.clear()
+    ref = [leja._newton_coeffs(*k, 64) for k in keys]
+    ref_keys = list(leja._coeff_cache)
+    leja._coeff_cache.clear()
+    got = leja.newton_coeffs_many(keys, 64)
+    assert list(leja._coeff_cache) == ref_keys
+    assert all(np.array_equal(a, b) for a, b in zip(ref, got))
+    leja._coeff_cache.clear()
