@@ -931,11 +931,15 @@ __device__ __forceinline__ RowSrc tile_row(int r, const Geom& g, const double* u
 }  // namespace
 
 template <int KX, int KY, int MINB>
-__global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const StencilArgs a) {
+__global__ void __launch_bounds__(MINB == 1 ? 2 * TNT : TNT, MINB)
+    leja_tile_loop_kernel(const StencilArgs a) {
+  // MINB == 1: 256 threads per tile (grids with at most one tile per SM: the
+  // halo phases take one pass instead of two); else 128 threads, MINB blocks/SM
+  constexpr int NT = (MINB == 1) ? 2 * TNT : TNT;
   extern __shared__ __align__(16) double smem_raw[];
   TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
   __shared__ LejaCtl lc;
-  __shared__ double red[4][TNT / 32];
+  __shared__ double red[4][NT / 32];
   cg::grid_group grid = cg::this_grid();
   const Geom& g = a.g;
   const int t = threadIdx.x;
@@ -975,7 +979,7 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
     if (zero_dir) {
       // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
       const long long n = (long long)NF * g.plane;
-      for (long long i = (long long)bid * TNT + t; i < n; i += (long long)nblk * TNT) {
+      for (long long i = (long long)bid * NT + t; i < n; i += (long long)nblk * NT) {
         const double y = __ldcg(dir + i);
         const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                     __dmul_rn(xim, y));
@@ -997,20 +1001,23 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
         const int X0 = (tile % ntx) * TX, Y0 = (tile / ntx) * TY;
         // output cell of this thread and its epilogue operands (issued first)
         const int oj = t / TX, oi = t - oj * TX;
-        const bool out_ok = (Y0 + oj < g.ny) && (X0 + oi < g.nx);
+        const bool is_out = (NT == TNT) || (t < TNT);
+        const bool out_ok = is_out && (Y0 + oj < g.ny) && (X0 + oi < g.nx);
         const unsigned obase = out_ok ? (unsigned)(Y0 + oj) * (unsigned)g.nx + (unsigned)(X0 + oi) : 0u;
         double efu[NF], ey[NF], ep[NF];
+        if (is_out) {
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-          const unsigned i = obase + (unsigned)f * plane;
-          efu[f] = __ldg(a.fu + i);
-          ey[f] = __ldcg(dir + i);
-          if (pread) ep[f] = __ldcg(pin + i);
+          for (int f = 0; f < NF; ++f) {
+            const unsigned i = obase + (unsigned)f * plane;
+            efu[f] = __ldg(a.fu + i);
+            ey[f] = __ldcg(dir + i);
+            if (pread) ep[f] = __ldcg(pin + i);
+          }
         }
-        // ---- phase 1: primitives and ideal fluxes on the tile + halo (2 cells / thread)
+        // ---- phase 1: primitives and ideal fluxes on the tile + halo
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int e = t + h * TNT;
+        for (int h = 0; h < (NE + NT - 1) / NT; ++h) {
+          const int e = t + h * NT;
           if (e < NE) {
             const int ej = e / EX, ei = e - ej * EX;
             const int j = ej - 2, i = ei - 2;
@@ -1052,8 +1059,8 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
         // ---- phase 2: diffusive fluxes on the level-1 ring (mhd.py:182-221)
         if (g.diffusive) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int e = t + h * TNT;
+          for (int h = 0; h < (NGB + NT - 1) / NT; ++h) {
+            const int e = t + h * NT;
             if (e < NGB) {
               const int bj = e / GBW, bi = e - bj * GBW;
               const int j = bj - 1, i = bi - 1;
@@ -1174,7 +1181,7 @@ __global__ void __launch_bounds__(TNT, MINB) leja_tile_loop_kernel(const Stencil
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           double sk = 0.0;
-          for (int j = 0; j < TNT / 32; ++j) sk += red[k][j];
+          for (int j = 0; j < NT / 32; ++j) sk += red[k][j];
           slot[k] = sk;
         }
       }
@@ -1222,7 +1229,7 @@ cudaError_t launch_tile_loop_one(const StencilArgs& a, int grid, cudaStream_t s)
   }
   void* kargs[] = {(void*)&a};
   return cudaLaunchCooperativeKernel((const void*)leja_tile_loop_kernel<KX, KY, MINB>, dim3(grid),
-                                     dim3(TNT), kargs, tile_smem_bytes(), s);
+                                     dim3(MINB == 1 ? 2 * TNT : TNT), kargs, tile_smem_bytes(), s);
 }
 
 template <int MINB>
@@ -1232,7 +1239,8 @@ int tile_blocks_per_sm() {
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem_bytes()) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &n, leja_tile_loop_kernel<DIV_MUL, DIV_MUL, MINB>, TNT, tile_smem_bytes()) != cudaSuccess) {
+          &n, leja_tile_loop_kernel<DIV_MUL, DIV_MUL, MINB>, MINB == 1 ? 2 * TNT : TNT,
+          tile_smem_bytes()) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1241,11 +1249,13 @@ int tile_blocks_per_sm() {
 
 }  // namespace
 
-// minb: 2 or 3 (leja_tile_loop_grid's choice).
+// minb: 1 (256 threads per tile), 2 or 3 (128 threads; leja_tile_loop_grid's choice).
 cudaError_t launch_leja_tile_loop(const StencilArgs& a, int grid, int minb, cudaStream_t s) {
   return with_div_kinds(a.g, [&](auto X, auto Y) {
-    return minb == 3 ? launch_tile_loop_one<decltype(X)::value, decltype(Y)::value, 3>(a, grid, s)
-                     : launch_tile_loop_one<decltype(X)::value, decltype(Y)::value, 2>(a, grid, s);
+    constexpr int KX = decltype(X)::value, KY = decltype(Y)::value;
+    if (minb == 1) return launch_tile_loop_one<KX, KY, 1>(a, grid, s);
+    if (minb == 3) return launch_tile_loop_one<KX, KY, 3>(a, grid, s);
+    return launch_tile_loop_one<KX, KY, 2>(a, grid, s);
   });
 }
 
@@ -1256,11 +1266,16 @@ int leja_tile_loop_grid(const Geom& g, int nsm, int* minb) {
   const long long ntiles = (long long)((g.nx + TX - 1) / TX) * ((g.ny + TY - 1) / TY);
   const int n2 = tile_blocks_per_sm<2>();
   int mb = 2, n = n2;
-  const char* force = std::getenv("XMHD_TILE_MINB");   // A/B knob: 2 or 3
-  if (force && std::atoi(force) == 3) {
+  const char* force = std::getenv("XMHD_TILE_MINB");   // A/B knob: 1, 2 or 3
+  const int fmb = force ? std::atoi(force) : 0;
+  const int n1 = (fmb == 0 || fmb == 1) ? tile_blocks_per_sm<1>() : 0;
+  if (fmb == 3) {
     const int n3 = tile_blocks_per_sm<3>();
     if (n3 > 0) { mb = 3; n = n3; }
-  } else if (!force && ntiles > (long long)n2 * nsm) {
+  } else if ((fmb == 1 || (fmb == 0 && ntiles <= (long long)nsm)) && n1 > 0) {
+    mb = 1;   // every tile on its own SM: 256 threads per tile
+    n = n1;
+  } else if (fmb == 0 && ntiles > (long long)n2 * nsm) {
     const int n3 = tile_blocks_per_sm<3>();
     if (n3 > n2) { mb = 3; n = n3; }
   }
