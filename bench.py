@@ -187,8 +187,14 @@ def cpu_sample(n, iters=3, adt=10.0):
         p = p + c[m] * y
         _ = abs(c[m]) * ny / max(1.0, np.linalg.norm(p))
     wall = time.perf_counter() - t0
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((l.split(":", 1)[1].strip() for l in fh if l.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": iters * n * n / wall, "unit": "cell-updates/s", "cores": threads,
-            "kind": "port",
+            "kind": "port", "cpu_model": model, "host_cpus": os.cpu_count(),
             "sample": f"{iters} Leja iterations (FD-JVP + Newton update + 2 norms) of the "
                       f"config-1 phi_1 call at {n}^2, alpha*dt={adt:g}, NumPy oracle (the "
                       f"reference's algorithm and ufunc sequence): ufuncs on 1 core, BLAS "
@@ -378,7 +384,7 @@ def main():
 
     exprb = None
     if not args.no_exprb and rank == 0 and world == 1:
-        exprb = exprb_step_time(xb)
+        exprb = exprb_step_time(xb, with_cpu=not args.no_cpu_baseline)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -443,7 +449,7 @@ def time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha, n_iter=48):
     return float(out.value)
 
 
-def exprb_step_time(xb):
+def exprb_step_time(xb, with_cpu=False):
     """Config 0 (KH 128^2, EXPRB43, tol 1e-4, t_end 0.5): wall-s per accepted step."""
     from paper_2108_13622_b200 import leja, scenarios as sc
     import torch
@@ -455,9 +461,27 @@ def exprb_step_time(xb):
     rep = xb.run(xb.RunConfig(scenario=setup, scheme=xb.Scheme.EXPRB43, tol=setup.tol))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return {"config": "config0 KH 128^2 EXPRB43 tol 1e-4 t_end 0.5",
-            "accepted": rep.accepted, "rejected": rep.rejected, "rhs_evals": rep.rhs_evals,
-            "wall_s": wall, "wall_s_per_step": wall / max(rep.accepted, 1)}
+    out = {"config": "config0 KH 128^2 EXPRB43 tol 1e-4 t_end 0.5",
+           "accepted": rep.accepted, "rejected": rep.rejected, "rhs_evals": rep.rhs_evals,
+           "wall_s": wall, "wall_s_per_step": wall / max(rep.accepted, 1)}
+    if with_cpu:
+        out["cpu_baseline"] = exprb_cpu_time(setup)
+    return out
+
+
+def exprb_cpu_time(setup):
+    """The same adaptive run through the NumPy oracle (the reference's algorithm
+    and ufunc sequence) on this host: wall-s per accepted step, beside ours."""
+    from oracle import steppers_np as ost
+    from paper_2108_13622_b200 import scenarios as sc
+    q = sc.initial_fields(setup)
+    t0 = time.perf_counter()
+    rep = ost.run(q, setup.dx, setup.dy, setup.mu, setup.eta, setup.kappa, "exprb43", setup.tol,
+                  setup.t_final)
+    wall = time.perf_counter() - t0
+    return {"kind": "port", "accepted": rep.accepted, "rhs_evals": rep.rhs_evals,
+            "wall_s": wall, "wall_s_per_step": wall / max(rep.accepted, 1),
+            "sample": "the whole config-0 run (same step sequence) through the NumPy oracle"}
 
 
 if __name__ == "__main__":
