@@ -80,6 +80,13 @@ struct Geom {
   const double* halo_hi_dir;
 };
 
+// Diffusive terms present (mhd.py:181)?  Only the generic variant
+// (K == DIV_IEEE) is launched for mu = eta = kappa = 0, so the others skip the
+// runtime test.
+template <int K>
+__device__ __forceinline__ bool diff_on(const Geom& g) {
+  return K == DIV_IEEE ? g.diffusive != 0 : true;
+}
 // Compile-time variant of exact_div (the kind is a template parameter).
 template <int K>
 __device__ __forceinline__ double qdiv(double a, const Divisor& v) {
@@ -119,7 +126,12 @@ __device__ __forceinline__ Divisor make_divisor_dev(double d) {
   return v;
 }
 
+// GM = false: the launch was dispatched for mu0 == 1.0 (x/1.0 == x exactly),
+// so no per-call branch on the runtime flag (6 uniform branches and their
+// register moves per cell in the fused kernels); GM = true: any mu0.
+template <bool GM>
 __device__ __forceinline__ double over_mu0(double a, const Geom& g) {
+  if (!GM) return a;
   return g.mu0_one ? a : rdiv(a, g.mu0d);
 }
 
@@ -129,6 +141,7 @@ struct Prim {
   double b2, pres, ptot, bdotv, emf, temp;
 };
 
+template <bool GM>
 __device__ __forceinline__ void primitives(const double x[NF], const Geom& g, Prim& p) {
   p.rho = x[RHO];
   // the four divisions by the density share one correctly rounded reciprocal;
@@ -151,7 +164,7 @@ __device__ __forceinline__ void primitives(const double x[NF], const Geom& g, Pr
                         __dmul_rn(p.vz, p.vz));
   double kin = __dmul_rn(__dmul_rn(0.5, p.rho), vv);
   // 0.5*b2/mu0
-  double hb = over_mu0(__dmul_rn(0.5, p.b2), g);
+  double hb = over_mu0<GM>(__dmul_rn(0.5, p.b2), g);
   // pres = (gamma-1)*(E - kin - 0.5*b2/mu0); ptot = pres + 0.5*b2/mu0
   p.pres = __dmul_rn(g.gm1, __dsub_rn(__dsub_rn(p.en, kin), hb));
   p.ptot = __dadd_rn(p.pres, hb);
@@ -167,29 +180,31 @@ __device__ __forceinline__ void primitives(const double x[NF], const Geom& g, Pr
 // Non-zero ideal x-flux rows, mhd.py:161-175.  Slot order:
 // RHO, MX, MY, MZ, BY, BZ, EN  (flux_x[BX] == 0).
 constexpr int NFX = 7;
+template <bool GM>
 __device__ __forceinline__ void flux_x(const Prim& p, const Geom& g, double f[NFX]) {
   double rv = __dmul_rn(p.rho, p.vx);
   f[0] = rv;
-  f[1] = __dsub_rn(__dadd_rn(__dmul_rn(rv, p.vx), p.ptot), over_mu0(__dmul_rn(p.bx, p.bx), g));
-  f[2] = __dsub_rn(__dmul_rn(rv, p.vy), over_mu0(__dmul_rn(p.bx, p.by), g));
-  f[3] = __dsub_rn(__dmul_rn(rv, p.vz), over_mu0(__dmul_rn(p.bx, p.bz), g));
+  f[1] = __dsub_rn(__dadd_rn(__dmul_rn(rv, p.vx), p.ptot), over_mu0<GM>(__dmul_rn(p.bx, p.bx), g));
+  f[2] = __dsub_rn(__dmul_rn(rv, p.vy), over_mu0<GM>(__dmul_rn(p.bx, p.by), g));
+  f[3] = __dsub_rn(__dmul_rn(rv, p.vz), over_mu0<GM>(__dmul_rn(p.bx, p.bz), g));
   f[4] = -p.emf;
   f[5] = __dsub_rn(__dmul_rn(p.vx, p.bz), __dmul_rn(p.bx, p.vz));
-  f[6] = __dsub_rn(__dmul_rn(__dadd_rn(p.en, p.ptot), p.vx), over_mu0(__dmul_rn(p.bx, p.bdotv), g));
+  f[6] = __dsub_rn(__dmul_rn(__dadd_rn(p.en, p.ptot), p.vx), over_mu0<GM>(__dmul_rn(p.bx, p.bdotv), g));
 }
 
 // Non-zero ideal y-flux rows, mhd.py:162-176.  Slot order:
 // RHO, MX, MY, MZ, BX, BZ, EN  (flux_y[BY] == 0).
 constexpr int NFY = 7;
+template <bool GM>
 __device__ __forceinline__ void flux_y(const Prim& p, const Geom& g, double f[NFY]) {
   double rv = __dmul_rn(p.rho, p.vy);
   f[0] = rv;
-  f[1] = __dsub_rn(__dmul_rn(rv, p.vx), over_mu0(__dmul_rn(p.by, p.bx), g));
-  f[2] = __dsub_rn(__dadd_rn(__dmul_rn(rv, p.vy), p.ptot), over_mu0(__dmul_rn(p.by, p.by), g));
-  f[3] = __dsub_rn(__dmul_rn(rv, p.vz), over_mu0(__dmul_rn(p.by, p.bz), g));
+  f[1] = __dsub_rn(__dmul_rn(rv, p.vx), over_mu0<GM>(__dmul_rn(p.by, p.bx), g));
+  f[2] = __dsub_rn(__dadd_rn(__dmul_rn(rv, p.vy), p.ptot), over_mu0<GM>(__dmul_rn(p.by, p.by), g));
+  f[3] = __dsub_rn(__dmul_rn(rv, p.vz), over_mu0<GM>(__dmul_rn(p.by, p.bz), g));
   f[4] = p.emf;
   f[5] = __dsub_rn(__dmul_rn(p.vy, p.bz), __dmul_rn(p.by, p.vz));
-  f[6] = __dsub_rn(__dmul_rn(__dadd_rn(p.en, p.ptot), p.vy), over_mu0(__dmul_rn(p.by, p.bdotv), g));
+  f[6] = __dsub_rn(__dmul_rn(__dadd_rn(p.en, p.ptot), p.vy), over_mu0<GM>(__dmul_rn(p.by, p.bdotv), g));
 }
 
 // Quantities of a cell that neighbours differentiate (mhd.py:182-201).

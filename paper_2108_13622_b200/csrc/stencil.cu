@@ -445,7 +445,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
             }
           }
           Prim p;
-          primitives(x, g, p);
+          primitives<KX == DIV_IEEE>(x, g, p);
           pn[PD_VX] = p.vx;
           pn[PD_VY] = p.vy;
           pn[PD_VZ] = p.vz;
@@ -457,10 +457,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
           double fv[NFX];
 #pragma unroll
           for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
-          flux_x(p, g, fv);
+          flux_x<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
-          flux_y(p, g, fv);
+          flux_y<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
         }
@@ -470,7 +470,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         double gyn[NG];
 #pragma unroll
         for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
-        if (g.diffusive && s >= 2) {
+        if (diff_on<KX>(g) && s >= 2) {
           double xl[NPD], xr[NPD];   // PD of row r-1 at t-1, t+1
 #pragma unroll
           for (int k = 0; k < NPD; ++k) {
@@ -514,7 +514,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
             }
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
-          if (g.diffusive) {
+          if (diff_on<KX>(g)) {
             // out += dGX/2dx; out += dGY/2dy                 (mhd.py:222-223)
             double gr[NG], gl[NG];
 #pragma unroll
@@ -762,7 +762,10 @@ cudaError_t with_div_kinds(const Geom& g, F&& f) {
   using K2 = std::integral_constant<int, DIV_MK2>;
   using IE = std::integral_constant<int, DIV_IEEE>;
   const int kx = g.h2x.kind, ky = g.h2y.kind;
-  if (kx == DIV_IEEE || ky == DIV_IEEE) return f(IE{}, IE{});
+  // the generic variant (correctly rounded divisions, any mu0, diffusive or
+  // not) serves every geometry; the others are compiled for mu0 == 1.0 and a
+  // diffusive operator (common.cuh over_mu0, diff_on)
+  if (kx == DIV_IEEE || ky == DIV_IEEE || !g.mu0_one || !g.diffusive) return f(IE{}, IE{});
   if (kx == DIV_MUL && ky == DIV_MUL) return f(M{}, M{});
   // a power-of-two divisor is also exact on the one-correction path
   const int x2 = (kx == DIV_MK2), y2 = (ky == DIV_MK2);
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 2 * TNT : TNT, MINB)
             if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
             if (rs.flip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
             Prim p;
-            primitives(x, g, p);
+            primitives<KX == DIV_IEEE>(x, g, p);
             S.pd[PD_VX][e] = p.vx;
             S.pd[PD_VY][e] = p.vy;
             S.pd[PD_VZ][e] = p.vz;
@@ -1044,12 +1047,12 @@ __global__ void __launch_bounds__(MINB == 1 ? 2 * TNT : TNT, MINB)
             S.pd[PD_B2][e] = p.b2;
             double fv[NFX];
             if (j >= 0 && j < TY && i >= -1 && i <= TX) {
-              flux_x(p, g, fv);
+              flux_x<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
               for (int k = 0; k < NFX; ++k) S.fx[k][j * FXW + i + 1] = fv[k];
             }
             if (j >= -1 && j <= TY && i >= 0 && i < TX) {
-              flux_y(p, g, fv);
+              flux_y<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
               for (int k = 0; k < NFY; ++k) S.fy[k][(j + 1) * TX + i] = fv[k];
             }
@@ -1057,7 +1060,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 2 * TNT : TNT, MINB)
         }
         __syncthreads();
         // ---- phase 2: diffusive fluxes on the level-1 ring (mhd.py:182-221)
-        if (g.diffusive) {
+        if (diff_on<KX>(g)) {
 #pragma unroll
           for (int h = 0; h < (NGB + NT - 1) / NT; ++h) {
             const int e = t + h * NT;
@@ -1106,7 +1109,7 @@ __global__ void __launch_bounds__(MINB == 1 ? 2 * TNT : TNT, MINB)
             F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(S.fy[k][cy + TX], S.fy[k][cy - TX]), g.h2y));
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
-          if (g.diffusive) {
+          if (diff_on<KX>(g)) {
             double gr[NG], gl[NG], gu[NG], gd[NG];
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
