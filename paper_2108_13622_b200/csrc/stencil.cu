@@ -48,6 +48,9 @@ namespace cg = cooperative_groups;
 // epilogue 2 ahead 0.329; bulk cp.async.bulk.prefetch instead of per-line
 // prefetches 0.339).
 #ifndef XB_L2PF
+#ifndef XB_EPI_K1
+#define XB_EPI_K1 0   // measured: 0.284 vs 0.280 ms at 2048^2 (four epilogue copies; i-cache)
+#endif
 #define XB_L2PF 2   // row steps of the state / direction prefetch (0: no prefetch)
 #endif
 #ifndef XB_L2PF_E
@@ -75,7 +78,15 @@ namespace {
 __host__ __device__ constexpr int fx_field(int k) { return k < 4 ? k : k + 1; }   // skip BX
 __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; }   // skip BY
 
-constexpr int RING_PD = 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
+// One barrier per row step (XB_ONEBAR): with a 3-slot PD ring, P1 of step s+1
+// writes a PD slot no P2 of step s reads, so the barrier between P2 and the
+// next P1 goes; every other ring hazard is still separated by the barrier
+// after P1 (FX: P3(s) reads slot s-2 while P1(s+1) writes s+1; GX: P2(s)
+// writes s+1 while P3(s) reads s; FY is read by its own column only).
+#ifndef XB_ONEBAR
+#define XB_ONEBAR 0   // measured: 0.282 vs 0.281 ms (2048^2), 1.088 vs 1.080 (4096^2): the larger carve-out costs more than the barrier
+#endif
+constexpr int RING_PD = XB_ONEBAR ? 3 : 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
 
 // Source of one ghost-extended row.  Element offsets are 32-bit unsigned: a
 // per-GPU vector of 8*nx*ny < 2^32 doubles (34 GB) covers every grid that fits
@@ -329,7 +340,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       double gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
-      int s3 = 0;  // s % 3 (GY ring)
+      int s3 = 0;  // s % 3 (PD ring)
       // own-column differentiated primitives of rows r-1 and r-2 (registers);
       // shared memory holds only the row x-neighbours read (PD of row r-1)
       double pr1[NPD], pr2[NPD];
@@ -456,7 +467,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
           pn[PD_B2] = p.b2;
           double fv[NFX];
 #pragma unroll
-          for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
+          for (int k = 0; k < NPD; ++k) pd[XB_ONEBAR ? s3 : (s & 1)][k][t] = pn[k];
           flux_x<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
           for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
@@ -472,10 +483,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
         if (diff_on<KX>(g) && s >= 2) {
           double xl[NPD], xr[NPD];   // PD of row r-1 at t-1, t+1
+          const int sp = XB_ONEBAR ? (s3 == 0 ? 2 : s3 - 1) : ((s + 1) & 1);   // row r-1
 #pragma unroll
           for (int k = 0; k < NPD; ++k) {
-            xl[k] = pd[(s + 1) & 1][k][tl];
-            xr[k] = pd[(s + 1) & 1][k][tr];
+            xl[k] = pd[sp][k][tl];
+            xr[k] = pd[sp][k][tr];
           }
           double gxv[NG];
           diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyn);
@@ -484,7 +496,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         }
 #pragma unroll
         for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
-        __syncthreads();
+        if (!XB_ONEBAR) __syncthreads();
 
         // ---- P3: output row o = r-2
         if (out_row) {
@@ -545,40 +557,55 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
               ex = max(ex, (unsigned)__double2hiint(F[f]) & 0x7ff00000u);
             bad |= (ex == 0x7ff00000u);
           }
+          // The epilogue's two divisions (by eps, by theta) take the
+          // one-correction path when the divisor's class proves it exact
+          // (XB_EPI_K1: one uniform branch per row step into one of four copies).
+          auto epilogue = [&](auto KEc, auto KTc) {
+            constexpr int KE = decltype(KEc)::value, KT = decltype(KTc)::value;
 #pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const unsigned i = obase + (unsigned)f * plane;
-            if (MODE == MODE_RHS) {
-              a.out[i] = F[f];
-            } else if (MODE == MODE_JVP) {
-              const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
-              a.out[i] = jv;
-              acc0 = __fma_rn(jv, jv, acc0);
-            } else {
-              // per-launch divisors (eps, theta): the general two-correction path,
-              // branch-free (exact for every divisor)
-              const double w = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
-              const double y = ey[f];
-              const double yn = __dsub_rn(
-                  qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
-                  __dmul_rn(xim, y));
-              yout[i] = yn;
-              double pn = 0.0;
-              if (pread) {
-                double pb = ep[f];
-                if (padd) {   // the pending term first
-                  pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
-                  if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+            for (int f = 0; f < NF; ++f) {
+              const unsigned i = obase + (unsigned)f * plane;
+              if (MODE == MODE_RHS) {
+                a.out[i] = F[f];
+              } else if (MODE == MODE_JVP) {
+                const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
+                a.out[i] = jv;
+                acc0 = __fma_rn(jv, jv, acc0);
+              } else {
+                // per-launch divisors (eps, theta): exact on either path
+                const double w = qdiv<KE>(__dsub_rn(F[f], efu[f]), epsd);
+                const double y = ey[f];
+                const double yn = __dsub_rn(
+                    qdiv<KT>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
+                    __dmul_rn(xim, y));
+                yout[i] = yn;
+                double pn = 0.0;
+                if (pread) {
+                  double pb = ep[f];
+                  if (padd) {   // the pending term first
+                    pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+                    if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+                  }
+                  pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+                  if (pstore) pout[i] = pn;
                 }
-                pn = __dadd_rn(pb, __dmul_rn(cm, yn));
-                if (pstore) pout[i] = pn;
+                if (P2P)
+                  push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
+                             g.nx, c_out, yn);
+                acc0 = __fma_rn(yn, yn, acc0);
+                acc1 = __fma_rn(pn, pn, acc1);
               }
-              if (P2P)
-                push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, r - 2, g.ny,
-                           g.nx, c_out, yn);
-              acc0 = __fma_rn(yn, yn, acc0);
-              acc1 = __fma_rn(pn, pn, acc1);
             }
+          };
+          using MK1c = std::integral_constant<int, DIV_MK1>;
+          using MK2c = std::integral_constant<int, DIV_MK2>;
+          if (XB_EPI_K1 && MODE == MODE_LEJA && epsd.kind == DIV_MK1) {
+            if (thd.kind == DIV_MK1) epilogue(MK1c{}, MK1c{});
+            else epilogue(MK1c{}, MK2c{});
+          } else if (XB_EPI_K1 && MODE == MODE_LEJA && thd.kind == DIV_MK1) {
+            epilogue(MK2c{}, MK1c{});
+          } else {
+            epilogue(MK2c{}, MK2c{});
           }
         }
 
