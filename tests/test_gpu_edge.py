@@ -312,3 +312,17 @@ def test_device_power_nonfinite_rhs_raises_like_reference():
     assert str(err.value) == str(ref_err.value)
     assert err.value.cells == ref_err.value.cells
     assert op.calls == calls + 1
+
+
+def test_prefetched_start_vector_uploaded_and_identical():
+    """On a GPU the prefetched start vector is drawn in chunks and uploaded as
+    it goes (device-resident when the first estimate needs it); values and the
+    continuation of the run RNG's stream are still exactly the reference's."""
+    from paper_2108_13622_b200 import harness
+    for n in (1_000_003, 2 * harness._PrefetchedNormals._CHUNK + 5):
+        pre = harness._PrefetchedNormals(5, n)
+        ref = np.random.default_rng(5)
+        w = pre.standard_normal(n)
+        assert torch.is_tensor(w) and w.is_cuda and w.numel() == n
+        assert np.array_equal(w.cpu().numpy(), ref.standard_normal(n))
+        assert np.array_equal(pre.standard_normal(9), ref.standard_normal(9))

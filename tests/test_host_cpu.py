@@ -140,3 +140,16 @@ def test_newton_coeffs_many_matches_sequential_calls(lib):
     assert list(leja._coeff_cache) == ref_keys
     assert all(np.array_equal(a, b) for a, b in zip(ref, got))
     leja._coeff_cache.clear()
+
+
+def test_prefetched_start_vector_is_the_run_rng_stream():
+    """The run RNG's first standard_normal(n) is drawn ahead on a host thread
+    (into page-locked memory when CUDA is up); values and the continuation of
+    the stream equal the reference's plain draws (harness.py:130,
+    linearize.py:113)."""
+    from paper_2108_13622_b200 import harness
+    n = 100_003
+    pre = harness._PrefetchedNormals(11, n)
+    ref = np.random.default_rng(11)
+    assert np.array_equal(pre.standard_normal(n), ref.standard_normal(n))
+    assert np.array_equal(pre.standard_normal(7), ref.standard_normal(7))
