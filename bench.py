@@ -14,6 +14,8 @@ coefficient cache cleared per step so the host coefficient work is included.
           320 (lookahead interpolant schedule: an odd term reads u, y, F(u)
           and writes y' = 256 B, the even term reads u, y, F(u), p and writes
           y', p' = 384 B), 384 with XMHD_PDEFER=0.
+  stencil_kernels : the RHS (128 B/cell) and FD-JVP (256 B/cell) stencil
+          kernels of the metric's "RHS/Jv", timed the same way (N=1 only).
   cpu_baseline : the NumPy oracle (the reference's own algorithm, oracle/) on a
           bounded sample of the same workload on this host.
 
@@ -340,6 +342,8 @@ def main():
 
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
     kern_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
+    # single domain only: in y-strip mode the stencil needs exchanged ghost rows
+    stencil_ms = time_stencil_modes(_lib, lin, mhd, v_dev) if world == 1 else {}
     local_cells = u_dev.numel() // 8
     bpc = bytes_per_cell_term(world)
     achieved = bpc * local_cells / (kern_ms * 1e-3) / 1e9
@@ -413,6 +417,14 @@ def main():
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
                          "kernel_ms": kern_ms, "bytes_per_cell": bpc,
                          "traffic": ncu_traffic(args.n, local_cells)},
+            # the other two stencil kernels of the metric's "RHS/Jv", timed the same
+            # way (not in the timed step: the phi sweep runs only the fused term)
+            "stencil_kernels": {
+                k: {"kernel_ms": t, "bytes_per_cell": b,
+                    "achieved_gbs": b * local_cells / (t * 1e-3) / 1e9,
+                    "frac": b * local_cells / (t * 1e-3) / 1e9 / peak,
+                    "cell_updates_per_s": local_cells / (t * 1e-3)}
+                for k, (t, b) in stencil_ms.items()},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -424,6 +436,26 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_stencil_modes(_lib, lin, mhd, v_dev, n_iter=40):
+    """Average duration (CUDA events on the context stream) of the RHS stencil
+    (F(u), 128 B/cell: read u, write F) and of the FD-JVP stencil (256 B/cell:
+    read u, w, F(u), write Jw), each launched back to back (xmhd_time_stencil)."""
+    import ctypes
+    import torch
+    lib = _lib.load()
+    out = torch.empty_like(v_dev)
+    res = {}
+    for name, mode, b in (("rhs", 0, 128.0), ("jvp", 1, 256.0)):
+        ms = ctypes.c_double()
+        rc = lib.xmhd_time_stencil(mhd.ctx.bind_stream(), mode, _lib.ptr(lin.base_state),
+                                   _lib.ptr(lin.base_rhs), float(lin._base_norm),
+                                   _lib.ptr(v_dev), _lib.ptr(out), int(n_iter), ctypes.byref(ms))
+        _lib.check(rc, "xmhd_time_stencil")
+        res[name] = (float(ms.value), b)
+    torch.cuda.synchronize()
+    return res
 
 
 def time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha, n_iter=48):

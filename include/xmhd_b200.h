@@ -270,6 +270,13 @@ int xmhd_leja_query(xmhd_ctx* ctx, xmhd_leja_state* st);
 int xmhd_leja_set_coeffs(xmhd_ctx* ctx, const double* coeffs, int ncoef);
 
 /* Benchmark hook: average duration (CUDA events on the context stream) of
+ * n_iter back-to-back stencil launches, mode 0 = F(u) into out (as xmhd_rhs),
+ * mode 1 = the FD Jacobian-vector product of w into out (as xmhd_jvp; fu, unorm
+ * and w required).  Returns XMHD_NONFINITE like those calls. */
+int xmhd_time_stencil(xmhd_ctx* ctx, int mode, const double* u, const double* fu, double unorm,
+                      const double* w, double* out, int n_iter, double* ms_per_launch);
+
+/* Benchmark hook: average duration (CUDA events on the context stream) of
  * n_iter back-to-back fused Leja iteration kernels with the convergence test
  * disabled (tol = 0); coeffs500 holds 500 Newton coefficients. */
 int xmhd_time_leja_iterations(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,

@@ -996,6 +996,51 @@ int xmhd_leja_generic_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_
   return XMHD_OK;
 }
 
+int xmhd_time_stencil(xmhd_ctx* c, int mode, const double* u, const double* fu, double unorm,
+                      const double* w, double* out, int n_iter, double* ms_per_launch) {
+  if (!c || !u || !out || !ms_per_launch) return fail(XMHD_BADARG, "null arg");
+  if (mode != MODE_RHS && mode != MODE_JVP) return fail(XMHD_BADARG, "mode must be 0 (RHS) or 1 (JVP)");
+  if (mode == MODE_JVP && (!fu || !w)) return fail(XMHD_BADARG, "null arg");
+  if (n_iter < 1 || n_iter > 400) return fail(XMHD_BADARG, "n_iter must be in [1, 400]");
+  StencilArgs a = base_args(c);
+  a.u = u;
+  a.out = out;
+  if (mode == MODE_JVP) {
+    const long long n = NF * c->g.plane;
+    CK(launch_norm(w, n, redbuf(c), c->stream));
+    c->launches++;
+    int rc = fetch_doubles(c, 1);
+    if (rc) return rc;
+    const double wn = c->h_dbl[0];
+    if (wn == 0.0) return fail(XMHD_BADARG, "zero direction");
+    // the FD step of xmhd_jvp (linearize.py:65)
+    const double eps = (1.4901161193847656e-08 * py_max(1.0, unorm)) / py_max(wn, 1e-300);
+    a.dir = w;
+    a.fu = fu;
+    a.eps = eps;
+    a.epsd = make_divisor(eps, c->force_ieee);
+  }
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(launch_stencil(mode, a, c->grid, c->stream));   // warm-up
+  CK(cudaEventRecord(e0, c->stream));
+  for (int k = 0; k < n_iter; ++k) CK(launch_stencil(mode, a, c->grid, c->stream));
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaEventSynchronize(e1));
+  c->launches += n_iter + 1;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  int bad = 0;
+  int rc = fetch_bad(c, &bad);
+  if (rc) return rc;
+  *ms_per_launch = (double)ms / n_iter;
+  return bad ? XMHD_NONFINITE : XMHD_OK;
+}
+
 int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, double unorm,
                               const double* v, double dt, double q, double theta,
                               const double* xi, const double* coeffs500, int n_iter,
