@@ -319,7 +319,7 @@ def test_prefetched_start_vector_uploaded_and_identical():
     it goes (device-resident when the first estimate needs it); values and the
     continuation of the run RNG's stream are still exactly the reference's."""
     from paper_2108_13622_b200 import harness
-    for n in (1_000_003, 2 * harness._PrefetchedNormals._CHUNK + 5):
+    for n in (1_000_003, 2 * harness._PrefetchedNormals._CHUNK + 5, 9_000_011):
         pre = harness._PrefetchedNormals(5, n)
         ref = np.random.default_rng(5)
         w = pre.standard_normal(n)

@@ -153,3 +153,24 @@ def test_prefetched_start_vector_is_the_run_rng_stream():
     ref = np.random.default_rng(11)
     assert np.array_equal(pre.standard_normal(n), ref.standard_normal(n))
     assert np.array_equal(pre.standard_normal(7), ref.standard_normal(7))
+
+
+@pytest.mark.parametrize("n,piece,rho", [
+    (3_000_017, 1 << 17, None),     # 23 pieces aligned on their continuation
+    (2_500_000, 1 << 16, 0.05),     # guesses too late: every piece redrawn from its predecessor
+    (2_200_000, 1 << 16, 0.0),      # guesses early beyond the window: redrawn as well
+    (1 << 21, 1 << 21, None),       # one piece
+    (1_000_003, 1 << 16, None),     # below the parallel threshold: one plain draw
+])
+def test_parallel_normals_equal_one_draw(n, piece, rho):
+    """The start vector drawn in parallel pieces (``_normals.draw``) is value
+    for value the reference's single ``rng.standard_normal(n)``
+    (harness.py:130, linearize.py:113) and leaves the run RNG in the same
+    state, including when a piece's alignment falls back to a redraw."""
+    from paper_2108_13622_b200 import _normals
+    kw = {} if rho is None else {"rho": rho}
+    r1, r2 = np.random.default_rng(7), np.random.default_rng(7)
+    got = _normals.standard_normal(r1, n, piece=piece, threads=4, **kw)
+    assert np.array_equal(got, r2.standard_normal(n))
+    assert r1.bit_generator.state == r2.bit_generator.state
+    assert np.array_equal(r1.standard_normal(5), r2.standard_normal(5))
