@@ -105,8 +105,10 @@ class ClockSampler:
             self.thread.start()
             # let nvidia-smi finish starting up (process spawn, NVML init) before
             # the timed region begins, so it does not compete with the host side
+            # (NVML initialisation on a fresh box can take seconds; a timed
+            # region that overlapped it once ran 2.3x slow on the host side)
             t0 = time.perf_counter()
-            while not self.lines and time.perf_counter() - t0 < 3.0:
+            while len(self.lines) < 2 and time.perf_counter() - t0 < 20.0:
                 time.sleep(0.01)
             self.lines.clear()
         except OSError:
