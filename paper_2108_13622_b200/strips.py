@@ -158,22 +158,24 @@ def global_normal_slice(rng, layout, nx):
     """This rank's slice of rng.standard_normal(8*ny*nx) in the global field-major order.
 
     The reference draws the power-iteration start vector for the whole state
-    (linearize.py:113, harness.py:130); drawing the stream in row chunks
-    reproduces it exactly, and each rank keeps its own rows.
+    (linearize.py:113, harness.py:130).  Every rank draws the whole stream
+    (split over its host cores by ``_normals.draw``: same values, same final
+    generator state as one draw) and keeps its own rows of every field.
     """
+    from paper_2108_13622_b200 import _normals
     out = np.empty((NF, layout.ny, nx))
-    row_chunk = max(1, (1 << 22) // nx)
-    for f in range(NF):
-        r = 0
-        while r < layout.ny_global:
-            k = min(row_chunk, layout.ny_global - r)
-            lo, hi = max(r, layout.y0), min(r + k, layout.y0 + layout.ny)
-            if lo < hi:
-                draw = rng.standard_normal(k * nx).reshape(k, nx)
-                out[f, lo - layout.y0:hi - layout.y0] = draw[lo - r:hi - r]
-            else:
-                rng.standard_normal(k * nx)
-            r += k
+    flat = out.reshape(NF, -1)
+    plane = layout.ny_global * nx
+    lo_off, hi_off = layout.y0 * nx, (layout.y0 + layout.ny) * nx
+
+    def sink(i0, vals):
+        i1 = i0 + vals.size
+        for f in range(NF):
+            a, b = max(i0, f * plane + lo_off), min(i1, f * plane + hi_off)
+            if a < b:
+                flat[f, a - f * plane - lo_off:b - f * plane - lo_off] = vals[a - i0:b - i0]
+
+    _normals.draw(rng, NF * plane, np.empty, sink)
     return out.reshape(-1)
 
 

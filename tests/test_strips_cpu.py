@@ -265,3 +265,19 @@ def test_leja_strip_loop_gloo(tmp_path):
     _spawn(_leja_body, str(path))
     res = eval(path.read_text())
     assert set(res) == {1.0, 25.0} and res[25.0][0] > 64   # crossed a coefficient growth
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_rng_slice_parallel_draw(nranks):
+    """At sizes where the start vector is drawn in parallel pieces, every
+    rank's slice is still its rows of the reference's single global draw
+    (linearize.py:113) and the generator ends where that draw leaves it."""
+    ny, nx = 515, 1024
+    full = np.random.default_rng(9)
+    ref = full.standard_normal(8 * ny * nx).reshape(8, ny, nx)
+    for rank in range(nranks):
+        lay = strips.StripLayout(ny, nranks, rank)
+        rng = np.random.default_rng(9)
+        mine = strips.global_normal_slice(rng, lay, nx)
+        assert np.array_equal(mine.reshape(8, lay.ny, nx), ref[:, lay.y0:lay.y0 + lay.ny])
+        assert rng.bit_generator.state == full.bit_generator.state
