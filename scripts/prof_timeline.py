@@ -1,7 +1,7 @@
 """Device timeline of an adaptive run (torch.profiler / CUPTI): kernel busy time
 vs wall time, per-kernel totals, and the idle gaps between kernels.
 
-usage: prof_timeline.py {c0|c2} [t_final]
+usage: prof_timeline.py {c0|c2} [t_final] | {c3|c4} [steps]
 """
 import collections
 import os
@@ -15,9 +15,15 @@ from paper_2108_13622_b200 import leja, scenarios as sc  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c0"
 tf = float(sys.argv[2]) if len(sys.argv) > 2 else None
-if which == "c3":
+if which in ("c3", "c4"):
     tf, steps = None, (int(sys.argv[2]) if len(sys.argv) > 2 else 5)
-if which == "c3":
+if which == "c4":
+    s = sc.CONFIGS[4]()
+    s.max_accepted = steps
+    warm = sc.CONFIGS[4]()
+    warm.max_accepted = 1
+    scheme = xb.Scheme.EXPRB54S4
+elif which == "c3":
     s = sc.CONFIGS[3]()
     s.max_accepted = steps
     warm = sc.kh_setup(4096, tol=1e-5, t_final=1e9, max_accepted=1)
