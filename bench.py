@@ -84,7 +84,12 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every 100 ms during the timed region.
+
+    In-process NVML (nvidia_ml_py) from a background thread: a few light
+    queries per sample.  A polling nvidia-smi process (the fallback) was seen
+    to stall the host-driven launch loop on some boxes (the timed region ran
+    1.2-2.3x slower than the same loop unsampled)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -93,9 +98,47 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self._stop = threading.Event()
+
+    def _nvml_handle(self, nv):
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        flags = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        act = ["Active" if r & f else "Not Active" for f in flags]
+        return ", ".join([str(sm), str(smax), "0"] + act)
+
+    def _nvml_loop(self):
+        while not self._stop.wait(0.1):
+            try:
+                self.lines.append(self._nvml_sample())
+            except Exception:
+                return
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, self._nvml_handle(nv))
+            self._nvml_sample()   # first query outside the timed region
+            self.thread = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -105,8 +148,6 @@ class ClockSampler:
             self.thread.start()
             # let nvidia-smi finish starting up (process spawn, NVML init) before
             # the timed region begins, so it does not compete with the host side
-            # (NVML initialisation on a fresh box can take seconds; a timed
-            # region that overlapped it once ran 2.3x slow on the host side)
             t0 = time.perf_counter()
             while len(self.lines) < 2 and time.perf_counter() - t0 < 20.0:
                 time.sleep(0.01)
@@ -120,6 +161,14 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self.lines.append(self._nvml_sample())   # the region's last state
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
