@@ -89,14 +89,43 @@ long long xmhd_launch_count(xmhd_ctx* ctx);
 int xmhd_set_halo(xmhd_ctx* ctx, const double* lo, const double* hi, const double* lo_dir,
                   const double* hi_dir);
 
-/* mhd_rhs (mhd.py:127-232): f = F(u). */
-int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f);
+/* Non-finite cells of a failed RHS evaluation, the payload of the reference's
+ * RhsBlowupError (mhd.py:225-231: message from the first cell, `cells` = the
+ * first 8 in C order): bad_cells[0] = number of non-finite entries,
+ * bad_cells[1 + 3k .. 3 + 3k] = (field, i, j) of the k-th (k < 8), -1 when
+ * unused.  j is the row of THIS context's grid (a y-strip adds its y0). */
+#define XMHD_BAD_CELLS_LEN 25
+
+/* mhd_rhs (mhd.py:127-232): f = F(u).  Replaces the RHS callback
+ * `lambda flat: mhd_rhs(geometry.with_flat(flat), params)` (harness.py:129).
+ * On XMHD_NONFINITE, bad_cells (int[XMHD_BAD_CELLS_LEN], may be NULL) receives
+ * the cells. */
+int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f, int* bad_cells);
 
 /* jvp (linearize.py:56-67): out = (F(u + eps*w) - fu) / eps with
  * eps = sqrt(eps_mach)*max(1,unorm)/max(||w||,1e-300); zero w -> zeros, no RHS call.
- * *called = number of RHS evaluations (0 or 1); *out_norm = ||out|| (may be NULL). */
+ * *called = number of RHS evaluations (0 or 1); *out_norm = ||out|| (may be NULL).
+ * On XMHD_NONFINITE, bad_cells (may be NULL) receives the cells of
+ * F(u + eps*w), the evaluation the reference raises from (single domain). */
 int xmhd_jvp(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w,
-             double* out, int* called, double* out_norm);
+             double* out, int* called, double* out_norm, int* bad_cells);
+
+/* apply_phi_leja (leja.py:103-150) for the frozen MHD Jacobian in ONE call:
+ * p_out = phi_l(dt J(u)) v by Newton interpolation at the Leja points xi[500]
+ * on [q - 2 theta, q + 2 theta], the whole loop on the device.  `coeffs` holds
+ * ncoef entries of the table the reference indexes (xmhd_leja_schedule builds
+ * the uncached one; a caller with a coefficient cache passes its cached chunk
+ * where leja.py:90-99 would return it).  Outputs = PhiApplyResult: iterations
+ * (= RHS evaluations, *rhs_calls), converged (0/1), residual (inf after a
+ * blow-up).  Non-convergence is a result, not an error (XMHD_OK); a
+ * non-finite RHS returns XMHD_NONFINITE with bad_cells filled (the reference
+ * raises RhsBlowupError from the matvec); a table shorter than the degree
+ * reached returns XMHD_BADARG.  Single-domain contexts only. */
+int xmhd_leja(xmhd_ctx* ctx, int l, const double* u, const double* fu, double unorm,
+              const double* v, double dt, double q, double theta, double tol,
+              const double* xi, const double* coeffs, int ncoef, double* p_out,
+              int* iterations, int* converged, double* residual, int* rhs_calls,
+              int* bad_cells);
 
 /* Asynchronous single-domain steps: every call below only enqueues work on the
  * context's stream; xmhd_async_fetch synchronises once and returns the step's
@@ -345,6 +374,13 @@ int xmhd_krylov_combine(xmhd_ctx* ctx, const double* const* basis, const double*
  * phi_l of the bidiagonal node matrix, bitwise equal to the NumPy routine.
  * out has n entries. */
 int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double subdiag, double* out);
+/* _newton_coeffs without the cache (leja.py:94-96): the first `count` Newton
+ * coefficients of phi_l(q + theta*xi) / theta**l (host, bitwise NumPy). */
+int xmhd_newton_coeffs(int l, double q, double theta, const double* xi, int count, double* out);
+/* The 500-entry table an uncached apply_phi_leja call indexes with the chunk
+ * schedule of leja.py:119-130 (64 -> 128 -> 256 -> 500, each chunk recomputed):
+ * entries [0,64) of the 64-chunk, [64,128) of the 128-chunk, ... (host). */
+int xmhd_leja_schedule(int l, double q, double theta, const double* xi, double* out500);
 
 #ifdef __cplusplus
 }

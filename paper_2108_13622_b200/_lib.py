@@ -14,6 +14,7 @@ import torch
 from paper_2108_13622_b200 import build as _build
 
 OK, NONFINITE, BADARG, CUDA_ERROR = 0, 1, 2, 3
+BAD_CELLS_LEN = 25   # XMHD_BAD_CELLS_LEN: count + 8 (field, i, j) triples
 BC_PERIODIC, BC_REFLECTING, BC_HALO = 0, 1, 2
 (LEJA_RUNNING, LEJA_CONVERGED, LEJA_BLOWUP, LEJA_RHS_NONFINITE, LEJA_NEED_COEFFS,
  LEJA_EXHAUSTED, LEJA_PEER_TIMEOUT, LEJA_MODE_ERROR) = range(8)
@@ -58,8 +59,12 @@ _SIGS = {
     "xmhd_plan_info": (_I, [_P, _PI]),
     "xmhd_launch_count": (_L, [_P]),
     "xmhd_set_halo": (_I, [_P, _P, _P, _P, _P]),
-    "xmhd_rhs": (_I, [_P, _P, _P]),
-    "xmhd_jvp": (_I, [_P, _P, _P, _D, _P, _P, _PI, _PD]),
+    "xmhd_rhs": (_I, [_P, _P, _P, _PI]),
+    "xmhd_jvp": (_I, [_P, _P, _P, _D, _P, _P, _PI, _PD, _PI]),
+    "xmhd_leja": (_I, [_P, _I, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I, _P, _PI, _PI,
+                       _PD, _PI, _PI]),
+    "xmhd_newton_coeffs": (_I, [_I, _D, _D, _PD, _I, _PD]),
+    "xmhd_leja_schedule": (_I, [_I, _D, _D, _PD, _PD]),
     "xmhd_async_begin": (_I, [_P]),
     "xmhd_rhs_async": (_I, [_P, _P, _P]),
     "xmhd_jvp_async": (_I, [_P, _P, _P, _D, _P, _P]),

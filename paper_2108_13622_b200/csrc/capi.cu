@@ -69,6 +69,8 @@ struct xmhd_ctx {
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
   bool force_ieee = false;
+  unsigned long long* scan_d = nullptr;   // [2] non-finite scan (min index, count)
+  unsigned long long* scan_h = nullptr;   // pinned [2]
 };
 
 namespace {
@@ -269,9 +271,10 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   h.thetad = make_divisor(theta, c->force_ieee);
   h.force_ieee = c->force_ieee ? 1 : 0;
   h.epoch = c->p2p_epoch;
-  // the generic update stores every term; y-strips keep p (their all-reduce
-  // carries two sums); a single domain defers with lookahead
-  h.defer = (!c->leja_defer || generic) ? 0 : 2;   // the generic update stores every term
+  // the generic update stores every term; every fused call (one domain and
+  // y-strips alike) uses the lookahead schedule, the strips all-reducing four
+  // values per term [sum y'^2, sum p'^2, sum pending p^2, bad]
+  h.defer = (!c->leja_defer || generic) ? 0 : 2;
   c->leja_next_term = 1;
   *c->ctl_h = h;
   // staged from pageable memory at the call: back-to-back asynchronous
@@ -440,7 +443,70 @@ int xmhd_set_halo(xmhd_ctx* c, const double* lo, const double* hi, const double*
   return XMHD_OK;
 }
 
-int xmhd_rhs(xmhd_ctx* c, const double* u, double* f) {
+// RhsBlowupError.cells of mhd.py:225-231 from a device RHS output: out[0] =
+// number of non-finite entries, then up to 8 (field, i, j) triples in C order
+// (flat index order of the (8, ny, nx) layout); unused triples are -1.
+static int scan_bad_cells(xmhd_ctx* c, const double* f, int* out) {
+  if (!out) return XMHD_OK;
+  for (int k = 0; k < XMHD_BAD_CELLS_LEN; ++k) out[k] = -1;
+  if (!c->scan_d) {
+    CK(cudaMalloc(&c->scan_d, 2 * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&c->scan_h, 2 * sizeof(unsigned long long)));
+  }
+  const long long n = NF * c->g.plane;
+  long long after = -1;
+  for (int k = 0; k < 8; ++k) {
+    CK(cudaMemsetAsync(c->scan_d, 0xff, sizeof(unsigned long long), c->stream));
+    if (k == 0) CK(cudaMemsetAsync(c->scan_d + 1, 0, sizeof(unsigned long long), c->stream));
+    CK(launch_nonfinite_scan(f, n, after, c->scan_d, k == 0 ? c->scan_d + 1 : nullptr,
+                             c->stream));
+    c->launches++;
+    CK(cudaMemcpyAsync(c->scan_h, c->scan_d, 2 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (k == 0) out[0] = c->scan_h[1] > 0x7fffffffull ? 0x7fffffff : (int)c->scan_h[1];
+    const unsigned long long idx = c->scan_h[0];
+    if (idx == ~0ull) break;
+    const long long plane = c->g.plane;
+    const long long field = (long long)idx / plane, rem = (long long)idx - field * plane;
+    out[1 + 3 * k] = (int)field;
+    out[2 + 3 * k] = (int)(rem % c->g.nx);
+    out[3 + 3 * k] = (int)(rem / c->g.nx);
+    after = (long long)idx;
+  }
+  return XMHD_OK;
+}
+
+// F(u + eps*w) into scratch and its non-finite cells (the JVP / Leja failure
+// path: the reference raises from mhd_rhs of that state, linearize.py:67).
+static int scan_bad_cells_shifted(xmhd_ctx* c, const double* u, const double* w, double eps,
+                                  int* out) {
+  if (!out) return XMHD_OK;
+  const long long n = NF * c->g.plane;
+  double* x = nullptr;
+  double* fx = nullptr;
+  CK(cudaMallocAsync(&x, 2 * sizeof(double) * n, c->stream));
+  fx = x + n;
+  const double* v[2] = {u, w};
+  const double cf[2] = {1.0, eps};
+  int rc = XMHD_OK;
+  if (launch_lincomb(x, n, v, cf, 2, 0, redbuf(c), c->stream) != cudaSuccess) {
+    rc = fail(XMHD_CUDA_ERROR, "lincomb launch failed");
+  } else {
+    StencilArgs a = base_args(c);
+    a.u = x;
+    a.out = fx;
+    if (launch_stencil(MODE_RHS, a, c->grid, c->stream) != cudaSuccess)
+      rc = fail(XMHD_CUDA_ERROR, "rhs launch failed");
+    else
+      rc = scan_bad_cells(c, fx, out);
+    c->launches += 2;
+  }
+  cudaFreeAsync(x, c->stream);
+  return rc;
+}
+
+int xmhd_rhs(xmhd_ctx* c, const double* u, double* f, int* bad_cells) {
   if (!c || !u || !f) return fail(XMHD_BADARG, "null arg");
   if (c->g.bcy == BC_HALO && !c->g.halo_lo) return fail(XMHD_BADARG, "halo rows not set");
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
@@ -452,11 +518,13 @@ int xmhd_rhs(xmhd_ctx* c, const double* u, double* f) {
   int bad = 0;
   int rc = fetch_bad(c, &bad);
   if (rc) return rc;
-  return bad ? XMHD_NONFINITE : XMHD_OK;
+  if (!bad) return XMHD_OK;
+  rc = scan_bad_cells(c, f, bad_cells);
+  return rc ? rc : XMHD_NONFINITE;
 }
 
 int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w,
-             double* out, int* called, double* out_norm) {
+             double* out, int* called, double* out_norm, int* bad_cells) {
   if (!c || !u || !fu || !w || !out) return fail(XMHD_BADARG, "null arg");
   const long long n = NF * c->g.plane;
   CK(launch_norm(w, n, redbuf(c), c->stream));
@@ -489,7 +557,12 @@ int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const
   int bad = 0;
   rc = fetch_bad(c, &bad);
   if (rc) return rc;
-  return bad ? XMHD_NONFINITE : XMHD_OK;
+  if (!bad) return XMHD_OK;
+  if (c->g.bcy != BC_HALO) {
+    rc = scan_bad_cells_shifted(c, u, w, eps, bad_cells);
+    if (rc) return rc;
+  }
+  return XMHD_NONFINITE;
 }
 
 // Device-resident power iteration of estimate_alpha (linearize.py:113-135).
@@ -945,6 +1018,61 @@ int xmhd_leja_result(xmhd_ctx* c, double* p_out) {
   const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
   CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
   c->launches++;
+  return XMHD_OK;
+}
+
+// apply_phi_leja (leja.py:103-150) in ONE call: the whole Newton loop runs
+// on the device (one cooperative launch on small grids, host-paced batches of
+// fused iteration kernels otherwise) against a coefficient table that already
+// holds every entry the call may index, built with the reference's chunk
+// schedule (xmhd_leja_schedule: entries [0,64) of the 64-chunk, [64,128) of
+// the 128-chunk, ... as leja.py:119-130 fetches them for an uncached
+// (l, q, theta)).  A table shorter than the degree the call reaches is an
+// error (XMHD_BADARG), never a silent truncation.
+int xmhd_leja(xmhd_ctx* c, int l, const double* u, const double* fu, double unorm,
+              const double* v, double dt, double q, double theta, double tol,
+              const double* xi, const double* coeffs, int ncoef, double* p_out,
+              int* iterations, int* converged, double* residual, int* rhs_calls,
+              int* bad_cells) {
+  if (!c || !u || !fu || !v || !xi || !coeffs || !p_out)
+    return fail(XMHD_BADARG, "null arg");
+  if (l < 0 || l > 4) return fail(XMHD_BADARG, "phi order must be an integer in [0, 4]");
+  if (!(tol > 0.0)) return fail(XMHD_BADARG, "tolerance must be positive");
+  if (!(theta > 0.0)) return fail(XMHD_BADARG, "spectral magnitude must be positive");
+  if (ncoef < 2 || ncoef > 500) return fail(XMHD_BADARG, "ncoef must lie in [2, 500]");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "use the strip driver for BC_HALO");
+  const long long n = NF * c->g.plane;
+  c->leja_u = u;
+  c->leja_fu = fu;
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+  if (rc) return rc;
+  xmhd_leja_state st;
+  if (xmhd_leja_loop_available(c)) {
+    rc = xmhd_leja_loop(c);
+    if (rc) return rc;
+    rc = sync_ctl(c);
+    if (rc) return rc;
+    fill_state(*c->ctl_h, &st);
+  } else {
+    rc = leja_run(c, &st);
+    if (rc) return rc;
+  }
+  if (st.status == LJ_MODE_ERROR)
+    return fail(XMHD_CUDA_ERROR, "Leja kernel variant / interpolant mode mismatch");
+  if (st.status == LJ_NEED_COEFFS)
+    return fail(XMHD_BADARG, "coefficient table ended at term " + std::to_string(st.m) +
+                                 ": pass entries up to the reference's 500-entry chunk");
+  if (iterations) *iterations = st.iterations;
+  if (rhs_calls) *rhs_calls = st.rhs_calls;
+  if (converged) *converged = st.status == LJ_CONVERGED;
+  if (residual) *residual = st.residual;
+  if (st.status == LJ_RHS_BAD) {
+    rc = scan_bad_cells_shifted(c, u, c->ybuf[c->ctl_h->cur], st.eps, bad_cells);
+    return rc ? rc : XMHD_NONFINITE;
+  }
+  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
+  c->launches++;
+  CK(cudaStreamSynchronize(c->stream));
   return XMHD_OK;
 }
 

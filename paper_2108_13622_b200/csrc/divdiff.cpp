@@ -80,3 +80,36 @@ extern "C" int xmhd_phi_divided_diffs(int l, const double* nodes, int n, double 
   for (int i = 0; i < n; ++i) out[i] = col[l + i];
   return XMHD_OK;
 }
+
+// _newton_coeffs without the cache (leja.py:94-96): the divided differences of
+// phi_l(q + theta*xi) at the first `count` Leja points, divided by theta**l
+// (Python float ** int is C pow).
+extern "C" int xmhd_newton_coeffs(int l, double q, double theta, const double* xi, int count,
+                                  double* out) {
+  if (l < 0 || l > 4 || count < 1 || count > 500 || !xi || !out || !(theta > 0.0))
+    return XMHD_BADARG;
+  std::vector<double> nodes(count);
+  for (int i = 0; i < count; ++i) nodes[i] = q + theta * xi[i];
+  const int rc = xmhd_phi_divided_diffs(l, nodes.data(), count, theta, out);
+  if (rc) return rc;
+  const double s = std::pow(theta, (double)l);
+  for (int i = 0; i < count; ++i) out[i] = out[i] / s;
+  return XMHD_OK;
+}
+
+// The 500-entry table one apply_phi_leja call of an uncached (l, q, theta)
+// indexes (leja.py:119-130): term m < 64 reads the 64-chunk, m < 128 the
+// 128-chunk (recomputed, not extended), m < 256 the 256-chunk, else the
+// 500-chunk.  xmhd_leja takes it as its coefficient table.
+extern "C" int xmhd_leja_schedule(int l, double q, double theta, const double* xi, double* out) {
+  if (!out) return XMHD_BADARG;
+  std::vector<double> chunk(500);
+  int lo = 0;
+  for (int size : {64, 128, 256, 500}) {
+    const int rc = xmhd_newton_coeffs(l, q, theta, xi, size, chunk.data());
+    if (rc) return rc;
+    for (int i = lo; i < size; ++i) out[i] = chunk[i];
+    lo = size;
+  }
+  return XMHD_OK;
+}

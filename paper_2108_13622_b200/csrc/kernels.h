@@ -284,6 +284,11 @@ cudaError_t launch_leja_p2p_init_emul(const StencilArgs* args_dev, int nranks, c
 cudaError_t launch_leja_extend(LejaCtl* ctl, int to, cudaStream_t s);
 // Connectivity probe: write `value` into every peer board (slot 0, my row).
 cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s);
+// Non-finite scan (vec.cu): count of non-finite entries and the smallest flat
+// index > after (atomicMin into *minidx, preset by the caller to ~0).
+cudaError_t launch_nonfinite_scan(const double* f, long long n, long long after,
+                                  unsigned long long* minidx, unsigned long long* count,
+                                  cudaStream_t s);
 
 #ifdef __CUDACC__
 // All-reduce of 4 doubles over the ranks through peer memory (one thread).

@@ -630,3 +630,36 @@ cudaError_t launch_leja_update(const double* w, long long n, LejaCtl* ctl, doubl
 }
 
 }  // namespace xb
+
+// ---------------------------------------------------------------------------
+// Non-finite cell scan of an RHS output (failure path of xmhd_rhs / xmhd_jvp /
+// xmhd_leja): the count of non-finite entries and the smallest flat index
+// above `after` (C order (field, j, i) of mhd.py:225-231).  One pass per
+// reported cell; only runs after a kernel already flagged the output.
+namespace xb {
+
+__global__ void __launch_bounds__(VT) nonfinite_scan_kernel(const double* __restrict__ f,
+                                                             long long n, long long after,
+                                                             unsigned long long* minidx,
+                                                             unsigned long long* count) {
+  unsigned long long cnt = 0, best = ~0ull;
+  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
+       i += (long long)gridDim.x * VT) {
+    const unsigned hi = (unsigned)__double2hiint(__ldg(f + i));
+    if ((hi & 0x7ff00000u) == 0x7ff00000u) {
+      ++cnt;
+      if (i > after && (unsigned long long)i < best) best = (unsigned long long)i;
+    }
+  }
+  if (count && cnt) atomicAdd(count, cnt);
+  if (best != ~0ull) atomicMin(minidx, best);
+}
+
+cudaError_t launch_nonfinite_scan(const double* f, long long n, long long after,
+                                  unsigned long long* minidx, unsigned long long* count,
+                                  cudaStream_t s) {
+  nonfinite_scan_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(f, n, after, minidx, count);
+  return cudaGetLastError();
+}
+
+}  // namespace xb

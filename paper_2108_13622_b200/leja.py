@@ -112,7 +112,36 @@ def _compute_coeffs(l, q, theta, count):
 # (l, q, theta, count), so the values are the ones an on-demand computation
 # would produce).  The cache below still follows the reference's policy.
 _spec_pool = ThreadPoolExecutor(max_workers=4, thread_name_prefix="leja-coeffs")
-_spec = {}
+_spec_all = {}
+
+
+class _SpecView:
+    """Per-host-thread view of the speculation table (like _cache()): ranks
+    emulated by threads share (l, q, theta, count) keys and must not pop or
+    iterate each other's entries."""
+
+    def _d(self):
+        if threading.current_thread() is threading.main_thread():
+            return _spec_all
+        d = getattr(_tls, "spec", None)
+        if d is None:
+            d = _tls.spec = {}
+        return d
+
+    def __contains__(self, key):
+        return key in self._d()
+
+    def __iter__(self):
+        return iter(list(self._d()))
+
+    def __setitem__(self, key, value):
+        self._d()[key] = value
+
+    def pop(self, key, default=None):
+        return self._d().pop(key, default)
+
+
+_spec = _SpecView()
 _degree_hint = {}
 
 
@@ -125,7 +154,9 @@ def _speculate(l, q, theta, count):
 
 def _drop_speculation(l, q, theta):
     for key in [k for k in _spec if k[:3] == (l, q, theta)]:
-        _spec.pop(key).cancel()
+        fut = _spec.pop(key, None)
+        if fut is not None:
+            fut.cancel()
 
 
 def _newton_coeffs(l, q, theta, count):
@@ -207,6 +238,37 @@ def _grow(l, q, theta, chunk, coeffs, m):
         # the reference indexes coeffs[m] next and fails the same way
         raise IndexError(f"index {m} is out of bounds for axis 0 with size {coeffs.size}")
     return chunk, coeffs
+
+
+def _grow_pending(l, q, theta, chunk, m):
+    """The table leja.py:128-130 fetches at term m, WITHOUT touching the cache.
+
+    A device loop with the lookahead schedule can stop for coefficients at an
+    odd term whose convergence is not resolved yet; if the call turns out to
+    have converged on the term before, the reference never grew the table.
+    So the grown table is only uploaded here, and ``_commit_growth`` performs
+    the cache insert afterwards for the boundaries the call actually crossed.
+    Returns (chunk, table, computed): ``computed`` is False when the reference
+    would have found the table in the cache (no insert then)."""
+    chunk = min(2 * chunk, LEJA_MAX)
+    hit = _cache().get((l, q, theta))
+    if hit is not None and hit.size >= chunk:
+        table, computed = hit, False
+    else:
+        fut = _spec.pop((l, q, theta, chunk), None)
+        table = fut.result() if fut is not None else _compute_coeffs(l, q, theta, chunk)
+        computed = True
+    if m >= table.size:
+        raise IndexError(f"index {m} is out of bounds for axis 0 with size {table.size}")
+    return chunk, table, computed
+
+
+def _commit_growth(l, q, theta, grown, iterations):
+    """Cache inserts of the growths in ``grown`` ([(m, table, computed)]) whose
+    term m the call reached (iterations >= m), in order."""
+    for m_b, table, computed in grown:
+        if computed and iterations >= m_b:
+            _cache_insert(l, q, theta, table)
 
 
 def _ptr_d(a):
@@ -355,13 +417,17 @@ def drive_loop(lib, h, l, q, theta, coeffs):
     st = _lib.LejaState()
     chunk = 64
     size = coeffs.size
+    grown = []
     while True:
         _lib.check(lib.xmhd_leja_loop(h), "xmhd_leja_loop")
         _lib.check(lib.xmhd_leja_sync(h, ctypes.byref(st)), "xmhd_leja_sync")
         if st.status != _lib.LEJA_NEED_COEFFS:
+            _commit_growth(l, q, theta, grown, st.iterations)
             return st
-        chunk, grown = _grow(l, q, theta, chunk, _cache().get((l, q, theta), coeffs), st.m)
-        arr = np.ascontiguousarray(grown)
+        m = int(st.m)
+        chunk, table, computed = _grow_pending(l, q, theta, chunk, m)
+        grown.append((m, table, computed))
+        arr = np.ascontiguousarray(table)
         _lib.check(lib.xmhd_leja_extend(h, _ptr_d(arr), size, arr.size), "xmhd_leja_extend")
         size = arr.size
 

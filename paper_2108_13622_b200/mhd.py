@@ -107,15 +107,50 @@ def context_for(nx, ny, dx, dy, params):
     return c
 
 
-def _blowup(f, nx, ny):
-    """RhsBlowupError with the reference's message and cell list (mhd.py:225-231)."""
+def _blowup_scan(f, nx, ny, j0=0):
+    """(count, first <= 8 non-finite cells as (field, j + j0, i)) in C order."""
     host = _ops.to_host(f).reshape(NVAR, ny, nx)
     bad = np.argwhere(~np.isfinite(host))
-    field, j, i = bad[0]
+    return len(bad), [(int(k), int(jj) + j0, int(ii)) for k, jj, ii in bad[:8]]
+
+
+def _blowup_error(count, cells):
+    """RhsBlowupError with the reference's message and cell list (mhd.py:225-231)
+    from C-ordered (field, j, i) cells and the total count."""
+    field, j, i = cells[0]
     return RhsBlowupError(
         f"non-finite rhs in field {FIELD_NAMES[field]} at cell "
-        f"(i={i}, j={j}); {len(bad)} cells affected",
-        cells=[(FIELD_NAMES[k], int(ii), int(jj)) for k, jj, ii in bad[:8]])
+        f"(i={i}, j={j}); {count} cells affected",
+        cells=[(FIELD_NAMES[k], ii, jj) for k, jj, ii in cells[:8]])
+
+
+def _blowup(f, nx, ny):
+    """RhsBlowupError with the reference's message and cell list (mhd.py:225-231)."""
+    return _blowup_error(*_blowup_scan(f, nx, ny))
+
+
+def bad_cells_buffer():
+    """int[XMHD_BAD_CELLS_LEN] out-parameter of xmhd_rhs / xmhd_jvp / xmhd_leja."""
+    return (ctypes.c_int * _lib.BAD_CELLS_LEN)()
+
+
+def decode_bad_cells(buf, j0=0):
+    """(count, [(field, j + j0, i)]) from an XMHD_BAD_CELLS_LEN buffer."""
+    cells = []
+    for k in range(8):
+        f, i, j = buf[1 + 3 * k], buf[2 + 3 * k], buf[3 + 3 * k]
+        if f < 0:
+            break
+        cells.append((f, j + j0, i))
+    return buf[0], cells
+
+
+def blowup_from_cells(buf):
+    """RhsBlowupError from the cells the C-ABI reported."""
+    count, cells = decode_bad_cells(buf)
+    if not cells:
+        return RhsBlowupError("non-finite rhs (no cell reported)")
+    return _blowup_error(count, cells)
 
 
 class MhdRhs:
@@ -140,10 +175,11 @@ class MhdRhs:
         if out is None:
             out = torch.empty_like(u)
         lib = _lib.load()
-        rc = lib.xmhd_rhs(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(out))
+        bad = bad_cells_buffer()
+        rc = lib.xmhd_rhs(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(out), bad)
         _lib.check(rc, "xmhd_rhs")
         if rc == _lib.NONFINITE:
-            raise _blowup(out, self.nx, self.ny)
+            raise blowup_from_cells(bad)
         return out
 
 

@@ -163,6 +163,11 @@ def initial_fields(s):
 
 
 def unit_gaussian(n, seed):
-    """Seeded unit-norm Gaussian vector (config 1's v)."""
+    """Seeded unit-norm Gaussian vector (config 1's v).
+
+    Normalised with NumPy's pairwise ``add.reduce`` rather than
+    ``np.linalg.norm``: OpenBLAS ``ddot`` splits large vectors over threads, so
+    its last bit depends on the host's core count, and the committed golden
+    fixtures (tests/golden/large/) must see the same v on every host."""
     v = np.random.default_rng(seed).standard_normal(n)
-    return v / np.linalg.norm(v)
+    return v / np.sqrt(np.add.reduce(v * v))

@@ -254,20 +254,36 @@ class StripMhd:
         return halo.exchange(flat.reshape(NF, self.ny, self.nx), self.comm, self.periodic_y)
 
     def __call__(self, flat, out=None):
-        from paper_2108_13622_b200.mhd import _blowup
         u = _ops.as_device(flat).reshape(-1)
         if u.numel() != self.n:
             raise ValueError(f"strip state has {u.numel()} entries, needs {self.n}")
         out = torch.empty_like(u) if out is None else out
         self.exchange(u, self.state_halo)
         self._set_halo(self.state_halo)
-        rc = _lib.load().xmhd_rhs(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(out))
+        from paper_2108_13622_b200.mhd import bad_cells_buffer
+        bad = bad_cells_buffer()
+        rc = _lib.load().xmhd_rhs(self.ctx.bind_stream(), _lib.ptr(u), _lib.ptr(out), bad)
         _lib.check(rc, "xmhd_rhs (strip)")
-        if rc == _lib.NONFINITE:
-            err = _blowup(out, self.nx, self.ny)
-            err.cells = [(f, i, j + self.layout.y0) for f, i, j in (err.cells or [])]
-            raise err
+        self.raise_if_nonfinite(rc == _lib.NONFINITE, bad, out.device)
         return out
+
+    def raise_if_nonfinite(self, local_bad, bad, device):
+        """Every rank raises the same RhsBlowupError when ANY strip's F is
+        non-finite (one scalar all-reduce): the message and ``cells`` name the
+        first cells of the whole grid in C order with global row indices and
+        the global count, as mhd.py:225-231 reports them on one grid."""
+        from paper_2108_13622_b200.mhd import _blowup_error, decode_bad_cells
+        if self.comm.size > 1:
+            t = torch.tensor([1.0 if local_bad else 0.0], dtype=torch.float64, device=device)
+            if not self.comm.allreduce_sum(t).item():
+                return
+        elif not local_bad:
+            return
+        count, cells = decode_bad_cells(bad, self.layout.y0) if local_bad else (0, [])
+        parts = self.comm.gather_host((count, cells))
+        total = sum(c for c, _ in parts)
+        merged = sorted(cell for _, cl in parts for cell in cl)
+        raise _blowup_error(total, merged[:8])
 
     # -- per-step diagnostics over all strips (harness.py:105-116, 137-138, 209-211, 243)
     def divb_max(self, u):
@@ -436,13 +452,19 @@ def apply_phi_leja_strips(l, lin, v, dt, shift, tol, xi):
         leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
         return c
 
+    grown = []
+
     def grow_fn(chunk, coeffs, m):
-        chunk, grown = leja._grow(l, q, theta, chunk, coeffs, m)
+        # the cache insert waits for the call's end (lookahead: term m may
+        # never have happened in the reference, leja._grow_pending)
+        chunk, table, computed = leja._grow_pending(l, q, theta, chunk, m)
+        grown.append((m, table, computed))
         leja._speculate(l, q, theta, min(2 * chunk, leja.LEJA_MAX))
-        return chunk, np.ascontiguousarray(grown)
+        return chunk, np.ascontiguousarray(table)
 
     st = leja_strips(backend, mhd.comm, mhd.periodic_y, l, vd, dt, q, theta, tol, xi,
                      coeff_fn, grow_fn)
+    leja._commit_growth(l, q, theta, grown, st.iterations)
     leja._drop_speculation(l, q, theta)
     return _finish(l, lin, mhd, backend, vd, v, st)
 

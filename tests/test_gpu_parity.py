@@ -83,7 +83,7 @@ def test_rhs_ieee_division_build_agrees(xb, monkeypatch):
             ctx = _lib.Context(setup.nx, setup.ny, setup.dx, setup.dy, setup.mu, setup.eta,
                                setup.kappa, setup.gamma, setup.mu0, 0, 0)
             f = torch.empty_like(q)
-            assert _lib.load().xmhd_rhs(ctx.bind_stream(), _lib.ptr(q), _lib.ptr(f)) == 0
+            assert _lib.load().xmhd_rhs(ctx.bind_stream(), _lib.ptr(q), _lib.ptr(f), None) == 0
             outs.append(f.cpu().numpy())
         assert np.array_equal(outs[0], outs[1])
 
