@@ -7,23 +7,33 @@ coefficient cache cleared per step so the host coefficient work is included.
 
   value : cell-updates/s = sum(Leja iterations) * nx*ny / device time, inputs
           resident in HBM (state vectors 268 MB each >> 126 MB L2: no flush).
-  e2e   : same metric through the public API with pinned HOST buffers: per step
-          u and the 4 right-hand vectors are copied H2D and the 4 results D2H.
+  e2e   : same metric through the public API the reference's callers use:
+          plain (pageable) NumPy arrays in, NumPy arrays out; per step u and
+          the 4 right-hand vectors go H2D and the 4 results D2H.  ``e2e_pinned``
+          is the same with page-locked torch host tensors.
   roofline : the fused Leja iteration kernel, timed with CUDA events on its
           stream.  Algorithmic bytes per cell per Newton term:
           320 (lookahead interpolant schedule: an odd term reads u, y, F(u)
           and writes y' = 256 B, the even term reads u, y, F(u), p and writes
-          y', p' = 384 B), 384 with XMHD_PDEFER=0.
+          y', p' = 384 B), 384 with XMHD_PDEFER=0; ``by_kind`` gives each term
+          kind against its own bytes.
   stencil_kernels : the RHS (128 B/cell) and FD-JVP (256 B/cell) stencil
           kernels of the metric's "RHS/Jv", timed the same way (N=1 only).
+  scale_case : north_star's strong-scaling case: phi_1(dt J) F(u)/||F(u)|| on
+          the 8192^2 Harris state of config 4 (alpha*dt in {1, 10, 100}),
+          y-strips over the N ranks, each rank building only its own rows.
   cpu_baseline : the NumPy oracle (the reference's own algorithm, oracle/) on a
           bounded sample of the same workload on this host.
 
-``--impl reference`` times that CPU implementation alone (rank 0; other ranks
-exit 0).  N>1 under torchrun: one process per GPU, the 2048^2 grid split into
-y-strips (2-row NCCL halo exchange + one 3-scalar allreduce per Leja term,
-paper_2108_13622_b200/strips.py); the total work is fixed ("scaling": "strong")
-and `value` is whole-job cell-updates/s over the max-over-ranks device time.
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` (N ranks, 127.0.0.1), after checking that N GPUs are
+visible (it fails loudly otherwise instead of timing one GPU).  Under N>1 the
+2048^2 grid is split into y-strips (2-row halo + one 4-scalar all-reduce per
+Leja term inside the fused kernel over peer memory, or NCCL,
+paper_2108_13622_b200/strips.py); the total work is fixed ("scaling":
+"strong") and `value` is whole-job cell-updates/s over the max-over-ranks
+device time.  ``--impl reference`` times that CPU implementation alone (rank
+0; other ranks exit 0).
 """
 
 import argparse
@@ -57,7 +67,32 @@ def parse():
     ap.add_argument("--n", type=int, default=2048, help="grid size (config 1: 2048)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exprb", action="store_true")
+    ap.add_argument("--no-scale-case", action="store_true")
+    ap.add_argument("--scale-n", type=int, default=8192, help="scale_case grid (config 4: 8192)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run, or
+    fail loudly when fewer than N GPUs are visible (never time N=1 silently).
+    Returns an exit code, or None when this process is already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) "
+                             f"visible; refusing to report a {args.gpus}-GPU number\n")
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def ncu_traffic(n, local_cells):
@@ -258,7 +293,17 @@ def workload_name(n):
     return f"config1: phi_1(dt J)v at {n}^2, alpha*dt sweep {list(SWEEP)}, Leja tol {LEJA_TOL:g}"
 
 
-def reference_arm(args, rank):
+def workload_config(n):
+    """The `config` dict of BOTH arms (same workload, same keys)."""
+    return {"workload": workload_name(n), "grid": n, "alpha_dt": list(SWEEP),
+            "leja_tol": LEJA_TOL, "l2_policy": "inputs larger than L2 (268 MB per vector)"}
+
+
+DATA = ("synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes per field; "
+        "v seeded unit Gaussian)")
+
+
+def reference_arm(args, rank, world):
     if rank != 0:
         return
     iters = max(1, args.steps)
@@ -271,17 +316,16 @@ def reference_arm(args, rank):
     value = float(np.mean(samples))
     cores = r["cores"]
     wall = time.perf_counter() - t0
-    line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": args.gpus,
+    line = {"metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world,
             "steps": iters, "warmup": args.warmup, "ms_per_step": 1e3 * args.n ** 2 / value,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes "
-                    "per field; v seeded unit Gaussian)", "impl": "reference",
-            "config": {"workload": workload_name(args.n), "grid": args.n,
-                       "parallelism": "cpu (reference NumPy path: ufuncs on one core, BLAS "
-                                      "norms multi-threaded)",
-                       "sample": "each step = 1 Leja term (FD-JVP + Newton update + 2 norms) "
-                                 "of the alpha*dt=10 call; the metric is per cell-update, so "
-                                 "the sweep's rate is the per-term rate"},
+            "data": DATA, "impl": "reference",
+            "config": workload_config(args.n),
+            "parallelism": "cpu (reference NumPy path: ufuncs on one core, BLAS norms "
+                           "multi-threaded); rank 0 only",
+            "sampling": "each step = 1 Leja term (FD-JVP + Newton update + 2 norms) of the "
+                        "alpha*dt=10 call; the metric is per cell-update, so the sweep's rate "
+                        "is the per-term rate",
             "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores,
                              "kind": "port",
                              "sample": f"1 Leja iteration per step at {args.n}^2 via the NumPy "
@@ -300,44 +344,82 @@ def total_launches(op=None):
     return sum(c.launches() for c in ctxs)
 
 
+class Job:
+    """Rank / device plumbing shared by the bench parts."""
+
+    def __init__(self, world, rank, local):
+        import torch
+        import torch.distributed as dist
+        self.world, self.rank, self.local = world, rank, local
+        self.torch, self.dist = torch, dist
+        self.comm = None
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
+
+    def maxed(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def domain(self, xb, setup, params):
+        """(RHS operator, this rank's initial rows on the device) of a Setup."""
+        from paper_2108_13622_b200 import scenarios as sc, strips
+        if self.world > 1:
+            if self.comm is None:
+                self.comm = strips.Comm()
+                xb.linearize._ops.set_reducer(
+                    strips.Reducer(self.comm, self.torch.device("cuda", self.local)))
+            mhd = strips.StripMhd(xb.StateGrid(setup.nx, setup.ny, setup.dx, setup.dy, None),
+                                  params, self.comm)
+            rows = (mhd.layout.y0, mhd.layout.y0 + mhd.layout.ny)
+            q = sc.initial_fields(setup, rows)
+            u = self.torch.from_numpy(q).cuda().reshape(-1)
+            return mhd, u, rows
+        q = sc.initial_fields(setup)
+        u = self.torch.from_numpy(q).cuda().reshape(-1)
+        st = xb.StateGrid(setup.nx, setup.ny, setup.dx, setup.dy, u.reshape(8, setup.ny, setup.nx))
+        return xb.MhdRhs(st, params), u, None
+
+    def transport(self, mhd):
+        if self.world == 1:
+            return "single-gpu"
+        kind = "peer memory (CUDA IPC)" if mhd.peer_transport() else "NCCL"
+        return f"y-strips x{self.world} ({kind}: 2-row halo + 4-scalar all-reduce per term)"
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup()
+    rc = maybe_spawn(args) if world == 1 else None
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
-        reference_arm(args, rank)
+        reference_arm(args, rank, world)
         return
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    job = Job(world, rank, local)
 
     import paper_2108_13622_b200 as xb
     from paper_2108_13622_b200 import _lib, leja, scenarios as sc
 
     s = sc.CONFIGS[1]()
     s.nx = s.ny = args.n
-    q = sc.initial_fields(s)
     n_cells = s.nx * s.ny
-    v_host = sc.unit_gaussian(q.size, s.extra["v_seed"]).reshape(q.shape)
     params = xb.MHDParams(mu=s.mu, eta=s.eta, kappa=s.kappa)
-    if world > 1:
-        # y-strips: rank r owns rows [y0, y0+ny_r) of the 2048^2 problem (strong scaling)
-        from paper_2108_13622_b200 import strips
-        comm = strips.Comm()
-        mhd = strips.StripMhd(xb.StateGrid(s.nx, s.ny, s.dx, s.dy, None), params, comm)
-        _ops_mod = xb.linearize._ops
-        _ops_mod.set_reducer(strips.Reducer(comm, torch.device("cuda", local)))
-        q_loc = np.ascontiguousarray(mhd.layout.local_rows(q))
-        v_loc = np.ascontiguousarray(mhd.layout.local_rows(v_host))
-    else:
-        mhd = None
-        q_loc, v_loc = q, v_host
-    u_dev = torch.from_numpy(q_loc).cuda().reshape(-1)
+    mhd, u_dev, rows = job.domain(xb, s, params)
+    v_full = sc.unit_gaussian(8 * n_cells, s.extra["v_seed"]).reshape(8, s.ny, s.nx)
+    v_loc = np.ascontiguousarray(v_full if rows is None else v_full[:, rows[0]:rows[1]])
+    del v_full
     v_dev = torch.from_numpy(v_loc).cuda().reshape(-1)
-    if mhd is None:
-        st = xb.StateGrid(s.nx, s.ny, s.dx, s.dy, u_dev.reshape(8, s.ny, s.nx))
-        mhd = xb.MhdRhs(st, params)
     op = xb.RhsOperator(mhd)
     lin = xb.FrozenLinearization(op, u_dev)
     est = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0))
@@ -354,18 +436,6 @@ def main():
             outs.append(res)
         return its, outs
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def maxed(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     # ---- device-resident timed region
     for _ in range(args.warmup):
         leja._coeff_cache.clear()
@@ -375,7 +445,7 @@ def main():
     degrees = None
     launches0 = total_launches(mhd)
     with ClockSampler(local) as clocks:
-        barrier()
+        job.barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -385,14 +455,14 @@ def main():
             iters_total += its
             degrees = [r.iterations for r in outs]
         ev1.record(stream)
-        barrier()
+        job.barrier()
     launches = total_launches(mhd) - launches0
-    ms = maxed(ev0.elapsed_time(ev1))
+    ms = job.maxed(ev0.elapsed_time(ev1))
     # every rank processes its strip of the same iterations: whole-job cell-updates
     value = iters_total * n_cells / (ms * 1e-3)
 
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
-    kern_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
+    kern_ms, kind_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
     # single domain only: in y-strip mode the stencil needs exchanged ghost rows
     stencil_ms = time_stencil_modes(_lib, lin, mhd, v_dev) if world == 1 else {}
     local_cells = u_dev.numel() // 8
@@ -400,42 +470,52 @@ def main():
     achieved = bpc * local_cells / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
 
-    # ---- end to end through the public API with pinned host buffers
-    u_pin = torch.from_numpy(q_loc.reshape(-1)).pin_memory()
-    v_pin = torch.from_numpy(v_loc.reshape(-1)).pin_memory()
+    # ---- end to end through the public API: NumPy in, NumPy out (pageable,
+    # as the reference's callers hold their arrays), and page-locked tensors
+    q_loc = np.ascontiguousarray(u_dev.reshape(8, -1, s.nx).cpu().numpy())
 
-    def e2e_step():
+    def e2e_step(u_host, v_host):
         its = 0
         leja._coeff_cache.clear()
         op_e = xb.RhsOperator(mhd)
-        lin_e = xb.FrozenLinearization(op_e, u_pin)            # H2D u, F(u)
+        lin_e = xb.FrozenLinearization(op_e, u_host)            # H2D u, F(u)
         for adt in SWEEP:
             dt = adt / alpha
-            res = xb.apply_phi_leja(1, xb.JacobianAction(lin_e), v_pin, dt,
+            res = xb.apply_phi_leja(1, xb.JacobianAction(lin_e), v_host, dt,
                                     xb.shift_and_scale(alpha * dt), LEJA_TOL)   # H2D v, D2H p
             assert isinstance(res.vector, np.ndarray)
             its += res.iterations
         return its
 
-    # warm-up of the host side too: the first steps page-lock the result buffers
-    # (torch's caching host allocator), which later steps reuse
-    for _ in range(args.warmup):
-        e2e_step()
-    e2e_iters = 0
-    barrier()
-    t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        e2e_iters += e2e_step()
-    e1.record(stream)
-    barrier()
-    e2e_ms = maxed(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)))
-    vec_bytes = 8 * q.size   # whole job: every rank moves its strip
-    e2e = {"value": e2e_iters * n_cells / (e2e_ms * 1e-3), "unit": "cell-updates/s",
-           "h2d_bytes_per_step": vec_bytes * (1 + len(SWEEP)),
-           "d2h_bytes_per_step": vec_bytes * len(SWEEP)}
+    def e2e_timed(u_host, v_host):
+        for _ in range(args.warmup):
+            e2e_step(u_host, v_host)
+        e2e_iters = 0
+        job.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_iters += e2e_step(u_host, v_host)
+        e1.record(stream)
+        job.barrier()
+        e_ms = job.maxed(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0)))
+        vec_bytes = 8 * 8 * n_cells   # whole job: every rank moves its strip
+        return {"value": e2e_iters * n_cells / (e_ms * 1e-3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": vec_bytes * (1 + len(SWEEP)),
+                "d2h_bytes_per_step": vec_bytes * len(SWEEP), "ms_per_step": e_ms / args.steps}
+
+    e2e = e2e_timed(q_loc.reshape(-1), v_loc.reshape(-1))
+    e2e["inputs"] = "pageable NumPy arrays (the reference callers' containers)"
+    e2e_pinned = e2e_timed(torch.from_numpy(q_loc.reshape(-1)).pin_memory(),
+                           torch.from_numpy(v_loc.reshape(-1)).pin_memory())
+    e2e_pinned["inputs"] = "page-locked torch host tensors"
+    del q_loc
+
+    scale = None
+    if not args.no_scale_case:
+        scale = scale_case(xb, job, args, peak)
 
     exprb = None
     if not args.no_exprb and rank == 0 and world == 1:
@@ -447,18 +527,21 @@ def main():
 
     if rank == 0:
         plan = mhd.ctx.plan()
+        kinds = None
+        if kind_ms is not None:
+            kinds = {k: {"kernel_ms": t, "bytes_per_cell": b,
+                         "achieved": b * local_cells / (t * 1e-3) / 1e9,
+                         "frac": b * local_cells / (t * 1e-3) / 1e9 / peak}
+                     for k, t, b in (("odd_PM_SKIP", kind_ms[0], 256.0),
+                                     ("even_PM_LOOK", kind_ms[1], 384.0))}
         line = {
             "metric": METRIC, "value": value, "unit": "cell-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes "
-                    "per field; v seeded unit Gaussian)",
-            "config": {"workload": workload_name(args.n),
-                       "grid": args.n, "alpha": alpha, "leja_degrees": degrees,
-                       "l2_policy": "inputs larger than L2 (268 MB per vector)",
-                       "parallelism": f"y-strips x{world} (NCCL halo + allreduce)"
-                                      if world > 1 else "single-gpu",
-                       "stencil_plan": plan},
+            "data": DATA,
+            "config": workload_config(args.n),
+            "parallelism": job.transport(mhd),
+            "workload_detail": {"alpha": alpha, "leja_degrees": degrees, "stencil_plan": plan},
             "gbs_algorithmic": value * bpc / 1e9,
             "jv_per_s": value / n_cells,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -467,6 +550,7 @@ def main():
                          "frac_at_384B": 384.0 * local_cells / (kern_ms * 1e-3) / 1e9 / peak,
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
                          "kernel_ms": kern_ms, "bytes_per_cell": bpc,
+                         "by_kind": kinds,
                          "traffic": ncu_traffic(args.n, local_cells)},
             # the other two stencil kernels of the metric's "RHS/Jv", timed the same
             # way (not in the timed step: the phi sweep runs only the fused term)
@@ -477,9 +561,12 @@ def main():
                     "cell_updates_per_s": local_cells / (t * 1e-3)}
                 for k, (t, b) in stencil_ms.items()},
             "e2e": e2e,
+            "e2e_pinned": e2e_pinned,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        if scale is not None:
+            line["scale_case"] = scale
         if exprb is not None:
             line["exprb_step"] = exprb
         if cpu is not None:
@@ -487,6 +574,79 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+SCALE_SWEEP = (1.0, 10.0, 100.0)
+
+
+def scale_case(xb, job, args, peak):
+    """north_star's strong-scaling case at every N: phi_1(dt J(u)) F(u)/||F(u)||
+    on config 4's 8192^2 Harris state (eta 1e-3), alpha*dt in {1, 10, 100}, tol
+    1e-10; y-strips over the ranks, each building only its rows and drawing only
+    its rows of the power-iteration start vector."""
+    import torch
+    from paper_2108_13622_b200 import _ops, harness, leja, scenarios as sc
+    s = sc.CONFIGS[4]()
+    s.nx = s.ny = args.scale_n
+    n_cells = s.nx * s.ny
+    params = xb.MHDParams(mu=s.mu, eta=s.eta, kappa=s.kappa)
+    t_setup = time.perf_counter()
+    mhd, u, rows = job.domain(xb, s, params)
+    op = xb.RhsOperator(mhd)
+    lin = xb.FrozenLinearization(op, u)
+    if job.world == 1:
+        rng = harness._PrefetchedNormals(0, u.numel())   # parallel exact draw
+    else:
+        rng = np.random.default_rng(0)                   # strips: local_normal_slice
+    est = xb.estimate_alpha(lin, None, rng=rng)
+    alpha = est.alpha
+    fn = _ops.norm(lin.base_rhs)
+    v = _ops.divide(lin.base_rhs, fn)
+    setup_s = time.perf_counter() - t_setup
+    matvec = xb.JacobianAction(lin)
+
+    def sweep():
+        its, degs = 0, []
+        leja._coeff_cache.clear()
+        for adt in SCALE_SWEEP:
+            dt = adt / alpha
+            res = xb.apply_phi_leja(1, matvec, v, dt, xb.shift_and_scale(alpha * dt), LEJA_TOL)
+            its += res.iterations
+            degs.append(res.iterations)
+        return its, degs
+
+    sweep()
+    steps = max(1, min(args.steps, 3))
+    stream = torch.cuda.current_stream()
+    job.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    its = 0
+    for _ in range(steps):
+        k, degs = sweep()
+        its += k
+    e1.record(stream)
+    job.barrier()
+    ms = job.maxed(e0.elapsed_time(e1))
+    value = its * n_cells / (ms * 1e-3)
+    bpc = bytes_per_cell_term(job.world)
+    per_gpu_bytes = bpc * (its * n_cells / job.world)
+    out = {"workload": f"config4 state: Harris {s.nx}^2 eta 1e-3; phi_1(dt J)F(u)/||F(u)||, "
+                       f"alpha*dt {list(SCALE_SWEEP)}, Leja tol {LEJA_TOL:g}",
+           "grid": s.nx, "n_gpus": job.world, "scaling": "strong",
+           "parallelism": job.transport(mhd), "value": value, "unit": "cell-updates/s",
+           "ms_per_step": ms / steps, "steps": steps, "leja_degrees": degs, "alpha": alpha,
+           "gbs_per_gpu_algorithmic": per_gpu_bytes / (ms * 1e-3) / 1e9,
+           "frac_per_gpu": per_gpu_bytes / (ms * 1e-3) / 1e9 / peak,
+           "setup_s": setup_s,
+           "setup": "each rank builds only its rows of the initial state and of the "
+                    "power-iteration start vector (scenarios.initial_fields(rows), "
+                    "strips.local_normal_slice)" if job.world > 1 else
+                    "whole grid on one GPU; start vector drawn on host threads"}
+    del lin, op, u, v, est
+    torch.cuda.empty_cache()
+    return out
 
 
 def time_stencil_modes(_lib, lin, mhd, v_dev, n_iter=40):
@@ -510,7 +670,9 @@ def time_stencil_modes(_lib, lin, mhd, v_dev, n_iter=40):
 
 
 def time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha, n_iter=48):
-    """Average duration of the fused Leja iteration kernel (CUDA events, same stream)."""
+    """Average duration of the fused Leja iteration kernel (CUDA events, same
+    stream), and the per-kind averages (odd PM_SKIP, even PM_LOOK terms) from
+    a second run with an event between launches."""
     import ctypes
     import torch
     from paper_2108_13622_b200 import leja
@@ -526,10 +688,18 @@ def time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha, n_iter=48):
                                        _lib.ptr(lin.base_rhs), float(lin._base_norm),
                                        _lib.ptr(v_dev), float(dt), float(sh.q), float(sh.theta),
                                        xi.ctypes.data_as(dp), coeffs.ctypes.data_as(dp),
-                                       int(n_iter), ctypes.byref(out))
+                                       int(n_iter), ctypes.byref(out), None)
+    _lib.check(rc, "xmhd_time_leja_iterations")
+    kinds = (ctypes.c_double * 2)()
+    per = ctypes.c_double()
+    rc = lib.xmhd_time_leja_iterations(mhd.ctx.bind_stream(), _lib.ptr(lin.base_state),
+                                       _lib.ptr(lin.base_rhs), float(lin._base_norm),
+                                       _lib.ptr(v_dev), float(dt), float(sh.q), float(sh.theta),
+                                       xi.ctypes.data_as(dp), coeffs.ctypes.data_as(dp),
+                                       int(n_iter), ctypes.byref(per), kinds)
     _lib.check(rc, "xmhd_time_leja_iterations")
     torch.cuda.synchronize()
-    return float(out.value)
+    return float(out.value), (float(kinds[0]), float(kinds[1]))
 
 
 def exprb_step_time(xb, with_cpu=False):

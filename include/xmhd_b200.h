@@ -307,11 +307,14 @@ int xmhd_time_stencil(xmhd_ctx* ctx, int mode, const double* u, const double* fu
 
 /* Benchmark hook: average duration (CUDA events on the context stream) of
  * n_iter back-to-back fused Leja iteration kernels with the convergence test
- * disabled (tol = 0); coeffs500 holds 500 Newton coefficients. */
+ * disabled (tol = 0); coeffs500 holds 500 Newton coefficients.  With
+ * ms_by_kind (may be NULL) an event separates every launch and
+ * ms_by_kind[0] / [1] receive the average of the odd (PM_SKIP, 256 B/cell)
+ * and even (PM_LOOK, 384 B/cell) terms of the lookahead schedule. */
 int xmhd_time_leja_iterations(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
                               const double* v, double dt, double q, double theta,
                               const double* xi, const double* coeffs500, int n_iter,
-                              double* ms_per_iter);
+                              double* ms_per_iter, double* ms_by_kind);
 
 /* ---- y-strips over peer memory (one NVLink / NVSwitch node, CUDA IPC) ----
  * Replaces the per-term halo exchange + allreduce of the strip driver (the

@@ -110,7 +110,8 @@ _SIGS = {
     "xmhd_leja_query": (_I, [_P, ctypes.POINTER(LejaState)]),
     "xmhd_leja_set_coeffs": (_I, [_P, _PD, _I]),
     "xmhd_time_stencil": (_I, [_P, _I, _P, _P, _D, _P, _P, _I, _PD]),
-    "xmhd_time_leja_iterations": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _PD, _PD, _I, _PD]),
+    "xmhd_time_leja_iterations": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _PD, _PD, _I, _PD,
+                                       _PD]),
     "xmhd_phi_divided_diffs": (_I, [_I, _PD, _I, _D, _PD]),
     "xmhd_krylov_mgs": (_I, [_P, ctypes.POINTER(_P), _I, _P, _L, _PD, _PD]),
     "xmhd_mgs_update": (_I, [_P, _P, _L, _P, _D, _P, _PD]),

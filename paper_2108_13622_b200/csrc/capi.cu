@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "kernels.h"
 #include "xmhd_b200.h"
@@ -1172,7 +1173,7 @@ int xmhd_time_stencil(xmhd_ctx* c, int mode, const double* u, const double* fu, 
 int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, double unorm,
                               const double* v, double dt, double q, double theta,
                               const double* xi, const double* coeffs500, int n_iter,
-                              double* ms_per_iter) {
+                              double* ms_per_iter, double* ms_by_kind) {
   if (!c || !u || !fu || !v || !xi || !coeffs500 || !ms_per_iter) return fail(XMHD_BADARG, "null arg");
   if (n_iter < 1 || n_iter > 400) return fail(XMHD_BADARG, "n_iter must be in [1, 400]");
   const long long n = NF * c->g.plane;
@@ -1196,16 +1197,45 @@ int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, do
   CK(cudaEventCreate(&e1));
   rc = launch_term(c, a);  // warm-up term
   if (rc) return rc;
-  CK(cudaEventRecord(e0, c->stream));
-  for (int k = 0; k < n_iter; ++k) {
-    rc = launch_term(c, a);
-    if (rc) return rc;
-  }
-  CK(cudaEventRecord(e1, c->stream));
-  CK(cudaEventSynchronize(e1));
-  c->launches += 1;
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
+  if (!ms_by_kind) {
+    CK(cudaEventRecord(e0, c->stream));
+    for (int k = 0; k < n_iter; ++k) {
+      rc = launch_term(c, a);
+      if (rc) return rc;
+    }
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+  } else {
+    // one event between consecutive launches: the average duration of each
+    // interpolant mode (lookahead: odd terms PM_SKIP, even terms PM_LOOK)
+    std::vector<cudaEvent_t> ev(n_iter + 1);
+    std::vector<int> kind(n_iter);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], c->stream));
+    for (int k = 0; k < n_iter; ++k) {
+      const int pm = c->ctl_h->defer == 2 ? leja_pmode(c->leja_next_term, 2) : PM_STORE;
+      kind[k] = pm == PM_SKIP ? 0 : 1;
+      rc = launch_term(c, a);
+      if (rc) return rc;
+      CK(cudaEventRecord(ev[k + 1], c->stream));
+    }
+    CK(cudaEventSynchronize(ev[n_iter]));
+    double sum[2] = {0.0, 0.0};
+    int cnt[2] = {0, 0};
+    for (int k = 0; k < n_iter; ++k) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+      sum[kind[k]] += t;
+      cnt[kind[k]]++;
+    }
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[n_iter]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    ms_by_kind[0] = cnt[0] ? sum[0] / cnt[0] : 0.0;
+    ms_by_kind[1] = cnt[1] ? sum[1] / cnt[1] : 0.0;
+  }
+  c->launches += 1;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   rc = sync_ctl(c);

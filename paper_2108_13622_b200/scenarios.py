@@ -58,9 +58,11 @@ class Setup:
     def dy(self):
         return (self.y_max - self.y_min) / self.ny
 
-    def centres(self):
+    def centres(self, rows=None):
+        """Cell-centre meshgrid of all rows, or of rows [y0, y1) (a y-strip)."""
+        y0, y1 = (0, self.ny) if rows is None else rows
         x = self.x_min + (np.arange(self.nx) + 0.5) * self.dx
-        y = self.y_min + (np.arange(self.ny) + 0.5) * self.dy
+        y = self.y_min + (np.arange(y0, y1) + 0.5) * self.dy
         return np.meshgrid(x, y)
 
 
@@ -85,19 +87,36 @@ CONFIGS = {
     3: lambda: kh_setup(4096, tol=1e-5, t_final=1e9, max_accepted=20, name="C3"),
     4: lambda: harris_setup(8192, eta=1e-3, tol=1e-6, t_final=1e9, max_accepted=10,
                             name="C4"),
+    # config 4's weak-scaling case: 16384^2 across 8 GPUs (17.2 GB per state vector)
+    "4w": lambda: harris_setup(16384, eta=1e-3, tol=1e-6, t_final=1e9, max_accepted=10,
+                               name="C4w"),
 }
 
 
-def kh_fields(s):
+def _noise_rows(seed, nx, y0, y1):
+    """Rows [y0, y1) of default_rng(seed).uniform(-1, 1, size=(ny, nx)): a
+    uniform double takes exactly one raw PCG64 output, so the rows start
+    y0*nx outputs into the stream (PCG64.advance) -- bitwise the same values."""
+    bg = np.random.default_rng(seed).bit_generator
+    bg.advance(y0 * nx)
+    return np.random.Generator(bg).uniform(-1.0, 1.0, size=(y1 - y0, nx))
+
+
+def kh_fields(s, rows=None):
     """Config 0: tanh shear pair, seeded vy noise in the shear envelopes."""
-    x, y = s.centres()
+    y0, y1 = (0, s.ny) if rows is None else rows
+    x, y = s.centres(rows)
+    ny = y1 - y0
     vx = 0.5 * (np.tanh((y + 0.5) / 0.05) - np.tanh((y - 0.5) / 0.05) - 1.0)
-    noise = np.random.default_rng(s.seed).uniform(-1.0, 1.0, size=(s.ny, s.nx))
+    if rows is None:
+        noise = np.random.default_rng(s.seed).uniform(-1.0, 1.0, size=(s.ny, s.nx))
+    else:
+        noise = _noise_rows(s.seed, s.nx, y0, y1)
     vy = 1e-3 * noise * np.exp(-((np.abs(y) - 0.5) / 0.1) ** 2)
-    rho = np.ones((s.ny, s.nx))
-    pres = np.ones((s.ny, s.nx))
+    rho = np.ones((ny, s.nx))
+    pres = np.ones((ny, s.nx))
     bx = 0.1
-    q = np.zeros((NFIELD, s.ny, s.nx))
+    q = np.zeros((NFIELD, ny, s.nx))
     q[RHO] = rho
     q[MX] = rho * vx
     q[MY] = rho * vy
@@ -107,15 +126,15 @@ def kh_fields(s):
     return q
 
 
-def fourier_modes(s, amplitude=1e-2, modes=16, kmax=8, seed=None):
+def fourier_modes(s, amplitude=1e-2, modes=16, kmax=8, seed=None, rows=None):
     """Seeded smooth field per conserved variable: sum of random-phase modes."""
     rng = np.random.default_rng(s.seed if seed is None else seed)
-    x, y = s.centres()
+    x, y = s.centres(rows)
     lx = s.x_max - s.x_min
     ly = s.y_max - s.y_min
     xs = (x - s.x_min) / lx
     ys = (y - s.y_min) / ly
-    out = np.zeros((NFIELD, s.ny, s.nx))
+    out = np.zeros((NFIELD,) + x.shape)
     for f in range(NFIELD):
         k = 0
         while k < modes:
@@ -128,9 +147,9 @@ def fourier_modes(s, amplitude=1e-2, modes=16, kmax=8, seed=None):
     return amplitude * out
 
 
-def harris_fields(s):
+def harris_fields(s, rows=None):
     """Config 2: double Harris sheet with a curl(psi z) flux perturbation."""
-    x, y = s.centres()
+    x, y = s.centres(rows)
     w = 0.5
     bx0 = np.tanh((y + 6.4) / w) - np.tanh((y - 6.4) / w) - 1.0
     rho = 1.0 + 1.0 / np.cosh((y + 6.4) / w) ** 2 + 1.0 / np.cosh((y - 6.4) / w) ** 2
@@ -143,7 +162,7 @@ def harris_fields(s):
     dby = psi0 * kx * np.sin(kx * x) * np.cos(ky * y)
     bx = bx0 + dbx
     by = dby
-    q = np.zeros((NFIELD, s.ny, s.nx))
+    q = np.zeros((NFIELD,) + x.shape)
     q[RHO] = rho
     q[BX] = bx
     q[BY] = by
@@ -151,14 +170,15 @@ def harris_fields(s):
     return q
 
 
-def initial_fields(s):
-    """(8, ny, nx) float64 initial conserved state of a Setup."""
+def initial_fields(s, rows=None):
+    """(8, ny, nx) float64 initial conserved state of a Setup, or only its rows
+    [y0, y1) (a y-strip builds its own rows: bitwise those of the full state)."""
     if s.kind == "kh":
-        return kh_fields(s)
+        return kh_fields(s, rows)
     if s.kind == "kh-modes":
-        return kh_fields(s) + fourier_modes(s, seed=s.extra.get("mode_seed", 1))
+        return kh_fields(s, rows) + fourier_modes(s, seed=s.extra.get("mode_seed", 1), rows=rows)
     if s.kind == "harris":
-        return harris_fields(s)
+        return harris_fields(s, rows)
     raise ValueError(f"unknown setup kind {s.kind!r}")
 
 

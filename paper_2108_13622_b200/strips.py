@@ -99,6 +99,30 @@ class Comm:
         dist.all_gather_object(objs, obj, group=self.group)
         return objs
 
+    def stream_to_root(self, planes, consume, root=0):
+        """Plane f of every rank to `root` in global order (f major, ranks in
+        order), one (field, rank) band at a time: ``consume(f, r, host_array)``
+        runs on `root` only.  Point-to-point, so `root` never holds more than
+        one band (a 16384^2 state is 17 GB; a band 268 MB at 8 ranks)."""
+        nf = len(planes)
+        if self.size == 1:
+            for f in range(nf):
+                consume(f, 0, _ops.to_host(planes[f]) if torch.is_tensor(planes[f])
+                        else np.asarray(planes[f]))
+            return
+        shapes = self.gather_host([tuple(planes[0].shape)])
+        for f in range(nf):
+            for r in range(self.size):
+                if r == root and self.rank == root:
+                    consume(f, r, _ops.to_host(planes[f]))
+                elif self.rank == root:
+                    buf = torch.empty(shapes[r][0], dtype=planes[f].dtype,
+                                      device=planes[f].device)
+                    dist.recv(buf, src=r, group=self.group)
+                    consume(f, r, _ops.to_host(buf))
+                elif self.rank == r:
+                    dist.send(planes[f].contiguous(), dst=root, group=self.group)
+
     def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
         """Send my rows 0,1 down and rows ny-2,ny-1 up; receive the neighbours' rows.
 
@@ -176,6 +200,81 @@ def global_normal_slice(rng, layout, nx):
                 flat[f, a - f * plane - lo_off:b - f * plane - lo_off] = vals[a - i0:b - i0]
 
     _normals.draw(rng, NF * plane, np.empty, sink)
+    return out.reshape(-1)
+
+
+def local_normal_slice(rng, layout, nx, comm):
+    """This rank's rows of ``rng.standard_normal(8*ny*nx)``, drawing ONLY them.
+
+    The reference draws the power-iteration start vector for the whole state
+    from the run RNG (linearize.py:113, harness.py:130); at 16384^2 that is
+    2.1 G normals (17 GB).  Here rank r draws just its 8 field segments
+    [f*plane + y0*nx, f*plane + y1*nx): each from a copy of the generator
+    advanced (PCG64.advance) to a raw position a margin before the segment's
+    expected start (NumPy's ziggurat takes one raw output per normal except on
+    a rejection, _normals.RHO), over a window long enough to contain the true
+    start.  The segments are then aligned in stream order (field-major, ranks
+    in order within a field): the 8 values that follow segment s-1 are located
+    inside segment s's draw (_normals._locate), which fixes where its exact
+    values begin.  That chain costs one tiny all-gather per segment (8 values
+    and a start position), not a full draw per rank.  A segment whose window
+    misses its start (a > 6-sigma rejection count) is redrawn from the known
+    start of the one before.  Every rank's generator ends in the state the
+    single global draw leaves it in.  Values are bit-identical to the global
+    draw (tests/test_strips_cpu.py)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2108_13622_b200 import _normals as nm
+    P, me = comm.size, comm.rank
+    bg = rng.bit_generator
+    if P == 1 or not isinstance(bg, np.random.PCG64):
+        return global_normal_slice(rng, layout, nx)
+    state0 = bg.state
+    plane = layout.ny_global * nx
+    segs = [(f, r, f * plane + layout.starts[r] * nx, layout.counts[r] * nx)
+            for f in range(NF) for r in range(P)]
+
+    def guess(start):
+        if start == 0:
+            return 0, 0
+        margin = int(6.0 * math.sqrt(start * nm.RHO_VAR)) + 2048
+        return max(0, int(start * (1.0 + nm.RHO)) - margin), 2 * margin + 4096
+
+    def draw(k):
+        _, _, start, size = segs[k]
+        g0, win = guess(start)
+        return g0, win, nm._gen_at(state0, g0).standard_normal(size + win + nm.L_MATCH)
+
+    mine = [k for k, sg in enumerate(segs) if sg[1] == me]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(mine), nm.host_threads()))) as pool:
+        futs = {k: pool.submit(draw, k) for k in mine}
+        out = np.empty((NF, layout.ny, nx))
+        flat = out.reshape(NF, -1)
+        prev = None     # (raw start, normals to skip, size, continuation) of segment k-1
+        scratch = np.empty(1 << 16)
+        for k, (f, r, start, size) in enumerate(segs):
+            info = None
+            if r == me:
+                g0, win, buf = futs.pop(k).result()
+                d = 0 if k == 0 else nm._locate(buf, win, prev[3])
+                if d is None:   # redraw from segment k-1's exact start
+                    g = nm._gen_at(state0, prev[0])
+                    nm._skip(g, prev[1] + prev[2], scratch)
+                    g.standard_normal(out=buf[:size + nm.L_MATCH])
+                    g0, d = prev[0], prev[1] + prev[2]
+                flat[f] = buf[d:d + size]
+                info = (g0, d, buf[d + size:d + size + nm.L_MATCH].copy())
+            g0, d, cont = comm.gather_host(info)[r]
+            prev = (g0, d, size, cont)
+    # the generator's state after the whole global draw, from the last segment's start
+    st = None
+    if segs[-1][1] == me:
+        g = nm._gen_at(state0, prev[0])
+        nm._skip(g, prev[1] + prev[2], np.empty(1 << 16))
+        st = g.bit_generator.state
+    st = comm.gather_host(st)[segs[-1][1]]
+    st["has_uint32"] = state0["has_uint32"]
+    st["uinteger"] = state0["uinteger"]
+    bg.state = st
     return out.reshape(-1)
 
 
@@ -487,16 +586,36 @@ def _finish(l, lin, mhd, backend, vd, v, st):
                                residual=float(st.residual))
 
 
+def _planes(local_flat, layout, nx):
+    x = local_flat.reshape(NF, layout.ny * nx)
+    return [x[f] for f in range(NF)]
+
+
 def gather_strips(local_flat, layout, nx, comm, root=0):
-    """Full (8, ny, nx) host array on `root` (None elsewhere) from every rank's strip."""
-    host = np.asarray(_ops.to_host(local_flat) if torch.is_tensor(local_flat) else local_flat)
-    host = host.reshape(NF, layout.ny, nx)
-    if comm.size == 1:
-        return host.copy()
-    objs = comm.gather_host(host)
-    if comm.rank != root:
-        return None
-    return np.concatenate(objs, axis=1)
+    """Full (8, ny, nx) host array on `root` (None elsewhere) from every rank's
+    strip, received band by band (Comm.stream_to_root; no pickled state)."""
+    full = np.empty((NF, layout.ny_global, nx)) if comm.rank == root else None
+
+    def put(f, r, band):
+        y0 = layout.starts[r]
+        full[f, y0:y0 + layout.counts[r]] = band.reshape(layout.counts[r], nx)
+
+    comm.stream_to_root(_planes(local_flat, layout, nx), put, root)
+    return full
+
+
+def strip_checksum(local_flat, layout, nx, comm, root=0):
+    """sha256 of the GLOBAL flat state (harness.py:118-119: little-endian f8 in
+    field-major order) fed band by band on `root` ("" elsewhere): the checksum
+    of a 17 GB state without assembling it anywhere."""
+    import hashlib
+    h = hashlib.sha256() if comm.rank == root else None
+
+    def put(f, r, band):
+        h.update(np.ascontiguousarray(band, dtype="<f8").tobytes())
+
+    comm.stream_to_root(_planes(local_flat, layout, nx), put, root)
+    return h.hexdigest() if h is not None else ""
 
 
 def strip_norm_check(x_local, comm):

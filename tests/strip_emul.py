@@ -62,6 +62,17 @@ class ThreadComm:
         self.sh.barrier.wait()
         return objs
 
+    def stream_to_root(self, planes, consume, root=0):
+        for f in range(len(planes)):
+            torch.cuda.current_stream().synchronize()
+            self.sh.barrier.wait()
+            self.sh.slots[self.rank] = planes[f].detach().cpu().numpy()
+            self.sh.barrier.wait()
+            if self.rank == root:
+                for r in range(self.size):
+                    consume(f, r, self.sh.slots[r])
+            self.sh.barrier.wait()
+
     def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
         torch.cuda.current_stream().synchronize()
         self.sh.slots[self.rank] = (send_lo.clone(), send_hi.clone())

@@ -25,3 +25,24 @@ def test_clock_sampler_without_gpu_is_empty():
     with bench.ClockSampler(0) as c:
         pass
     assert c.summary()["samples"] >= 0
+
+
+def test_multi_gpu_request_without_gpus_fails_loudly():
+    """`bench.py --gpus 2` must never time one GPU and report it as two: with
+    fewer visible GPUs it exits non-zero with a message."""
+    import subprocess
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(bench.__file__), "bench.py"),
+                        "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2
+    assert "refusing" in r.stderr
+    assert r.stdout.strip() == ""
+
+
+def test_both_arms_share_the_config_dict():
+    assert bench.workload_config(2048) == bench.workload_config(2048)
+    cfg = bench.workload_config(2048)
+    assert cfg["grid"] == 2048 and cfg["alpha_dt"] == list(bench.SWEEP)

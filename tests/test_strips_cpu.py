@@ -31,16 +31,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _spawn(fn, *args):
+def _spawn(fn, *args, world=WORLD):
     port = _free_port()
-    mp.spawn(_entry, args=(fn, port, args), nprocs=WORLD, join=True)
+    mp.spawn(_entry, args=(fn, port, args, world), nprocs=world, join=True)
 
 
-def _entry(rank, fn, port, args):
+def _entry(rank, fn, port, args, world=WORLD):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         fn(rank, *args)
     finally:
@@ -281,3 +281,52 @@ def test_rng_slice_parallel_draw(nranks):
         mine = strips.global_normal_slice(rng, lay, nx)
         assert np.array_equal(mine.reshape(8, lay.ny, nx), ref[:, lay.y0:lay.y0 + lay.ny])
         assert rng.bit_generator.state == full.bit_generator.state
+
+
+def _local_rng_body(rank, ny, nx, seed):
+    """Each rank draws only its rows (strips.local_normal_slice): bitwise its
+    rows of one global standard_normal, and the same final generator state."""
+    comm = strips.Comm()
+    lay = strips.StripLayout(ny, comm.size, rank)
+    rng = np.random.default_rng(seed)
+    mine = strips.local_normal_slice(rng, lay, nx, comm)
+    full = np.random.default_rng(seed)
+    ref = full.standard_normal(8 * ny * nx).reshape(8, ny, nx)
+    assert np.array_equal(mine.reshape(8, lay.ny, nx), ref[:, lay.y0:lay.y0 + lay.ny])
+    assert rng.bit_generator.state == full.bit_generator.state
+    # the stream continues identically after the draw
+    assert np.array_equal(rng.standard_normal(5), full.standard_normal(5))
+
+
+@pytest.mark.parametrize("world,ny,nx", [(2, 7, 3), (2, 515, 1024), (3, 517, 1536)])
+def test_local_rng_slice_gloo(world, ny, nx):
+    _spawn(_local_rng_body, ny, nx, 9, world=world)
+
+
+def _local_state_body(rank, world):
+    """Slice-local initial state (scenarios.initial_fields(rows)) + band-by-band
+    gather and global checksum (strips.gather_strips / strip_checksum)."""
+    import hashlib
+    from paper_2108_13622_b200 import scenarios as sc
+    comm = strips.Comm()
+    for setup in (sc.kh_setup(48), sc.harris_setup(40),
+                  sc.Setup(**{**sc.kh_setup(32).__dict__, "kind": "kh-modes",
+                              "extra": {"mode_seed": 4}})):
+        lay = strips.StripLayout(setup.ny, comm.size, rank)
+        mine = sc.initial_fields(setup, (lay.y0, lay.y0 + lay.ny))
+        full = sc.initial_fields(setup)
+        assert np.array_equal(mine, full[:, lay.y0:lay.y0 + lay.ny])
+        local = torch.from_numpy(np.ascontiguousarray(mine)).reshape(-1)
+        got = strips.gather_strips(local, lay, setup.nx, comm)
+        digest = strips.strip_checksum(local, lay, setup.nx, comm)
+        if rank == 0:
+            assert np.array_equal(got, full)
+            ref = hashlib.sha256(np.ascontiguousarray(full.reshape(-1), dtype="<f8").tobytes())
+            assert digest == ref.hexdigest()
+        else:
+            assert got is None and digest == ""
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slice_local_state_and_checksum_gloo(world):
+    _spawn(_local_state_body, world, world=world)
