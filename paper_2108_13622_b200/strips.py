@@ -587,6 +587,8 @@ def _finish(l, lin, mhd, backend, vd, v, st):
 
 
 def _planes(local_flat, layout, nx):
+    if not torch.is_tensor(local_flat):
+        local_flat = torch.from_numpy(np.ascontiguousarray(local_flat, dtype=np.float64))
     x = local_flat.reshape(NF, layout.ny * nx)
     return [x[f] for f in range(NF)]
 
