@@ -200,6 +200,7 @@ def _leja_one_call(so, ctx, u, v, dt, q, theta, tol, xi, table):
 
 
 def _rel(a, b):
+    a, b = np.ravel(a), np.ravel(b)
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 

@@ -46,6 +46,7 @@ def sha(a):
 
 
 def rel(a, b):
+    a, b = np.ravel(a), np.ravel(b)
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
