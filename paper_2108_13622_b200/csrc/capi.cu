@@ -22,6 +22,7 @@ struct xmhd_ctx {
   int device = 0;
   int nsm = 148;
   int units_x = 0, nunits = 0, seg_rows = 0, grid = 0;
+  int ws_units_x = 0, ws_nunits = 0, ws_seg_rows = 0, ws_grid = 0;   // warp-specialized plan
   int red_grid = 0;
   double* partials = nullptr;  // [red_grid*8]  (also the stencil's [grid][2])
   unsigned* tickets = nullptr; // [8]
@@ -144,6 +145,10 @@ StencilArgs base_args(xmhd_ctx* c) {
   a.units_x = c->units_x;
   a.nunits = c->nunits;
   a.seg_rows = c->seg_rows;
+  a.ws_units_x = c->ws_units_x;
+  a.ws_nunits = c->ws_nunits;
+  a.ws_seg_rows = c->ws_seg_rows;
+  a.ws_grid = c->ws_grid;
   return a;
 }
 
@@ -348,6 +353,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
     return fail(XMHD_CUDA_ERROR, std::string("device query: ") + cudaGetErrorString(e));
   }
   stencil_plan(g, c->nsm, c->units_x, c->nunits, c->seg_rows, c->grid);
+  stencil_ws_plan(g, c->nsm, c->ws_units_x, c->ws_nunits, c->ws_seg_rows, c->ws_grid);
   if (const char* seg = std::getenv("XMHD_SEG_ROWS")) {
     // testing knob: another work decomposition = another (equally valid)
     // summation order of the norm partials; used to measure the rounding floor
@@ -357,6 +363,11 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
       c->seg_rows = s;
       c->nunits = c->units_x * ((ny + s - 1) / s);
       c->grid = c->nunits < slots ? c->nunits : slots;
+      if (c->ws_grid > 0) {
+        c->ws_seg_rows = s;
+        c->ws_nunits = c->ws_units_x * ((ny + s - 1) / s);
+        c->ws_grid = c->ws_nunits < c->nsm ? c->ws_nunits : c->nsm;
+      }
     }
   }
   c->red_grid = 4 * c->nsm;
@@ -424,10 +435,11 @@ int xmhd_set_stream(xmhd_ctx* c, void* stream) {
 
 int xmhd_plan_info(xmhd_ctx* c, int* out4) {
   if (!c || !out4) return fail(XMHD_BADARG, "null arg");
-  out4[0] = c->units_x;
-  out4[1] = c->nunits;
-  out4[2] = c->seg_rows;
-  out4[3] = c->grid;
+  const bool ws = c->ws_grid > 0;   // the plan the stencil launches use
+  out4[0] = ws ? c->ws_units_x : c->units_x;
+  out4[1] = ws ? c->ws_nunits : c->nunits;
+  out4[2] = ws ? c->ws_seg_rows : c->seg_rows;
+  out4[3] = ws ? c->ws_grid : c->grid;
   return XMHD_OK;
 }
 

@@ -152,6 +152,10 @@ struct StencilArgs {
   int* bad;            // |= 1 when a non-finite F cell is produced
   double* ext_sums;    // MODE_LEJA y-strips: [sum y'^2, sum p'^2, bad] of this rank
   int units_x, nunits, seg_rows;
+  // warp-specialized TMA kernel (stencil.cu, stencil_ws_kernel): its own
+  // unit plan (1 CTA of 384 threads per SM); ws_grid == 0 selects the
+  // one-role sliding-window kernel
+  int ws_units_x, ws_nunits, ws_seg_rows, ws_grid;
   P2PArgs p2p;         // MODE_LEJA y-strips over peer memory
   PowerCtl* pctl;      // MODE_JVP inside the device power iteration (eps from here)
 };
@@ -164,6 +168,10 @@ constexpr int SW_MINB = 256 / SW;   // resident blocks per SM the register budge
 constexpr int SOUT = SW - 4;     // output columns per strip
 size_t stencil_smem_bytes();
 void stencil_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows, int& grid);
+// Plan of the warp-specialized kernel; grid = 0 when it does not apply
+// (odd nx: rows are not 16-byte aligned for the bulk copies; narrow grids).
+void stencil_ws_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows,
+                     int& grid);
 cudaError_t launch_stencil(int mode, const StencilArgs& a, int grid, cudaStream_t s);
 // One Newton term with the variant compiled for its interpolant mode (LejaPMode).
 cudaError_t launch_leja_term(const StencilArgs& a, int grid, int pmode, cudaStream_t s);

@@ -714,6 +714,530 @@ __global__ void __launch_bounds__(SW, SW_MINB) leja_loop_kernel(const StencilArg
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized sliding window with TMA-fed state rows (sm_100a).
+//
+// One CTA of 384 threads per SM, persistent over the same (strip x segment)
+// units as the one-role kernel.  Three 128-thread roles work on different
+// rows of the unit in the same "tick" and meet at ONE __syncthreads() per
+// tick, so three phase instances are in flight per SM instead of the
+// one-role kernel's two (two CTAs, each in one phase between its barriers):
+//   A (warps 0-3)   row rA = Y0-2+s: x = u + eps*y read from a 3-stage shared
+//                   ring that cp.async.bulk row copies fill (mbarrier
+//                   complete_tx; no per-thread loads, addresses or prefetch
+//                   registers), primitives -> PD ring, ideal x-fluxes -> FX
+//                   ring, the divided ideal y-flux difference of row rA-1
+//                   (two FY rows kept in registers) -> DFY ring
+//   B (warps 4-7)   row rA-2: diffusive fluxes GX -> ring, the divided GY
+//                   difference of row rA-3 (two GY rows in registers) -> DGY
+//                   ring; thread 128 issues the bulk copies two ticks ahead
+//   C (warps 8-11)  output row rA-4: x-differences of FX and GX, the DFY /
+//                   DGY terms, in the reference's association order
+//                   (mhd.py:177-178, 222-223), then the mode epilogue and the
+//                   norm partials
+// Every value comes from the same device functions and operation sequence as
+// stencil_body, so F, J w, y' and p' are bitwise the one-role kernel's; only
+// the order of the per-block norm partial sums differs.
+// Ring lifetimes (write tick -> last read tick): PD s..s+3 (4), FX s..s+4
+// (5), DFY s..s+3 (4), GX s..s+2 (3), DGY s..s+1 (2); the single barrier per
+// tick separates every write from the reads of the slot's previous row.
+constexpr int WS_ROLE = 128, WS_THREADS = 3 * WS_ROLE;
+constexpr int WR_PD = 4, WR_FX = 5, WR_DFY = 4, WR_GX = 3, WR_DGY = 2, WR_IN = 3;
+
+struct WsSmem {
+  double in[WR_IN][2][NF][WS_ROLE];   // state / direction rows (bulk-copy targets)
+  double pd[WR_PD][NPD][WS_ROLE];
+  double fx[WR_FX][NFX][WS_ROLE];
+  double dfy[WR_DFY][NFY][WS_ROLE];
+  double gx[WR_GX][NG][WS_ROLE];
+  double dgy[WR_DGY][NG][WS_ROLE];
+  unsigned long long bar[WR_IN];
+};
+
+size_t stencil_ws_smem_bytes() { return sizeof(WsSmem); }
+
+namespace {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WS_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WS_WAIT;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// One contiguous piece of a row: `bytes` from global `src` into shared `dst`,
+// completing on mbarrier `b` (cp.async.bulk: 16-byte aligned, multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+// Column pieces of a unit's 128-column window [cg0, cg0+128): position ->
+// source column, as up to three contiguous copies.  Periodic x: window
+// position t holds column (cg0+t) mod nx (the left / right wraps are their own
+// copies); reflecting x: only the in-range columns, the consumer reads the
+// mirrored position of a ghost column.
+struct WsPieces {
+  int n;
+  int src[3], dst[3], len[3];   // in columns
+};
+
+__device__ __forceinline__ WsPieces ws_pieces(int cg0, const Geom& g) {
+  WsPieces p;
+  p.n = 0;
+  const int lo = max(cg0, 0), hi = min(cg0 + WS_ROLE, g.nx);
+  if (g.bcx == BC_PERIODIC && cg0 < 0) {
+    p.src[p.n] = g.nx + cg0; p.dst[p.n] = 0; p.len[p.n] = -cg0; ++p.n;
+  }
+  if (hi > lo) { p.src[p.n] = lo; p.dst[p.n] = lo - cg0; p.len[p.n] = hi - lo; ++p.n; }
+  if (g.bcx == BC_PERIODIC && cg0 + WS_ROLE > g.nx) {
+    p.src[p.n] = 0; p.dst[p.n] = g.nx - cg0; p.len[p.n] = cg0 + WS_ROLE - g.nx; ++p.n;
+  }
+  return p;
+}
+
+}  // namespace
+
+template <int MODE, int KX, int KY, int PM>
+__global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const StencilArgs a) {
+  extern __shared__ __align__(128) unsigned char ws_raw[];
+  WsSmem& S = *reinterpret_cast<WsSmem*>(ws_raw);
+  __shared__ double red[WS_THREADS / 32];
+  __shared__ int am_last;
+  const Geom& g = a.g;
+  const int tid = threadIdx.x;
+  const int role = tid / WS_ROLE;   // 0: A, 1: B, 2: C
+  const int t = tid - role * WS_ROLE;
+  const int bid = blockIdx.x, nblk = gridDim.x;
+
+  // ---- per-launch scalars (as stencil_body)
+  double eps = a.eps;
+  Divisor epsd = a.epsd;
+  Divisor thd = epsd;
+  const double* dir = a.dir;
+  double* yout = nullptr;
+  const double* pin = nullptr;
+  double* pout = nullptr;
+  double dt = 0.0, q = 0.0, xim = 0.0, cm = 0.0, pcoef = 0.0;
+  int ppend = 0, pm_rt = PM_STORE, zero_dir = 0;
+  if (MODE == MODE_LEJA) {
+    const volatile LejaCtl* c = a.ctl;
+    if (c->status != LJ_RUNNING) return;
+    const int cur = c->cur, m = c->m;
+    eps = c->eps;
+    epsd.d = c->epsd.d; epsd.r = c->epsd.r; epsd.kind = c->epsd.kind;
+    thd.d = c->thetad.d; thd.r = c->thetad.r; thd.kind = c->thetad.kind;
+    zero_dir = c->zero_dir;
+    dir = a.ybuf[cur];
+    yout = a.ybuf[cur ^ 1];
+    const int pc = c->pcur;
+    pin = a.pbuf[pc];
+    pout = a.pbuf[pc ^ 1];
+    ppend = c->ppend;
+    pcoef = c->pend_coef;
+    pm_rt = c->pmode;
+    if (PM != PM_ANY && pm_rt != PM) {
+      if (bid == 0 && tid == 0) a.ctl->status = LJ_MODE_ERROR;
+      return;
+    }
+    dt = c->dt;
+    q = c->q;
+    xim = __ldg(a.xi + (m - 1));
+    cm = __ldg(a.coeffs + m);
+  }
+  if (MODE == MODE_JVP && a.pctl) {
+    const PowerCtl* pc = a.pctl;
+    if (pc->status != PW_RUNNING) return;
+    eps = pc->eps;
+    epsd = pc->epsd;
+  }
+  const int pmode = (PM == PM_ANY) ? pm_rt : PM;
+  const bool pread = (pmode != PM_SKIP);
+  const bool pstore = (pmode == PM_STORE || pmode == PM_LOOK);
+  const bool padd = (PM == PM_LOOK) ? true : (PM == PM_SKIP ? false : (ppend != 0));
+  const bool pnorm2 = (pmode == PM_LOOK);
+  constexpr int NV = (MODE == MODE_RHS) ? 1 : 2;   // u (and the direction) rows
+
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  int bad = 0;
+
+  if (MODE == MODE_LEJA && zero_dir) {
+    // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
+    const long long n = (long long)NF * g.plane;
+    for (long long i = (long long)bid * WS_THREADS + tid; i < n; i += (long long)nblk * WS_THREADS) {
+      const double y = __ldg(dir + i);
+      const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
+                                  __dmul_rn(xim, y));
+      yout[i] = yn;
+      double pn = 0.0;
+      if (pread) {
+        double pb = __ldg(pin + i);
+        if (padd) {
+          pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+          if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+        }
+        pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+        if (pstore) pout[i] = pn;
+      }
+      acc0 = __fma_rn(yn, yn, acc0);
+      acc1 = __fma_rn(pn, pn, acc1);
+    }
+  } else {
+    if (tid == 0) {
+      for (int k = 0; k < WR_IN; ++k) mbar_init(&S.bar[k], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned kA = 0, kP = 0;   // bulk-copy stages consumed (role A) / issued (producer)
+    const bool producer = (tid == WS_ROLE);
+    for (int unit = bid; unit < a.ws_nunits; unit += nblk) {
+      const int ux = unit % a.ws_units_x, uy = unit / a.ws_units_x;
+      const int X0 = ux * SOUT;
+      const int Y0 = uy * a.ws_seg_rows;
+      const int Y1 = min(Y0 + a.ws_seg_rows, g.ny);
+      const int nrows = Y1 - Y0;
+      const int cg0 = X0 - 2;
+      const int cgt = cg0 + t;
+      // issue the row copies of A-tick sa (row Y0-2+sa) into the next stage
+      auto issue = [&](int sa) {
+        const int slot = kP % WR_IN;
+        ++kP;
+        const RowSrc rs = row_source(Y0 - 2 + sa, g, a.u, dir, g.halo_lo_dir, g.halo_hi_dir);
+        const WsPieces pc = ws_pieces(cg0, g);
+        unsigned cols = 0;
+        for (int k = 0; k < pc.n; ++k) cols += (unsigned)pc.len[k];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&S.bar[slot], cols * 8u * (unsigned)(NF * NV));
+        for (int v = 0; v < NV; ++v) {
+          const double* base = v == 0 ? rs.u : rs.d;
+          for (int f = 0; f < NF; ++f) {
+            const double* row = base + (rs.off + (unsigned)f * rs.fs);
+            for (int k = 0; k < pc.n; ++k)
+              bulk_g2s(&S.in[slot][v][f][pc.dst[k]], row + pc.src[k], (unsigned)pc.len[k] * 8u,
+                       &S.bar[slot]);
+          }
+        }
+      };
+      // consumer-side column of window position t (reflecting x: mirrored ghosts)
+      int wpos = t, flipx = 0;
+      if (g.bcx != BC_PERIODIC) {
+        int cs;
+        col_source(cgt, g, cs, flipx);
+        wpos = min(max(cs - cg0, 0), WS_ROLE - 1);
+      }
+      const int tl = max(t - 1, 0), tr = min(t + 1, WS_ROLE - 1);
+      const int c_out = cgt;
+      const bool col_ok = (t >= 2) && (t < WS_ROLE - 2) && (c_out < g.nx);
+      double fy1[NFY], fy2[NFY], gy1[NG], gy2[NG];
+#pragma unroll
+      for (int k = 0; k < NFY; ++k) fy1[k] = fy2[k] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
+      const int nt = nrows + 6;
+      for (int s = 0; s < nt; ++s) {
+        if (producer) {
+          if (s == 0) {
+            for (int sa = 0; sa < 3 && sa <= nrows + 3; ++sa) issue(sa);
+          } else if (s + 2 <= nrows + 3) {
+            issue(s + 2);
+          }
+        }
+        if (role == 0) {
+          // ---- A: primitives and ideal fluxes of row rA = Y0-2+s
+          if (s <= nrows + 3) {
+            const int rA = Y0 - 2 + s;
+            const int slot = kA % WR_IN;
+            mbar_wait(&S.bar[slot], (kA / WR_IN) & 1u);
+            ++kA;
+            int nflip = 0;
+            if (g.bcy == BC_REFLECT) nflip = (rA < 0 || rA >= g.ny);
+            double x[NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const double uu = S.in[slot][0][f][wpos];
+              x[f] = (MODE == MODE_RHS) ? uu : __dadd_rn(uu, __dmul_rn(eps, S.in[slot][1][f][wpos]));
+            }
+            if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
+            if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+            Prim p;
+            primitives<KX == DIV_IEEE>(x, g, p);
+            double* pd = &S.pd[s % WR_PD][0][0];
+            pd[PD_VX * WS_ROLE + t] = p.vx;
+            pd[PD_VY * WS_ROLE + t] = p.vy;
+            pd[PD_VZ * WS_ROLE + t] = p.vz;
+            pd[PD_BX * WS_ROLE + t] = p.bx;
+            pd[PD_BY * WS_ROLE + t] = p.by;
+            pd[PD_BZ * WS_ROLE + t] = p.bz;
+            pd[PD_T * WS_ROLE + t] = p.temp;
+            pd[PD_B2 * WS_ROLE + t] = p.b2;
+            double fv[NFX];
+            flux_x<KX == DIV_IEEE>(p, g, fv);
+#pragma unroll
+            for (int k = 0; k < NFX; ++k) S.fx[s % WR_FX][k][t] = fv[k];
+            flux_y<KX == DIV_IEEE>(p, g, fv);
+            if (s >= 2) {
+              // -(dFY/2dy) term of output row rA-1 (mhd.py:178), divided here
+#pragma unroll
+              for (int k = 0; k < NFY; ++k)
+                S.dfy[s % WR_DFY][k][t] = qdiv<KY>(__dsub_rn(fv[k], fy2[k]), g.h2y);
+            }
+#pragma unroll
+            for (int k = 0; k < NFY; ++k) { fy2[k] = fy1[k]; fy1[k] = fv[k]; }
+          }
+        } else if (role == 1) {
+          // ---- B: diffusive fluxes of row rB = Y0-4+s
+          if (diff_on<KX>(g) && s >= 3 && s <= nrows + 4) {
+            double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
+            const int so = (s - 2) % WR_PD, sd = (s - 3) % WR_PD, su = (s - 1) % WR_PD;
+#pragma unroll
+            for (int k = 0; k < NPD; ++k) {
+              xl[k] = S.pd[so][k][tl];
+              xr[k] = S.pd[so][k][tr];
+              own[k] = S.pd[so][k][t];
+              yd[k] = S.pd[sd][k][t];
+              yu[k] = S.pd[su][k][t];
+            }
+            double gxv[NG], gyv[NG];
+            diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyv);
+#pragma unroll
+            for (int k = 0; k < NG; ++k) S.gx[s % WR_GX][k][t] = gxv[k];
+            if (s >= 5) {
+              // +dGY/2dy term of row rB-1 (mhd.py:223), divided here
+#pragma unroll
+              for (int k = 0; k < NG; ++k)
+                S.dgy[s % WR_DGY][k][t] = qdiv<KY>(__dsub_rn(gyv[k], gy2[k]), g.h2y);
+            }
+#pragma unroll
+            for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyv[k]; }
+          }
+        } else if (s >= 6 && col_ok) {
+          // ---- C: output row rC = Y0-6+s
+          const int rC = Y0 - 6 + s;
+          const unsigned plane = (unsigned)g.plane;
+          const unsigned obase = (unsigned)rC * (unsigned)g.nx + (unsigned)c_out;
+          double efu[NF], ey[NF], ep[NF];
+          if (MODE != MODE_RHS) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const unsigned i = obase + (unsigned)f * plane;
+              efu[f] = __ldg(a.fu + i);
+              if (MODE == MODE_LEJA) {
+                ey[f] = __ldg(dir + i);
+                if (pread) ep[f] = __ldg(pin + i);
+              }
+            }
+          }
+          if (MODE != MODE_RHS && rC + 1 < Y1) {
+            // L2 prefetch of the next output row's epilogue operands
+            const unsigned nb = obase + (unsigned)g.nx;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              if (((unsigned)t & 15u) == 2u) {
+                const unsigned i = nb + (unsigned)f * plane;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
+                if (MODE == MODE_LEJA) {
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
+                  if (pread) asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
+                }
+              }
+            }
+          }
+          double F[NF];
+          {
+            const int sx = (s - 4) % WR_FX;
+            double aa[NFX], bb[NFX];
+#pragma unroll
+            for (int k = 0; k < NFX; ++k) { aa[k] = S.fx[sx][k][tr]; bb[k] = S.fx[sx][k][tl]; }
+#pragma unroll
+            for (int k = 0; k < NFX; ++k)
+              F[fx_field(k)] = -qdiv<KX>(__dsub_rn(aa[k], bb[k]), g.h2x);
+          }
+          F[BX] = -0.0;
+          {
+            const int sy = (s - 3) % WR_DFY;
+#pragma unroll
+            for (int k = 0; k < NFY; ++k) {
+              const int f = fy_field(k);
+              F[f] = __dsub_rn(F[f], S.dfy[sy][k][t]);
+            }
+          }
+          F[BY] = __dsub_rn(F[BY], 0.0);
+          if (diff_on<KX>(g)) {
+            const int sgx = (s - 2) % WR_GX, sgy = (s - 1) % WR_DGY;
+            double gr[NG], gl[NG];
+#pragma unroll
+            for (int k = 0; k < NG; ++k) { gr[k] = S.gx[sgx][k][tr]; gl[k] = S.gx[sgx][k][tl]; }
+            F[RHO] = __dadd_rn(F[RHO], 0.0);
+            F[BX] = __dadd_rn(F[BX], 0.0);
+            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gr[0], gl[0]), g.h2x));
+            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gr[1], gl[1]), g.h2x));
+            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gr[2], gl[2]), g.h2x));
+            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gr[3], gl[3]), g.h2x));
+            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gr[4], gl[4]), g.h2x));
+            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gr[5], gl[5]), g.h2x));
+            F[RHO] = __dadd_rn(F[RHO], 0.0);
+            F[BY] = __dadd_rn(F[BY], 0.0);
+            F[MX] = __dadd_rn(F[MX], S.dgy[sgy][0][t]);
+            F[MY] = __dadd_rn(F[MY], S.dgy[sgy][1][t]);
+            F[MZ] = __dadd_rn(F[MZ], S.dgy[sgy][2][t]);
+            F[BX] = __dadd_rn(F[BX], S.dgy[sgy][3][t]);
+            F[BZ] = __dadd_rn(F[BZ], S.dgy[sgy][4][t]);
+            F[EN] = __dadd_rn(F[EN], S.dgy[sgy][5][t]);
+          }
+          {
+            unsigned ex = 0;
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+              ex = max(ex, (unsigned)__double2hiint(F[f]) & 0x7ff00000u);
+            bad |= (ex == 0x7ff00000u);
+          }
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            const unsigned i = obase + (unsigned)f * plane;
+            if (MODE == MODE_RHS) {
+              a.out[i] = F[f];
+            } else if (MODE == MODE_JVP) {
+              const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
+              a.out[i] = jv;
+              acc0 = __fma_rn(jv, jv, acc0);
+            } else {
+              const double w = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
+              const double y = ey[f];
+              const double yn = __dsub_rn(
+                  qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
+                  __dmul_rn(xim, y));
+              yout[i] = yn;
+              double pn = 0.0;
+              if (pread) {
+                double pb = ep[f];
+                if (padd) {
+                  pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
+                  if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
+                }
+                pn = __dadd_rn(pb, __dmul_rn(cm, yn));
+                if (pstore) pout[i] = pn;
+              }
+              acc0 = __fma_rn(yn, yn, acc0);
+              acc1 = __fma_rn(pn, pn, acc1);
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  if (bad) atomicOr(a.bad, 1);
+  if (MODE == MODE_RHS) return;
+
+  // ---- block partials and the last block's reduction / control update
+  constexpr bool NEED_S2 = (MODE == MODE_LEJA) && (PM == PM_ANY || PM == PM_LOOK);
+  const double s0 = block_sum(acc0, red);
+  const double s1 = (MODE == MODE_LEJA && PM != PM_SKIP) ? block_sum(acc1, red) : 0.0;
+  const double s2 = NEED_S2 ? block_sum(acc2, red) : 0.0;
+  if (tid == 0) {
+    a.partials[3 * bid] = s0;
+    a.partials[3 * bid + 1] = s1;
+    a.partials[3 * bid + 2] = s2;
+    __threadfence();
+    const unsigned prev = atomicAdd(a.ticket, 1u);
+    am_last = (prev == (unsigned)nblk - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (tid < 32) {
+    const double sy = sum_partials(a.partials, nblk, 3, 0);
+    const double sp = (MODE == MODE_LEJA && PM != PM_SKIP) ? sum_partials(a.partials, nblk, 3, 1)
+                                                            : 0.0;
+    const double sp2 = NEED_S2 ? sum_partials(a.partials, nblk, 3, 2) : 0.0;
+    if (tid == 0) {
+      if (MODE == MODE_JVP && a.pctl) {
+        power_after_jvp(a.pctl, sy, *((volatile int*)a.bad));
+      } else if (MODE == MODE_JVP) {
+        a.result[0] = sqrt(sy);
+      } else if (a.ext_sums) {
+        a.ext_sums[0] = sy;
+        a.ext_sums[1] = sp;
+        a.ext_sums[2] = sp2;
+        a.ext_sums[3] = *((volatile int*)a.bad) ? 1.0 : 0.0;
+      } else {
+        const int flag = *((volatile int*)a.bad);
+        leja_finalize(a.ctl, sy, sp, sp2, flag, !zero_dir, cm);
+      }
+      if (MODE == MODE_JVP) a.result[1] = sy;
+      *a.ticket = 0u;
+    }
+  }
+}
+
+// Units of the warp-specialized kernel: column strips of SOUT outputs x
+// y-segments over one persistent CTA per SM; each segment costs 6 warm-up
+// ticks (the A -> B -> C pipeline).
+void stencil_ws_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows,
+                     int& grid) {
+  units_x = nunits = seg_rows = grid = 0;
+  const char* e = std::getenv("XMHD_WS");
+  if (e && std::atoi(e) == 0) return;
+  if ((g.nx & 1) || g.nx < 2 * WS_ROLE || g.ny < 16) return;
+  units_x = (g.nx + SOUT - 1) / SOUT;
+  const int slots = nsm;
+  double best = 1e300;
+  int best_seg = g.ny;
+  for (int s = 1; s <= g.ny; ++s) {
+    const int nseg = (g.ny + s - 1) / s;
+    const long long units = (long long)units_x * nseg;
+    const long long waves = (units + slots - 1) / slots;
+    const double cost = (double)waves * (s + 6);
+    if (cost < best - 1e-9) { best = cost; best_seg = s; }
+  }
+  seg_rows = best_seg;
+  nunits = units_x * ((g.ny + seg_rows - 1) / seg_rows);
+  grid = nunits < slots ? nunits : slots;
+}
+
+namespace {
+
+template <int MODE, int KX, int KY, int PM>
+cudaError_t launch_ws_one(const StencilArgs& a, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaError_t err = cudaFuncSetAttribute(stencil_ws_kernel<MODE, KX, KY, PM>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)stencil_ws_smem_bytes());
+    if (err != cudaSuccess) return err;
+    done = true;
+  }
+  stencil_ws_kernel<MODE, KX, KY, PM><<<a.ws_grid, WS_THREADS, stencil_ws_smem_bytes(), s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
 size_t stencil_smem_bytes() {
   return sizeof(double) * (size_t)SW *
          (RING_PD * NPD + RING_FX * NFX + RING_FY * NFY + RING_GX * NG);
@@ -804,6 +1328,11 @@ cudaError_t with_div_kinds(const Geom& g, F&& f) {
 
 template <int MODE, int PM = PM_ANY>
 cudaError_t launch_mode(const StencilArgs& a, int grid, cudaStream_t s) {
+  if (a.ws_grid > 0) {   // warp-specialized TMA kernel (even nx, wide grids)
+    return with_div_kinds(a.g, [&](auto X, auto Y) {
+      return launch_ws_one<MODE, decltype(X)::value, decltype(Y)::value, PM>(a, s);
+    });
+  }
   return with_div_kinds(a.g, [&](auto X, auto Y) {
     return launch_one<MODE, decltype(X)::value, decltype(Y)::value, PM>(a, grid, s);
   });
