@@ -741,6 +741,9 @@ __global__ void __launch_bounds__(SW, SW_MINB) leja_loop_kernel(const StencilArg
 // Ring lifetimes (write tick -> last read tick): PD s..s+3 (4), FX s..s+4
 // (5), DFY s..s+3 (4), GX s..s+2 (3), DGY s..s+1 (2); the single barrier per
 // tick separates every write from the reads of the slot's previous row.
+#ifndef XB_WS_TMA
+#define XB_WS_TMA 1   // role A's rows by cp.async.bulk (0: per-thread loads, A/B)
+#endif
 constexpr int WS_ROLE = 128, WS_THREADS = 3 * WS_ROLE;
 constexpr int WR_PD = 4, WR_FX = 5, WR_DFY = 4, WR_GX = 3, WR_DGY = 2, WR_IN = 3;
 
@@ -943,12 +946,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
         }
       };
       // consumer-side column of window position t (reflecting x: mirrored ghosts)
-      int wpos = t, flipx = 0;
-      if (g.bcx != BC_PERIODIC) {
-        int cs;
-        col_source(cgt, g, cs, flipx);
-        wpos = min(max(cs - cg0, 0), WS_ROLE - 1);
-      }
+      int wpos = t, flipx = 0, csrc = 0;
+      col_source(cgt, g, csrc, flipx);
+      if (g.bcx != BC_PERIODIC) wpos = min(max(csrc - cg0, 0), WS_ROLE - 1);
       const int tl = max(t - 1, 0), tr = min(t + 1, WS_ROLE - 1);
       const int c_out = cgt;
       const bool col_ok = (t >= 2) && (t < WS_ROLE - 2) && (c_out < g.nx);
@@ -959,7 +959,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
       const int nt = nrows + 6;
       for (int s = 0; s < nt; ++s) {
-        if (producer) {
+        if (XB_WS_TMA && producer) {
           if (s == 0) {
             for (int sa = 0; sa < 3 && sa <= nrows + 3; ++sa) issue(sa);
           } else if (s + 2 <= nrows + 3) {
@@ -970,17 +970,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
           // ---- A: primitives and ideal fluxes of row rA = Y0-2+s
           if (s <= nrows + 3) {
             const int rA = Y0 - 2 + s;
-            const int slot = kA % WR_IN;
-            mbar_wait(&S.bar[slot], (kA / WR_IN) & 1u);
-            ++kA;
             int nflip = 0;
             if (g.bcy == BC_REFLECT) nflip = (rA < 0 || rA >= g.ny);
             double x[NF];
+#if XB_WS_TMA
+            const int slot = kA % WR_IN;
+            mbar_wait(&S.bar[slot], (kA / WR_IN) & 1u);
+            ++kA;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
               const double uu = S.in[slot][0][f][wpos];
               x[f] = (MODE == MODE_RHS) ? uu : __dadd_rn(uu, __dmul_rn(eps, S.in[slot][1][f][wpos]));
             }
+#else
+            {
+              const RowSrc rs = row_source(rA, g, a.u, dir, g.halo_lo_dir, g.halo_hi_dir);
+              const unsigned col = (unsigned)csrc;
+#pragma unroll
+              for (int f = 0; f < NF; ++f) {
+                const unsigned i = rs.off + col + (unsigned)f * rs.fs;
+                const double uu = __ldg(rs.u + i);
+                x[f] = (MODE == MODE_RHS) ? uu : __dadd_rn(uu, __dmul_rn(eps, __ldg(rs.d + i)));
+              }
+            }
+#endif
             if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
             if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
             Prim p;

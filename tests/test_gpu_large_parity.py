@@ -247,7 +247,8 @@ def test_c4_strips_bitwise(xb):
     # ||u|| and ||w|| on the device vs the reference's (w: exact in any order)
     from paper_2108_13622_b200 import _ops
     assert _ops.norm(wd) == meta["wnorm"]
-    assert abs(_ops.norm(u) - meta["unorm"]) <= 1e-14 * meta["unorm"]
+    # 537 M terms: the reference's sequential ddot carries ~sqrt(n) ulps
+    assert abs(_ops.norm(u) - meta["unorm"]) <= 1e-12 * meta["unorm"]
     xi = np.ascontiguousarray(leja.leja_points(500))
     coeffs = np.ascontiguousarray(leja._compute_coeffs(1, meta["q"], meta["theta"], 64))
     assert coeffs[0] == meta["c0"] and coeffs[1] == meta["c1"]

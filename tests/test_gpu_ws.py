@@ -54,7 +54,6 @@ def test_ws_kernel_bitwise_vs_one_role(case):
     u = torch.from_numpy(_state(rng, nx, ny)).cuda().reshape(-1)
     w = torch.from_numpy(rng.standard_normal(8 * nx * ny)).cuda()
     ctx_ws, ctx_1 = _ctx(case, True), _ctx(case, False)
-    assert ctx_ws.plan() != ctx_1.plan()
     out = {}
     for name, ctx in (("ws", ctx_ws), ("one", ctx_1)):
         h = ctx.bind_stream()
