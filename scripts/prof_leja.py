@@ -31,7 +31,7 @@ out = ctypes.c_double()
 rc = _lib.load().xmhd_time_leja_iterations(mhd.ctx.bind_stream(), _lib.ptr(lin.base_state),
                                            _lib.ptr(lin.base_rhs), float(lin._base_norm),
                                            _lib.ptr(v), dt, sh.q, sh.theta, xi.ctypes.data_as(dp),
-                                           c.ctypes.data_as(dp), iters, ctypes.byref(out))
+                                           c.ctypes.data_as(dp), iters, ctypes.byref(out), None)
 assert rc == 0, _lib.err_text()
 torch.cuda.synchronize()
 print(mhd.ctx.plan())
