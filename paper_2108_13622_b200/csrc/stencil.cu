@@ -1214,8 +1214,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
 void stencil_ws_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows,
                      int& grid) {
   units_x = nunits = seg_rows = grid = 0;
+  // opt-in (XMHD_WS=1): measured slower than the one-role kernel at every
+  // size (2048^2 Leja term 1.40 ms with bulk-copied rows, 0.415
+  // ms with per-thread loads, vs 0.283 ms)
   const char* e = std::getenv("XMHD_WS");
-  if (e && std::atoi(e) == 0) return;
+  if (!e || std::atoi(e) == 0) return;
   if ((g.nx & 1) || g.nx < 2 * WS_ROLE || g.ny < 16) return;
   units_x = (g.nx + SOUT - 1) / SOUT;
   const int slots = nsm;
