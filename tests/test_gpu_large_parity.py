@@ -192,9 +192,16 @@ def _run_vs(xb, meta, g, setup, scheme, max_steps=1_000_000):
     # step sizes carry the error estimates' rounding-level differences
     # (controller ratios of ~1e-7 relative errors), the accept/reject
     # sequence and the counters above do not
-    dt_dev = max(abs(a.dt - b["dt"]) / b["dt"] for a, b in zip(rep.steps, meta["steps"]))
-    record(meta["name"] + "_dt", {"max_rel_dt_deviation": dt_dev})
+    # (the last step is clipped to t_final - t and is compared through t)
+    devs = [abs(a.dt - b["dt"]) / b["dt"] for a, b in zip(rep.steps[:-1], meta["steps"][:-1])]
+    t_dev = max(abs(a.t - b["t"]) for a, b in zip(rep.steps, meta["steps"]))
+    dt_dev = max(devs) if devs else 0.0
+    record(meta["name"] + "_dt", {"max_rel_dt_deviation_before_last": dt_dev,
+                                  "argmax": int(np.argmax(devs)) if devs else None,
+                                  "max_abs_t_deviation": t_dev,
+                                  "last_dt": [rep.steps[-1].dt, meta["steps"][-1]["dt"]]})
     assert dt_dev <= 1e-6
+    assert t_dev <= 1e-10 * max(1.0, meta["t_reached"])
     assert err <= 1e-8
     assert abs(rep.t_reached - meta["t_reached"]) <= 1e-8 * max(1.0, meta["t_reached"])
 
