@@ -47,12 +47,77 @@ def is_host(x):
         isinstance(x, (list, tuple, float, int))
 
 
+class _Staging:
+    """Pageable host -> device copies through page-locked chunks.
+
+    A plain copy from pageable memory runs at ~11 GB/s on the B200 boxes
+    (the driver stages it through its own bounce buffer on one thread); here
+    host threads fill 32 MB page-locked slots while the copy engine drains the
+    previous ones on the current stream: ~28 GB/s measured
+    (scripts/probe_h2d.py).  The reference's callers hand the API plain
+    NumPy arrays, so this is the H2D of bench.py's `e2e`."""
+
+    CHUNK = 32 << 20          # bytes per slot
+    SLOTS = 4
+    MIN_BYTES = 16 << 20      # below this a plain copy is as fast
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.slots = None
+        self.events = [None] * self.SLOTS
+        self.pool = None
+        self.threads = 1
+
+    def _init(self):
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        n = self.CHUNK // 8
+        self.slots = [torch.empty(n, dtype=torch.float64, pin_memory=True)
+                      for _ in range(self.SLOTS)]
+        try:
+            cores = len(os.sched_getaffinity(0))
+        except AttributeError:   # pragma: no cover
+            cores = os.cpu_count() or 1
+        self.threads = max(1, min(8, cores // 2))
+        self.pool = ThreadPoolExecutor(self.threads, thread_name_prefix="xmhd-h2d")
+
+    def copy(self, a):
+        out = torch.empty(a.size, dtype=torch.float64, device="cuda")
+        with self.lock:
+            if self.slots is None:
+                self._init()
+            stream = torch.cuda.current_stream()
+            chunk = self.CHUNK // 8
+            flat = a.reshape(-1)
+            for k, i0 in enumerate(range(0, flat.size, chunk)):
+                m = min(chunk, flat.size - i0)
+                s = k % self.SLOTS
+                if self.events[s] is not None:
+                    self.events[s].synchronize()      # the slot's previous copy is done
+                buf = self.slots[s].numpy()
+                cut = np.linspace(0, m, self.threads + 1).astype(np.int64)
+                list(self.pool.map(
+                    lambda j: np.copyto(buf[cut[j]:cut[j + 1]], flat[i0 + cut[j]:i0 + cut[j + 1]]),
+                    range(self.threads)))
+                out[i0:i0 + m].copy_(self.slots[s][:m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self.events[s] = ev
+        return out
+
+
+_staging = _Staging()
+
+
 def as_device(x, copy=False):
     """Contiguous CUDA float64 tensor view/copy of x (numpy, list, or tensor)."""
     if torch.is_tensor(x):
         t = x
         if not t.is_cuda:
             t = t.to(dtype=torch.float64).contiguous()
+            if not t.is_pinned() and t.numel() * 8 >= _Staging.MIN_BYTES:
+                _lib.require_cuda()
+                return _staging.copy(t.numpy()).reshape(t.shape)
             t = t.to("cuda", non_blocking=t.is_pinned())
             return t
         if t.dtype != torch.float64:
@@ -61,6 +126,8 @@ def as_device(x, copy=False):
         return t.clone() if copy else t
     a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     _lib.require_cuda()
+    if a.nbytes >= _Staging.MIN_BYTES:
+        return _staging.copy(a).reshape(a.shape)
     return torch.from_numpy(a).to("cuda")
 
 

@@ -326,3 +326,22 @@ def test_prefetched_start_vector_uploaded_and_identical():
         assert torch.is_tensor(w) and w.is_cuda and w.numel() == n
         assert np.array_equal(w.cpu().numpy(), ref.standard_normal(n))
         assert np.array_equal(pre.standard_normal(9), ref.standard_normal(9))
+
+
+def test_staged_pageable_h2d_is_exact():
+    """Large pageable NumPy inputs go through the page-locked staging pipeline
+    (_ops._Staging, several 32 MB chunks, a partial last chunk): bitwise the
+    plain copy, for NumPy arrays and pageable CPU tensors, repeated calls."""
+    import numpy as np
+    import torch
+    from paper_2108_13622_b200 import _ops
+    rng = np.random.default_rng(3)
+    for n in (2 * (1 << 20) + 5, 9 * (1 << 20) + 123):
+        a = rng.standard_normal(n)
+        for _ in range(2):
+            d = _ops.as_device(a)
+            assert d.is_cuda and d.shape == a.shape
+            assert torch.equal(d.cpu(), torch.from_numpy(a))
+        t = torch.from_numpy(a[: (n // 5) * 5].reshape(-1, 5))
+        d2 = _ops.as_device(t)
+        assert d2.shape == t.shape and torch.equal(d2.cpu(), t)
