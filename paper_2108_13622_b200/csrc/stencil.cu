@@ -715,126 +715,58 @@ __global__ void __launch_bounds__(SW, SW_MINB) leja_loop_kernel(const StencilArg
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialized sliding window with TMA-fed state rows (sm_100a).
+// Two-role sliding window with a split register file (sm_100a setmaxnreg).
 //
-// One CTA of 384 threads per SM, persistent over the same (strip x segment)
-// units as the one-role kernel.  Three 128-thread roles work on different
-// rows of the unit in the same "tick" and meet at ONE __syncthreads() per
-// tick, so three phase instances are in flight per SM instead of the
-// one-role kernel's two (two CTAs, each in one phase between its barriers):
-//   A (warps 0-3)   row rA = Y0-2+s: x = u + eps*y read from a 3-stage shared
-//                   ring that cp.async.bulk row copies fill (mbarrier
-//                   complete_tx; no per-thread loads, addresses or prefetch
-//                   registers), primitives -> PD ring, ideal x-fluxes -> FX
-//                   ring, the divided ideal y-flux difference of row rA-1
-//                   (two FY rows kept in registers) -> DFY ring
-//   B (warps 4-7)   row rA-2: diffusive fluxes GX -> ring, the divided GY
-//                   difference of row rA-3 (two GY rows in registers) -> DGY
-//                   ring; thread 128 issues the bulk copies two ticks ahead
-//   C (warps 8-11)  output row rA-4: x-differences of FX and GX, the DFY /
-//                   DGY terms, in the reference's association order
-//                   (mhd.py:177-178, 222-223), then the mode epilogue and the
-//                   norm partials
-// Every value comes from the same device functions and operation sequence as
+// The one-role kernel keeps ~254 registers per column thread, so an SM holds
+// two CTAs = 8 warps and the fp64 dependency chains leave the issue slots
+// 60% idle.  Here a CTA of 256 threads splits each column's work over two
+// warpgroups that work on different rows in the same "tick" and meet at ONE
+// __syncthreads() per tick:
+//   AB (warpgroup 0, setmaxnreg 176): row r = Y0-2+s: primitives -> PD ring,
+//        ideal x-fluxes -> FX ring, the divided ideal y-flux difference of
+//        row r-1 -> DFY ring; then the diffusive fluxes of row r-1 (its own
+//        column's PD rows r-2, r-1, r in registers, the x-neighbours of row
+//        r-1 from the PD ring written last tick) -> GX ring and the divided
+//        GY difference of row r-2 -> DGY ring.  The state / direction loads
+//        of row r+1 are issued after that work, so they are in flight across
+//        the barrier without adding to the register peak.
+//   C  (warpgroup 1, setmaxnreg 80): output row r-3: x-differences of FX and
+//        GX, the DFY / DGY terms in the reference's order (mhd.py:177-178,
+//        222-223), the mode epilogue and the norm partials; its epilogue
+//        operands for the next row are likewise loaded at the end of a tick.
+// Two CTAs per SM (95 KB of rings each, 128 registers per thread at launch)
+// = 16 warps and four phase instances in flight instead of two.  Every value
+// comes from the same device functions in the same operation order as
 // stencil_body, so F, J w, y' and p' are bitwise the one-role kernel's; only
 // the order of the per-block norm partial sums differs.
-// Ring lifetimes (write tick -> last read tick): PD s..s+3 (4), FX s..s+4
-// (5), DFY s..s+3 (4), GX s..s+2 (3), DGY s..s+1 (2); the single barrier per
-// tick separates every write from the reads of the slot's previous row.
-#ifndef XB_WS_TMA
-#define XB_WS_TMA 1   // role A's rows by cp.async.bulk (0: per-thread loads, A/B)
-#endif
-constexpr int WS_ROLE = 128, WS_THREADS = 3 * WS_ROLE;
-constexpr int WR_PD = 4, WR_FX = 5, WR_DFY = 4, WR_GX = 3, WR_DGY = 2, WR_IN = 3;
+// Ring lifetimes (write tick -> read tick): PD s -> s+1 (2 slots), FX s ->
+// s+3 (4), DFY s -> s+2 (3), GX s -> s+2 (3), DGY s -> s+1 (2).
+// (Round 2 also measured a three-role variant with cp.async.bulk rows: 1.40
+// ms per 2048^2 term, commit bd8cda0.)
+constexpr int W2_ROLE = 128, W2_THREADS = 2 * W2_ROLE;
+constexpr int W2_PD = 2, W2_FX = 4, W2_DFY = 3, W2_GX = 3, W2_DGY = 2;
+constexpr int W2_REG_AB = 176, W2_REG_C = 80;
 
-struct WsSmem {
-  double in[WR_IN][2][NF][WS_ROLE];   // state / direction rows (bulk-copy targets)
-  double pd[WR_PD][NPD][WS_ROLE];
-  double fx[WR_FX][NFX][WS_ROLE];
-  double dfy[WR_DFY][NFY][WS_ROLE];
-  double gx[WR_GX][NG][WS_ROLE];
-  double dgy[WR_DGY][NG][WS_ROLE];
-  unsigned long long bar[WR_IN];
+struct Ws2Smem {
+  double pd[W2_PD][NPD][W2_ROLE];
+  double fx[W2_FX][NFX][W2_ROLE];
+  double dfy[W2_DFY][NFY][W2_ROLE];
+  double gx[W2_GX][NG][W2_ROLE];
+  double dgy[W2_DGY][NG][W2_ROLE];
 };
 
-size_t stencil_ws_smem_bytes() { return sizeof(WsSmem); }
-
-namespace {
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P;\n"
-      "WS_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      "@!P bra WS_WAIT;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-
-// One contiguous piece of a row: `bytes` from global `src` into shared `dst`,
-// completing on mbarrier `b` (cp.async.bulk: 16-byte aligned, multiple of 16).
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-
-// Column pieces of a unit's 128-column window [cg0, cg0+128): position ->
-// source column, as up to three contiguous copies.  Periodic x: window
-// position t holds column (cg0+t) mod nx (the left / right wraps are their own
-// copies); reflecting x: only the in-range columns, the consumer reads the
-// mirrored position of a ghost column.
-struct WsPieces {
-  int n;
-  int src[3], dst[3], len[3];   // in columns
-};
-
-__device__ __forceinline__ WsPieces ws_pieces(int cg0, const Geom& g) {
-  WsPieces p;
-  p.n = 0;
-  const int lo = max(cg0, 0), hi = min(cg0 + WS_ROLE, g.nx);
-  if (g.bcx == BC_PERIODIC && cg0 < 0) {
-    p.src[p.n] = g.nx + cg0; p.dst[p.n] = 0; p.len[p.n] = -cg0; ++p.n;
-  }
-  if (hi > lo) { p.src[p.n] = lo; p.dst[p.n] = lo - cg0; p.len[p.n] = hi - lo; ++p.n; }
-  if (g.bcx == BC_PERIODIC && cg0 + WS_ROLE > g.nx) {
-    p.src[p.n] = 0; p.dst[p.n] = g.nx - cg0; p.len[p.n] = cg0 + WS_ROLE - g.nx; ++p.n;
-  }
-  return p;
-}
-
-}  // namespace
+size_t stencil_ws_smem_bytes() { return sizeof(Ws2Smem); }
 
 template <int MODE, int KX, int KY, int PM>
-__global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const StencilArgs a) {
-  extern __shared__ __align__(128) unsigned char ws_raw[];
-  WsSmem& S = *reinterpret_cast<WsSmem*>(ws_raw);
-  __shared__ double red[WS_THREADS / 32];
+__global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const StencilArgs a) {
+  extern __shared__ __align__(16) unsigned char ws_raw[];
+  Ws2Smem& S = *reinterpret_cast<Ws2Smem*>(ws_raw);
+  __shared__ double red[W2_THREADS / 32];
   __shared__ int am_last;
   const Geom& g = a.g;
   const int tid = threadIdx.x;
-  const int role = tid / WS_ROLE;   // 0: A, 1: B, 2: C
-  const int t = tid - role * WS_ROLE;
+  const int role = tid / W2_ROLE;   // 0: AB, 1: C
+  const int t = tid - role * W2_ROLE;
   const int bid = blockIdx.x, nblk = gridDim.x;
 
   // ---- per-launch scalars (as stencil_body)
@@ -883,7 +815,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
   const bool pstore = (pmode == PM_STORE || pmode == PM_LOOK);
   const bool padd = (PM == PM_LOOK) ? true : (PM == PM_SKIP ? false : (ppend != 0));
   const bool pnorm2 = (pmode == PM_LOOK);
-  constexpr int NV = (MODE == MODE_RHS) ? 1 : 2;   // u (and the direction) rows
+  const unsigned plane = (unsigned)g.plane;
 
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   int bad = 0;
@@ -891,7 +823,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
   if (MODE == MODE_LEJA && zero_dir) {
     // jvp of a zero vector is exactly zero and costs no RHS call (linearize.py:63-64)
     const long long n = (long long)NF * g.plane;
-    for (long long i = (long long)bid * WS_THREADS + tid; i < n; i += (long long)nblk * WS_THREADS) {
+    for (long long i = (long long)bid * W2_THREADS + tid; i < n; i += (long long)nblk * W2_THREADS) {
       const double y = __ldg(dir + i);
       const double yn = __dsub_rn(__ddiv_rn(__dsub_rn(__dmul_rn(dt, 0.0), __dmul_rn(q, y)), thd.d),
                                   __dmul_rn(xim, y));
@@ -909,179 +841,163 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
       acc0 = __fma_rn(yn, yn, acc0);
       acc1 = __fma_rn(pn, pn, acc1);
     }
-  } else {
-    if (tid == 0) {
-      for (int k = 0; k < WR_IN; ++k) mbar_init(&S.bar[k], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    unsigned kA = 0, kP = 0;   // bulk-copy stages consumed (role A) / issued (producer)
-    const bool producer = (tid == WS_ROLE);
+  } else if (role == 0) {
+    // ================================================================ AB
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(W2_REG_AB));
+    const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
     for (int unit = bid; unit < a.ws_nunits; unit += nblk) {
       const int ux = unit % a.ws_units_x, uy = unit / a.ws_units_x;
       const int X0 = ux * SOUT;
       const int Y0 = uy * a.ws_seg_rows;
       const int Y1 = min(Y0 + a.ws_seg_rows, g.ny);
       const int nrows = Y1 - Y0;
-      const int cg0 = X0 - 2;
-      const int cgt = cg0 + t;
-      // issue the row copies of A-tick sa (row Y0-2+sa) into the next stage
-      auto issue = [&](int sa) {
-        const int slot = kP % WR_IN;
-        ++kP;
-        const RowSrc rs = row_source(Y0 - 2 + sa, g, a.u, dir, g.halo_lo_dir, g.halo_hi_dir);
-        const WsPieces pc = ws_pieces(cg0, g);
-        unsigned cols = 0;
-        for (int k = 0; k < pc.n; ++k) cols += (unsigned)pc.len[k];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&S.bar[slot], cols * 8u * (unsigned)(NF * NV));
-        for (int v = 0; v < NV; ++v) {
-          const double* base = v == 0 ? rs.u : rs.d;
-          for (int f = 0; f < NF; ++f) {
-            const double* row = base + (rs.off + (unsigned)f * rs.fs);
-            for (int k = 0; k < pc.n; ++k)
-              bulk_g2s(&S.in[slot][v][f][pc.dst[k]], row + pc.src[k], (unsigned)pc.len[k] * 8u,
-                       &S.bar[slot]);
-          }
-        }
-      };
-      // consumer-side column of window position t (reflecting x: mirrored ghosts)
-      int wpos = t, flipx = 0, csrc = 0;
-      col_source(cgt, g, csrc, flipx);
-      if (g.bcx != BC_PERIODIC) wpos = min(max(csrc - cg0, 0), WS_ROLE - 1);
-      const int tl = max(t - 1, 0), tr = min(t + 1, WS_ROLE - 1);
-      const int c_out = cgt;
-      const bool col_ok = (t >= 2) && (t < WS_ROLE - 2) && (c_out < g.nx);
-      double fy1[NFY], fy2[NFY], gy1[NG], gy2[NG];
+      int cs, flipx;
+      col_source(X0 - 2 + t, g, cs, flipx);
+      const int tl = max(t - 1, 0), tr = min(t + 1, W2_ROLE - 1);
+      double pr1[NPD], pr2[NPD], fy1[NFY], fy2[NFY], gy1[NG], gy2[NG];
+#pragma unroll
+      for (int k = 0; k < NPD; ++k) pr1[k] = pr2[k] = 0.0;
 #pragma unroll
       for (int k = 0; k < NFY; ++k) fy1[k] = fy2[k] = 0.0;
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
-      const int nt = nrows + 6;
-      for (int s = 0; s < nt; ++s) {
-        if (XB_WS_TMA && producer) {
-          if (s == 0) {
-            for (int sa = 0; sa < 3 && sa <= nrows + 3; ++sa) issue(sa);
-          } else if (s + 2 <= nrows + 3) {
-            issue(s + 2);
-          }
-        }
-        if (role == 0) {
-          // ---- A: primitives and ideal fluxes of row rA = Y0-2+s
-          if (s <= nrows + 3) {
-            const int rA = Y0 - 2 + s;
-            int nflip = 0;
-            if (g.bcy == BC_REFLECT) nflip = (rA < 0 || rA >= g.ny);
-            double x[NF];
-#if XB_WS_TMA
-            const int slot = kA % WR_IN;
-            mbar_wait(&S.bar[slot], (kA / WR_IN) & 1u);
-            ++kA;
+      // state (and direction) of the row the next tick consumes
+      double nu[NF], nd[NF];
+      int nflip;
+      {
+        const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc, g.halo_lo_dir, g.halo_hi_dir);
+        nflip = rs.flip;
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const double uu = S.in[slot][0][f][wpos];
-              x[f] = (MODE == MODE_RHS) ? uu : __dadd_rn(uu, __dmul_rn(eps, S.in[slot][1][f][wpos]));
-            }
-#else
-            {
-              const RowSrc rs = row_source(rA, g, a.u, dir, g.halo_lo_dir, g.halo_hi_dir);
-              const unsigned col = (unsigned)csrc;
+        for (int f = 0; f < NF; ++f) {
+          nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+          if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+        }
+      }
+      const int nt = nrows + 5;
+      for (int s = 0; s < nt; ++s) {
+        const int r = Y0 - 2 + s;
+        if (s <= nrows + 3) {
+          // L2 prefetch of the row loaded two ticks from now
+          if (MODE != MODE_RHS || true) {
+            const int rp = r + 2;
+            if (s + 2 <= nrows + 3 && rp >= 0 && rp < g.ny && (t & 15) == 0) {
 #pragma unroll
               for (int f = 0; f < NF; ++f) {
-                const unsigned i = rs.off + col + (unsigned)f * rs.fs;
-                const double uu = __ldg(rs.u + i);
-                x[f] = (MODE == MODE_RHS) ? uu : __dadd_rn(uu, __dmul_rn(eps, __ldg(rs.d + i)));
+                const unsigned i = (unsigned)rp * (unsigned)g.nx + (unsigned)min(max(X0 - 2 + t, 0), g.nx - 1) +
+                                   (unsigned)f * plane;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.u + i));
+                if (MODE != MODE_RHS) asm volatile("prefetch.global.L2 [%0];" ::"l"(dsrc + i));
               }
             }
-#endif
-            if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-            if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
-            Prim p;
-            primitives<KX == DIV_IEEE>(x, g, p);
-            double* pd = &S.pd[s % WR_PD][0][0];
-            pd[PD_VX * WS_ROLE + t] = p.vx;
-            pd[PD_VY * WS_ROLE + t] = p.vy;
-            pd[PD_VZ * WS_ROLE + t] = p.vz;
-            pd[PD_BX * WS_ROLE + t] = p.bx;
-            pd[PD_BY * WS_ROLE + t] = p.by;
-            pd[PD_BZ * WS_ROLE + t] = p.bz;
-            pd[PD_T * WS_ROLE + t] = p.temp;
-            pd[PD_B2 * WS_ROLE + t] = p.b2;
+          }
+          // ---- P1: row r
+          double x[NF];
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
+          if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
+          if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
+          Prim p;
+          primitives<KX == DIV_IEEE>(x, g, p);
+          double pn[NPD];
+          pn[PD_VX] = p.vx;
+          pn[PD_VY] = p.vy;
+          pn[PD_VZ] = p.vz;
+          pn[PD_BX] = p.bx;
+          pn[PD_BY] = p.by;
+          pn[PD_BZ] = p.bz;
+          pn[PD_T] = p.temp;
+          pn[PD_B2] = p.b2;
+#pragma unroll
+          for (int k = 0; k < NPD; ++k) S.pd[s % W2_PD][k][t] = pn[k];
+          {
             double fv[NFX];
             flux_x<KX == DIV_IEEE>(p, g, fv);
 #pragma unroll
-            for (int k = 0; k < NFX; ++k) S.fx[s % WR_FX][k][t] = fv[k];
+            for (int k = 0; k < NFX; ++k) S.fx[s % W2_FX][k][t] = fv[k];
             flux_y<KX == DIV_IEEE>(p, g, fv);
             if (s >= 2) {
-              // -(dFY/2dy) term of output row rA-1 (mhd.py:178), divided here
+              // -(dFY/2dy) term of row r-1 (mhd.py:178), divided here
 #pragma unroll
               for (int k = 0; k < NFY; ++k)
-                S.dfy[s % WR_DFY][k][t] = qdiv<KY>(__dsub_rn(fv[k], fy2[k]), g.h2y);
+                S.dfy[s % W2_DFY][k][t] = qdiv<KY>(__dsub_rn(fv[k], fy2[k]), g.h2y);
             }
 #pragma unroll
             for (int k = 0; k < NFY; ++k) { fy2[k] = fy1[k]; fy1[k] = fv[k]; }
           }
-        } else if (role == 1) {
-          // ---- B: diffusive fluxes of row rB = Y0-4+s
-          if (diff_on<KX>(g) && s >= 3 && s <= nrows + 4) {
-            double xl[NPD], xr[NPD], yd[NPD], yu[NPD], own[NPD];
-            const int so = (s - 2) % WR_PD, sd = (s - 3) % WR_PD, su = (s - 1) % WR_PD;
+          // ---- P2: diffusive fluxes of row r-1 (x-neighbours from last tick's PD)
+          if (diff_on<KX>(g) && s >= 2) {
+            const int sp = (s - 1) % W2_PD;
+            double xl[NPD], xr[NPD];
 #pragma unroll
             for (int k = 0; k < NPD; ++k) {
-              xl[k] = S.pd[so][k][tl];
-              xr[k] = S.pd[so][k][tr];
-              own[k] = S.pd[so][k][t];
-              yd[k] = S.pd[sd][k][t];
-              yu[k] = S.pd[su][k][t];
+              xl[k] = S.pd[sp][k][tl];
+              xr[k] = S.pd[sp][k][tr];
             }
             double gxv[NG], gyv[NG];
-            diffusive_fluxes<KX, KY>(xl, xr, yd, yu, own, g, gxv, gyv);
+            diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyv);
 #pragma unroll
-            for (int k = 0; k < NG; ++k) S.gx[s % WR_GX][k][t] = gxv[k];
-            if (s >= 5) {
-              // +dGY/2dy term of row rB-1 (mhd.py:223), divided here
+            for (int k = 0; k < NG; ++k) S.gx[s % W2_GX][k][t] = gxv[k];
+            if (s >= 4) {
+              // +dGY/2dy term of row r-2 (mhd.py:223), divided here
 #pragma unroll
               for (int k = 0; k < NG; ++k)
-                S.dgy[s % WR_DGY][k][t] = qdiv<KY>(__dsub_rn(gyv[k], gy2[k]), g.h2y);
+                S.dgy[s % W2_DGY][k][t] = qdiv<KY>(__dsub_rn(gyv[k], gy2[k]), g.h2y);
             }
 #pragma unroll
             for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyv[k]; }
           }
-        } else if (s >= 6 && col_ok) {
-          // ---- C: output row rC = Y0-6+s
-          const int rC = Y0 - 6 + s;
-          const unsigned plane = (unsigned)g.plane;
+#pragma unroll
+          for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
+          // ---- loads of row r+1, in flight across the barrier
+          if (s + 1 <= nrows + 3) {
+            const RowSrc rs = row_source(r + 1, g, a.u, dsrc, g.halo_lo_dir, g.halo_hi_dir);
+            nflip = rs.flip;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+              if (MODE != MODE_RHS) nd[f] = __ldg(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
+  } else {
+    // ================================================================ C
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(W2_REG_C));
+    for (int unit = bid; unit < a.ws_nunits; unit += nblk) {
+      const int ux = unit % a.ws_units_x, uy = unit / a.ws_units_x;
+      const int X0 = ux * SOUT;
+      const int Y0 = uy * a.ws_seg_rows;
+      const int Y1 = min(Y0 + a.ws_seg_rows, g.ny);
+      const int nrows = Y1 - Y0;
+      const int c_out = X0 - 2 + t;
+      const bool col_ok = (t >= 2) && (t < W2_ROLE - 2) && (c_out < g.nx);
+      const int tl = max(t - 1, 0), tr = min(t + 1, W2_ROLE - 1);
+      double efu[NF], ey[NF], ep[NF];
+      auto load_ops = [&](int row) {
+        const unsigned ob = (unsigned)row * (unsigned)g.nx + (unsigned)c_out;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const unsigned i = ob + (unsigned)f * plane;
+          efu[f] = __ldg(a.fu + i);
+          if (MODE == MODE_LEJA) {
+            ey[f] = __ldg(dir + i);
+            if (pread) ep[f] = __ldg(pin + i);
+          }
+        }
+      };
+      const int nt = nrows + 5;
+      for (int s = 0; s < nt; ++s) {
+        const int rC = Y0 - 5 + s;
+        if (MODE != MODE_RHS && col_ok && s == 4) load_ops(Y0);   // first output row
+        if (s >= 5 && col_ok) {
           const unsigned obase = (unsigned)rC * (unsigned)g.nx + (unsigned)c_out;
-          double efu[NF], ey[NF], ep[NF];
-          if (MODE != MODE_RHS) {
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const unsigned i = obase + (unsigned)f * plane;
-              efu[f] = __ldg(a.fu + i);
-              if (MODE == MODE_LEJA) {
-                ey[f] = __ldg(dir + i);
-                if (pread) ep[f] = __ldg(pin + i);
-              }
-            }
-          }
-          if (MODE != MODE_RHS && rC + 1 < Y1) {
-            // L2 prefetch of the next output row's epilogue operands
-            const unsigned nb = obase + (unsigned)g.nx;
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              if (((unsigned)t & 15u) == 2u) {
-                const unsigned i = nb + (unsigned)f * plane;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
-                if (MODE == MODE_LEJA) {
-                  asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
-                  if (pread) asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
-                }
-              }
-            }
-          }
           double F[NF];
           {
-            const int sx = (s - 4) % WR_FX;
+            const int sx = (s - 3) % W2_FX;
             double aa[NFX], bb[NFX];
 #pragma unroll
             for (int k = 0; k < NFX; ++k) { aa[k] = S.fx[sx][k][tr]; bb[k] = S.fx[sx][k][tl]; }
@@ -1091,7 +1007,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
           }
           F[BX] = -0.0;
           {
-            const int sy = (s - 3) % WR_DFY;
+            const int sy = (s - 2) % W2_DFY;
 #pragma unroll
             for (int k = 0; k < NFY; ++k) {
               const int f = fy_field(k);
@@ -1100,7 +1016,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
           if (diff_on<KX>(g)) {
-            const int sgx = (s - 2) % WR_GX, sgy = (s - 1) % WR_DGY;
+            const int sgx = (s - 2) % W2_GX, sgy = (s - 1) % W2_DGY;
             double gr[NG], gl[NG];
 #pragma unroll
             for (int k = 0; k < NG; ++k) { gr[k] = S.gx[sgx][k][tr]; gl[k] = S.gx[sgx][k][tl]; }
@@ -1158,10 +1074,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
               acc1 = __fma_rn(pn, pn, acc1);
             }
           }
+          // epilogue operands of the next output row, in flight across the barrier
+          if (MODE != MODE_RHS && rC + 1 < Y1) load_ops(rC + 1);
         }
         __syncthreads();
       }
     }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
   }
 
   if (bad) atomicOr(a.bad, 1);
@@ -1208,27 +1127,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1) stencil_ws_kernel(const Stencil
   }
 }
 
-// Units of the warp-specialized kernel: column strips of SOUT outputs x
-// y-segments over one persistent CTA per SM; each segment costs 6 warm-up
-// ticks (the A -> B -> C pipeline).
+// Units of the two-role kernel: column strips of SOUT outputs x y-segments
+// over two persistent CTAs per SM; a segment costs 5 warm-up ticks.
 void stencil_ws_plan(const Geom& g, int nsm, int& units_x, int& nunits, int& seg_rows,
                      int& grid) {
   units_x = nunits = seg_rows = grid = 0;
-  // opt-in (XMHD_WS=1): measured slower than the one-role kernel at every
-  // size (2048^2 Leja term 1.40 ms with bulk-copied rows, 0.415
-  // ms with per-thread loads, vs 0.283 ms)
   const char* e = std::getenv("XMHD_WS");
   if (!e || std::atoi(e) == 0) return;
-  if ((g.nx & 1) || g.nx < 2 * WS_ROLE || g.ny < 16) return;
+  if (g.nx < 2 * W2_ROLE || g.ny < 16) return;
   units_x = (g.nx + SOUT - 1) / SOUT;
-  const int slots = nsm;
+  const int slots = 2 * nsm;
   double best = 1e300;
   int best_seg = g.ny;
   for (int s = 1; s <= g.ny; ++s) {
     const int nseg = (g.ny + s - 1) / s;
     const long long units = (long long)units_x * nseg;
     const long long waves = (units + slots - 1) / slots;
-    const double cost = (double)waves * (s + 6);
+    const double cost = (double)waves * (s + 5);
     if (cost < best - 1e-9) { best = cost; best_seg = s; }
   }
   seg_rows = best_seg;
@@ -1248,7 +1163,7 @@ cudaError_t launch_ws_one(const StencilArgs& a, cudaStream_t s) {
     if (err != cudaSuccess) return err;
     done = true;
   }
-  stencil_ws_kernel<MODE, KX, KY, PM><<<a.ws_grid, WS_THREADS, stencil_ws_smem_bytes(), s>>>(a);
+  stencil_ws_kernel<MODE, KX, KY, PM><<<a.ws_grid, W2_THREADS, stencil_ws_smem_bytes(), s>>>(a);
   return cudaGetLastError();
 }
 
