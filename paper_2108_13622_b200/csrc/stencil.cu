@@ -722,35 +722,44 @@ __global__ void __launch_bounds__(SW, SW_MINB) leja_loop_kernel(const StencilArg
 // 60% idle.  Here a CTA of 256 threads splits each column's work over two
 // warpgroups that work on different rows in the same "tick" and meet at ONE
 // __syncthreads() per tick:
-//   AB (warpgroup 0, setmaxnreg 176): row r = Y0-2+s: primitives -> PD ring,
-//        ideal x-fluxes -> FX ring, the divided ideal y-flux difference of
-//        row r-1 -> DFY ring; then the diffusive fluxes of row r-1 (its own
+//   AB (warpgroup 0, setmaxnreg 160): row r = Y0-2+s: primitives -> PD ring,
+//        ideal x- and y-fluxes -> FX / FY rings; then the diffusive fluxes
+//        of row r-1 (its own
 //        column's PD rows r-2, r-1, r in registers, the x-neighbours of row
 //        r-1 from the PD ring written last tick) -> GX ring and the divided
 //        GY difference of row r-2 -> DGY ring.  The state / direction loads
 //        of row r+1 are issued after that work, so they are in flight across
 //        the barrier without adding to the register peak.
-//   C  (warpgroup 1, setmaxnreg 80): output row r-3: x-differences of FX and
-//        GX, the DFY / DGY terms in the reference's order (mhd.py:177-178,
+//   C  (warpgroup 1, setmaxnreg 96): output row r-3: x-differences of FX and
+//        GX, y-differences of FY, the DGY terms in the reference's order (mhd.py:177-178,
 //        222-223), the mode epilogue and the norm partials; its epilogue
 //        operands for the next row are likewise loaded at the end of a tick.
-// Two CTAs per SM (95 KB of rings each, 128 registers per thread at launch)
+// Two CTAs per SM (109 KB of rings each, 128 registers per thread at launch)
 // = 16 warps and four phase instances in flight instead of two.  Every value
 // comes from the same device functions in the same operation order as
 // stencil_body, so F, J w, y' and p' are bitwise the one-role kernel's; only
 // the order of the per-block norm partial sums differs.
 // Ring lifetimes (write tick -> read tick): PD s -> s+1 (2 slots), FX s ->
-// s+3 (4), DFY s -> s+2 (3), GX s -> s+2 (3), DGY s -> s+1 (2).
+// s+3 (4), FY s -> s+4 (5), GX s -> s+2 (3), DGY s -> s+1 (2).
 // (Round 2 also measured a three-role variant with cp.async.bulk rows: 1.40
 // ms per 2048^2 term, commit bd8cda0.)
 constexpr int W2_ROLE = 128, W2_THREADS = 2 * W2_ROLE;
-constexpr int W2_PD = 2, W2_FX = 4, W2_DFY = 3, W2_GX = 3, W2_DGY = 2;
-constexpr int W2_REG_AB = 176, W2_REG_C = 80;
+constexpr int W2_PD = 2, W2_FX = 4, W2_FY = 5, W2_GX = 3, W2_DGY = 2;
+#ifndef XB_W2_AB
+#define XB_W2_AB 160   // registers of warpgroup AB (C gets 256 - AB: the launch's 2 x 128)
+#endif
+#ifndef XB_W2_LOOK
+#define XB_W2_LOOK 0   // AB's offset in the terms that read p
+#endif
+// the even Leja term keeps three epilogue operand rows (F(u), y, p) in C's
+// registers across the barrier: give C 8 more there
+template <int MODE, int PM>
+__host__ __device__ constexpr int w2_reg_ab() { return (MODE == MODE_LEJA && PM != PM_SKIP) ? XB_W2_AB + XB_W2_LOOK : XB_W2_AB; }
 
 struct Ws2Smem {
   double pd[W2_PD][NPD][W2_ROLE];
   double fx[W2_FX][NFX][W2_ROLE];
-  double dfy[W2_DFY][NFY][W2_ROLE];
+  double fy[W2_FY][NFY][W2_ROLE];
   double gx[W2_GX][NG][W2_ROLE];
   double dgy[W2_DGY][NG][W2_ROLE];
 };
@@ -843,7 +852,7 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
     }
   } else if (role == 0) {
     // ================================================================ AB
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(W2_REG_AB));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(w2_reg_ab<MODE, PM>()));
     const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
     for (int unit = bid; unit < a.ws_nunits; unit += nblk) {
       const int ux = unit % a.ws_units_x, uy = unit / a.ws_units_x;
@@ -854,11 +863,11 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
       int cs, flipx;
       col_source(X0 - 2 + t, g, cs, flipx);
       const int tl = max(t - 1, 0), tr = min(t + 1, W2_ROLE - 1);
-      double pr1[NPD], pr2[NPD], fy1[NFY], fy2[NFY], gy1[NG], gy2[NG];
+      const int pf_f = (t >> 3) & 7;
+      const int pf_c = min(max(X0 - 2 + (t & 7) * 16, 0), g.nx - 1);
+      double pr1[NPD], pr2[NPD], gy1[NG], gy2[NG];
 #pragma unroll
       for (int k = 0; k < NPD; ++k) pr1[k] = pr2[k] = 0.0;
-#pragma unroll
-      for (int k = 0; k < NFY; ++k) fy1[k] = fy2[k] = 0.0;
 #pragma unroll
       for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = 0.0;
       // state (and direction) of the row the next tick consumes
@@ -877,17 +886,14 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
       for (int s = 0; s < nt; ++s) {
         const int r = Y0 - 2 + s;
         if (s <= nrows + 3) {
-          // L2 prefetch of the row loaded two ticks from now
-          if (MODE != MODE_RHS || true) {
+          // L2 prefetch of the row loaded two ticks from now: one 128-B line
+          // per thread (8 lines per field row, u then the direction)
+          {
             const int rp = r + 2;
-            if (s + 2 <= nrows + 3 && rp >= 0 && rp < g.ny && (t & 15) == 0) {
-#pragma unroll
-              for (int f = 0; f < NF; ++f) {
-                const unsigned i = (unsigned)rp * (unsigned)g.nx + (unsigned)min(max(X0 - 2 + t, 0), g.nx - 1) +
-                                   (unsigned)f * plane;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.u + i));
-                if (MODE != MODE_RHS) asm volatile("prefetch.global.L2 [%0];" ::"l"(dsrc + i));
-              }
+            if (s + 2 <= nrows + 3 && rp >= 0 && rp < g.ny && (MODE != MODE_RHS || t < 64)) {
+              const double* base = (t < 64) ? a.u : dsrc;
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                  base + ((unsigned)pf_f * plane + (unsigned)rp * (unsigned)g.nx + (unsigned)pf_c)));
             }
           }
           // ---- P1: row r
@@ -916,14 +922,8 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
 #pragma unroll
             for (int k = 0; k < NFX; ++k) S.fx[s % W2_FX][k][t] = fv[k];
             flux_y<KX == DIV_IEEE>(p, g, fv);
-            if (s >= 2) {
-              // -(dFY/2dy) term of row r-1 (mhd.py:178), divided here
 #pragma unroll
-              for (int k = 0; k < NFY; ++k)
-                S.dfy[s % W2_DFY][k][t] = qdiv<KY>(__dsub_rn(fv[k], fy2[k]), g.h2y);
-            }
-#pragma unroll
-            for (int k = 0; k < NFY; ++k) { fy2[k] = fy1[k]; fy1[k] = fv[k]; }
+            for (int k = 0; k < NFY; ++k) S.fy[s % W2_FY][k][t] = fv[k];
           }
           // ---- P2: diffusive fluxes of row r-1 (x-neighbours from last tick's PD)
           if (diff_on<KX>(g) && s >= 2) {
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
     asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
   } else {
     // ================================================================ C
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(W2_REG_C));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(256 - w2_reg_ab<MODE, PM>()));
     for (int unit = bid; unit < a.ws_nunits; unit += nblk) {
       const int ux = unit % a.ws_units_x, uy = unit / a.ws_units_x;
       const int X0 = ux * SOUT;
@@ -977,6 +977,10 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
       const bool col_ok = (t >= 2) && (t < W2_ROLE - 2) && (c_out < g.nx);
       const int tl = max(t - 1, 0), tr = min(t + 1, W2_ROLE - 1);
       double efu[NF], ey[NF], ep[NF];
+      // F(u) and y of the next output row are loaded at the end of a tick (in
+      // flight across the barrier); p, only read by the even terms, at the
+      // start of the row's own work after an L2 prefetch one tick earlier
+      // (keeps C's register peak within its share)
       auto load_ops = [&](int row) {
         const unsigned ob = (unsigned)row * (unsigned)g.nx + (unsigned)c_out;
 #pragma unroll
@@ -985,7 +989,7 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
           efu[f] = __ldg(a.fu + i);
           if (MODE == MODE_LEJA) {
             ey[f] = __ldg(dir + i);
-            if (pread) ep[f] = __ldg(pin + i);
+            if (pread && (t & 15) == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
           }
         }
       };
@@ -995,6 +999,10 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
         if (MODE != MODE_RHS && col_ok && s == 4) load_ops(Y0);   // first output row
         if (s >= 5 && col_ok) {
           const unsigned obase = (unsigned)rC * (unsigned)g.nx + (unsigned)c_out;
+          if (MODE == MODE_LEJA && pread) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) ep[f] = __ldg(pin + obase + (unsigned)f * plane);
+          }
           double F[NF];
           {
             const int sx = (s - 3) % W2_FX;
@@ -1007,11 +1015,12 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
           }
           F[BX] = -0.0;
           {
-            const int sy = (s - 2) % W2_DFY;
+            // -(dFY/2dy): FY rows rC+1 and rC-1 of this column (mhd.py:178)
+            const int s1 = (s - 2) % W2_FY, s3 = (s - 4) % W2_FY;
 #pragma unroll
             for (int k = 0; k < NFY; ++k) {
               const int f = fy_field(k);
-              F[f] = __dsub_rn(F[f], S.dfy[sy][k][t]);
+              F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(S.fy[s1][k][t], S.fy[s3][k][t]), g.h2y));
             }
           }
           F[BY] = __dsub_rn(F[BY], 0.0);
