@@ -981,21 +981,34 @@ __global__ void __launch_bounds__(W2_THREADS, 2) stencil_ws_kernel(const Stencil
       // flight across the barrier); p, only read by the even terms, at the
       // start of the row's own work after an L2 prefetch one tick earlier
       // (keeps C's register peak within its share)
+      // L2 prefetch of an output row's epilogue operands (two ticks ahead):
+      // one 128-B line per thread, 8 lines per field row
+      const int pf_f = (t >> 3) & 7;
+      const int pf_c = min(max(X0 + (t & 7) * 16, 0), g.nx - 1);
+      auto prefetch_ops = [&](int row) {
+        if (MODE == MODE_RHS || row < 0 || row >= Y1) return;
+        const unsigned i = (unsigned)row * (unsigned)g.nx + (unsigned)pf_c + (unsigned)pf_f * plane;
+        if (t < 64) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.fu + i));
+        } else if (MODE == MODE_LEJA) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dir + i));
+        }
+        if (MODE == MODE_LEJA && pread && t < 64)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
+      };
       auto load_ops = [&](int row) {
         const unsigned ob = (unsigned)row * (unsigned)g.nx + (unsigned)c_out;
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
           const unsigned i = ob + (unsigned)f * plane;
           efu[f] = __ldg(a.fu + i);
-          if (MODE == MODE_LEJA) {
-            ey[f] = __ldg(dir + i);
-            if (pread && (t & 15) == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(pin + i));
-          }
+          if (MODE == MODE_LEJA) ey[f] = __ldg(dir + i);
         }
       };
       const int nt = nrows + 5;
       for (int s = 0; s < nt; ++s) {
         const int rC = Y0 - 5 + s;
+        if (s >= 2) prefetch_ops(rC + 2);
         if (MODE != MODE_RHS && col_ok && s == 4) load_ops(Y0);   // first output row
         if (s >= 5 && col_ok) {
           const unsigned obase = (unsigned)rC * (unsigned)g.nx + (unsigned)c_out;
