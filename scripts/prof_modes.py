@@ -34,8 +34,9 @@ with torch.profiler.profile(activities=acts) as prof:
     torch.cuda.synchronize()
 dur = {}
 for e in prof.events():
-    if e.device_type == torch.autograd.DeviceType.CUDA and "stencil_kernel" in e.name:
-        key = "RHS" if "stencil_kernel<0" in e.name else ("JVP" if "stencil_kernel<1" in e.name else e.name)
+    if e.device_type == torch.autograd.DeviceType.CUDA and "stencil" in e.name and "kernel<" in e.name:
+        mode = e.name.split("kernel<", 1)[1][:1]
+        key = "RHS" if mode == "0" else ("JVP" if mode == "1" else e.name)
         dur.setdefault(key, []).append(e.time_range.end - e.time_range.start)
 cells = n * n
 peak = 6529.7
