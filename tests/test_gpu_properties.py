@@ -46,7 +46,7 @@ def _build(n, kind):
     return xb, s, u, mhd
 
 
-@pytest.mark.parametrize("n,kind", [(8192, "harris"), (2048, "kh")])
+@pytest.mark.parametrize("n,kind", [(2048, "kh"), (8192, "harris")])
 def test_rhs_translation_equivariance_full_size(n, kind):
     xb, s, u, mhd = _setup(n, kind)
     f = mhd(u.reshape(-1)).reshape(u.shape)
@@ -56,7 +56,7 @@ def test_rhs_translation_equivariance_full_size(n, kind):
         assert torch.equal(fr, torch.roll(f, shifts=(dy, dx), dims=(1, 2))), (dy, dx)
 
 
-@pytest.mark.parametrize("n,kind", [(2048, "kh"), (8192, "harris")])
+@pytest.mark.parametrize("n,kind", [(8192, "harris"), (2048, "kh")])
 def test_jvp_power_of_two_homogeneity_full_size(n, kind):
     xb, s, u, mhd = _setup(n, kind)
     lin = xb.FrozenLinearization(xb.RhsOperator(mhd), u.reshape(-1))
