@@ -517,9 +517,10 @@ def main():
     if not args.no_scale_case:
         scale = scale_case(xb, job, args, peak)
 
-    exprb = None
+    exprb = exprb_c2 = None
     if not args.no_exprb and rank == 0 and world == 1:
         exprb = exprb_step_time(xb, with_cpu=not args.no_cpu_baseline)
+        exprb_c2 = exprb_step_time_c2(xb, with_cpu=not args.no_cpu_baseline)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -569,6 +570,8 @@ def main():
             line["scale_case"] = scale
         if exprb is not None:
             line["exprb_step"] = exprb
+        if exprb_c2 is not None:
+            line["exprb_step_c2"] = exprb_c2
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -719,6 +722,39 @@ def exprb_step_time(xb, with_cpu=False):
            "wall_s": wall, "wall_s_per_step": wall / max(rep.accepted, 1)}
     if with_cpu:
         out["cpu_baseline"] = exprb_cpu_time(setup)
+    return out
+
+
+def exprb_step_time_c2(xb, with_cpu=False):
+    """Config 2 (double Harris 512^2, EXPRB54s4, tol 1e-6, t_end 10): wall-s
+    per accepted step over the whole run; the CPU side is the oracle's first
+    step (a bounded sample: the whole reference run takes ~47 min)."""
+    from paper_2108_13622_b200 import leja, scenarios as sc
+    import torch
+    setup = sc.CONFIGS[2]()
+    xb.run(xb.RunConfig(scenario=sc.harris_setup(512, t_final=0.05), scheme=xb.Scheme.EXPRB54S4,
+                        tol=setup.tol))   # warm
+    leja._coeff_cache.clear()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = xb.run(xb.RunConfig(scenario=setup, scheme=xb.Scheme.EXPRB54S4, tol=setup.tol))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"config": "config2 Harris 512^2 EXPRB54s4 tol 1e-6 t_end 10",
+           "accepted": rep.accepted, "rejected": rep.rejected, "rhs_evals": rep.rhs_evals,
+           "wall_s": wall, "wall_s_per_step": wall / max(rep.accepted, 1)}
+    if with_cpu:
+        from oracle import steppers_np as ost
+        q = sc.initial_fields(setup)
+        t0 = time.perf_counter()
+        crep = ost.run(q, setup.dx, setup.dy, setup.mu, setup.eta, setup.kappa, "exprb54s4",
+                       setup.tol, setup.t_final, max_accepted=1)
+        cw = time.perf_counter() - t0
+        out["cpu_baseline"] = {"kind": "port", "accepted": crep.accepted,
+                               "rhs_evals": crep.rhs_evals, "wall_s": cw,
+                               "wall_s_per_step": cw / max(crep.accepted, 1),
+                               "sample": "the first step of the same run (incl. its spectral "
+                                         "estimate) through the NumPy oracle"}
     return out
 
 
