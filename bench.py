@@ -97,8 +97,8 @@ def maybe_spawn(args):
 
 def ncu_traffic(n, local_cells):
     """DRAM bytes per launch of the fused kernel from the committed ncu capture
-    (profiles/r01_leja_traffic.json), when it was taken on this grid and layout."""
-    path = os.path.join(REPO, "profiles", "r01_leja_traffic.json")
+    (profiles/r02_leja_traffic.json), when it was taken on this grid and layout."""
+    path = os.path.join(REPO, "profiles", "r02_leja_traffic.json")
     try:
         rec = json.load(open(path))
     except (OSError, ValueError):
