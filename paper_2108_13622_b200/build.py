@@ -47,21 +47,47 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_so(force=False, verbose=False, extra=()):
-    """Compile the C-ABI library if any source is newer than the .so."""
-    if not force and not _stale():
-        return SO_PATH
-    cmd = [nvcc()] + NVCC_FLAGS + list(extra) + ["-I", INCLUDE, "-I", CSRC, "-o", SO_PATH]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
+def build_so(force=False, verbose=False, extra=(), out=None):
+    """Compile the C-ABI library if any source is newer than the .so.
+
+    Each source compiles to an object in parallel (the translation units only
+    share host-linkage launch functions), then nvcc links the shared library."""
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    out = out or SO_PATH
+    if not force and out == SO_PATH and not _stale():
+        return out
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    tmp = tempfile.mkdtemp(prefix="xmhd_build_")
+
+    def compile_one(src):
+        obj = os.path.join(tmp, os.path.basename(src) + ".o")
+        cmd = [nvcc()] + compile_flags + list(extra) + ["-I", INCLUDE, "-I", CSRC, "-c",
+                                                        os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    for _, res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building %s" % SO_NAME)
+        if verbose and (res.stdout or res.stderr):
+            print(res.stdout + res.stderr)
+    link = [nvcc(), "-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a",
+            "-Xcompiler", "-fPIC", "-o", out] + [obj for obj, _ in results]
     if verbose:
-        print(" ".join(cmd), flush=True)
-    res = subprocess.run(cmd, capture_output=True, text=True)
+        print(" ".join(link), flush=True)
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building %s" % SO_NAME)
-    if verbose and (res.stdout or res.stderr):
-        print(res.stdout + res.stderr)
-    return SO_PATH
+        raise RuntimeError("nvcc failed linking %s" % SO_NAME)
+    for obj, _ in results:
+        os.remove(obj)
+    os.rmdir(tmp)
+    return out
 
 
 if __name__ == "__main__":
