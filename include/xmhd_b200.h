@@ -110,6 +110,14 @@ int xmhd_rhs(xmhd_ctx* ctx, const double* u, double* f, int* bad_cells);
 int xmhd_jvp(xmhd_ctx* ctx, const double* u, const double* fu, double unorm, const double* w,
              double* out, int* called, double* out_norm, int* bad_cells);
 
+/* The tail of _stage_difference (integrators.py:146-153) in one stencil pass:
+ * out = (fstage - fu) - jvp(d) with d = stage - u and dnorm = ||d|| as reduced by
+ * xmhd_lincomb_diff (same bits as xmhd_norm(d)); fstage = F(stage) from xmhd_rhs.
+ * Counters and the non-finite contract are xmhd_jvp's. */
+int xmhd_stage_difference(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                          const double* d, double dnorm, const double* fstage, double* out,
+                          int* called, int* bad_cells);
+
 /* apply_phi_leja (leja.py:103-150) for the frozen MHD Jacobian in ONE call:
  * p_out = phi_l(dt J(u)) v by Newton interpolation at the Leja points xi[500]
  * on [q - 2 theta, q + 2 theta], the whole loop on the device.  `coeffs` holds
@@ -157,6 +165,22 @@ int xmhd_set_loop_kind(xmhd_ctx* ctx, int kind);
  * reference's order (same bits): 320 instead of 384 B/cell per term.  A call
  * that converged on the odd term discards the even one (not counted). */
 int xmhd_set_leja_defer(xmhd_ctx* ctx, int on);
+/* xmhd_leja_start_async with an in-place start, for calls run by per-term
+ * launches (xmhd_leja_launch; not xmhd_leja_loop): nothing is copied -- the
+ * first term reads v where it lies (leja.py:121 `y = v`) and the interpolant
+ * c0*v (leja.py:123) is formed by the first term that reads it; v must stay
+ * untouched until the call's result has been taken.  Same bits, two vector
+ * passes less per call.  (xmhd_leja and xmhd_leja_start start in place
+ * themselves when they run per-term launches.) */
+int xmhd_leja_start_inplace(xmhd_ctx* ctx, const double* u, const double* fu, double unorm,
+                            const double* v, double dt, double q, double theta, double tol,
+                            const double* xi, const double* coeffs, int ncoef);
+/* Caller-owned interpolant buffers (two distinct vectors, or two NULLs to return
+ * to the context's own) for the following single-domain calls; with them
+ * xmhd_leja_result_inplace hands the result back in buffer *which (0 / 1)
+ * without a copy when the last term stored it, else after one p + c*y pass. */
+int xmhd_leja_set_pbuf(xmhd_ctx* ctx, double* p0, double* p1);
+int xmhd_leja_result_inplace(xmhd_ctx* ctx, int* which);
 int xmhd_leja_finish_async(xmhd_ctx* ctx, double* p_out);
 int xmhd_lincomb_async(xmhd_ctx* ctx, double* out, long long n, const double* const* v,
                        const double* coeffs, int nterms);
@@ -215,6 +239,16 @@ int xmhd_norm(xmhd_ctx* ctx, const double* x, long long n, double* out);
  * norm_out / nonfinite_out may be NULL (then no reduction is performed). */
 int xmhd_lincomb(xmhd_ctx* ctx, double* out, long long n, const double* const* v,
                  const double* c, int nterms, double* norm_out, int* nonfinite_out);
+/* A stage vector and its offset from the base state in one pass
+ * (integrators.py:139-153): out = the combination above with v[0] = u, c[0] = 1;
+ * diff = out - v[0]; *diff_norm = ||diff||. */
+int xmhd_lincomb_diff(xmhd_ctx* ctx, double* out, double* diff, long long n,
+                      const double* const* v, const double* c, int nterms, double* diff_norm);
+/* nout (2..4) combinations of the same three vectors in one pass (the w_k of
+ * integrators.py:166-167, 186-189): out[j] = sum_k coef[3j+k]*v[k], k in order,
+ * zero coefficients skipped (a term the reference's expression does not have). */
+int xmhd_lincomb_multi(xmhd_ctx* ctx, double* const* out, int nout, long long n,
+                       const double* const* v, const double* coef);
 
 /* out = x / d elementwise (IEEE), optionally ||out|| (w/||w||, jw/mag, v/l!). */
 int xmhd_divide(xmhd_ctx* ctx, double* out, const double* x, double d, long long n,
@@ -384,6 +418,15 @@ int xmhd_newton_coeffs(int l, double q, double theta, const double* xi, int coun
  * schedule of leja.py:119-130 (64 -> 128 -> 256 -> 500, each chunk recomputed):
  * entries [0,64) of the 64-chunk, [64,128) of the 128-chunk, ... (host). */
 int xmhd_leja_schedule(int l, double q, double theta, const double* xi, double* out500);
+
+/* Pageable host memory -> device, the H2D of a reference caller's NumPy array
+ * (the reference's API takes host arrays: leja.py:103, linearize.py:46-53).
+ * A persistent pool of host threads (xmhd_h2d_threads; env XMHD_H2D_THREADS)
+ * fills page-locked slots while the copy engine drains the ones filled before,
+ * in `stream` order.  Returns once src_host is no longer read; the device copy
+ * completes in stream order.  No context: one staging area per process. */
+int xmhd_h2d_staged(void* dst_dev, const void* src_host, long long bytes, void* stream);
+int xmhd_h2d_threads(void);
 
 #ifdef __cplusplus
 }

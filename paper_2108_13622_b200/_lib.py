@@ -131,6 +131,14 @@ _SIGS = {
                                       ctypes.POINTER(_P), _D, ctypes.POINTER(_P), _D, _D, _D,
                                       _D, _PD, _PD, _I]),
     "xmhd_leja_p2p_emul_run": (_I, [ctypes.POINTER(_P), _I, ctypes.POINTER(LejaState)]),
+    "xmhd_leja_start_inplace": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I]),
+    "xmhd_leja_set_pbuf": (_I, [_P, _P, _P]),
+    "xmhd_leja_result_inplace": (_I, [_P, _PI]),
+    "xmhd_stage_difference": (_I, [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI]),
+    "xmhd_lincomb_diff": (_I, [_P, _P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD]),
+    "xmhd_lincomb_multi": (_I, [_P, ctypes.POINTER(_P), _I, _L, ctypes.POINTER(_P), _PD]),
+    "xmhd_h2d_staged": (_I, [_P, _P, _L, _P]),
+    "xmhd_h2d_threads": (_I, []),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -7,6 +7,7 @@ reductions.
 
 import ctypes
 import math
+import os
 import threading
 
 import numpy as np
@@ -51,13 +52,15 @@ class _Staging:
     """Pageable host -> device copies through page-locked chunks.
 
     A plain copy from pageable memory runs at ~11 GB/s on the B200 boxes
-    (the driver stages it through its own bounce buffer on one thread); here
-    host threads fill 32 MB page-locked slots while the copy engine drains the
-    previous ones on the current stream: ~28 GB/s measured
-    (scripts/probe_h2d.py).  The reference's callers hand the API plain
-    NumPy arrays, so this is the H2D of bench.py's `e2e`."""
+    (the driver stages it through its own bounce buffer on one thread).  The
+    native ``xmhd_h2d_staged`` (csrc/hostio.cpp) keeps a persistent pool of
+    host threads filling page-locked slots with streaming stores while the
+    copy engine drains the previous ones on the current stream.  The
+    reference's callers hand the API plain NumPy arrays, so this is the H2D of
+    bench.py's ``e2e``.  (XMHD_H2D_PY=1: the same pipeline issued from Python,
+    28 GB/s; kept for A/B, scripts/probe_h2d.py.)"""
 
-    CHUNK = 32 << 20          # bytes per slot
+    CHUNK = 32 << 20          # bytes per slot (Python pipeline)
     SLOTS = 4
     MIN_BYTES = 16 << 20      # below this a plain copy is as fast
 
@@ -67,9 +70,9 @@ class _Staging:
         self.events = [None] * self.SLOTS
         self.pool = None
         self.threads = 1
+        self.python = bool(int(os.environ.get("XMHD_H2D_PY", "0") or "0"))
 
     def _init(self):
-        import os
         from concurrent.futures import ThreadPoolExecutor
         n = self.CHUNK // 8
         self.slots = [torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -83,6 +86,13 @@ class _Staging:
 
     def copy(self, a):
         out = torch.empty(a.size, dtype=torch.float64, device="cuda")
+        if not self.python:
+            flat = a.reshape(-1)
+            rc = _lib.load().xmhd_h2d_staged(ctypes.c_void_p(out.data_ptr()),
+                                             ctypes.c_void_p(flat.ctypes.data), flat.nbytes,
+                                             _lib.current_stream_handle())
+            _lib.check(rc, "xmhd_h2d_staged")
+            return out
         with self.lock:
             if self.slots is None:
                 self._init()
@@ -226,6 +236,38 @@ def lincomb(coeffs, vecs, out=None, want_norm=False, ctx=None):
     rc = lib.xmhd_lincomb(_h(ctx), _lib.ptr(out), n, arr, cs, len(vecs), None, None)
     _lib.check(rc, "xmhd_lincomb")
     return out
+
+
+def lincomb_diff(coeffs, vecs, ctx=None):
+    """(out, out - vecs[0], ||out - vecs[0]||) in one pass: a stage vector
+    u + sum c_k p_k and the direction stage - u of its stage difference
+    (integrators.py:139-153).  Single domain only (the norm is local)."""
+    assert 2 <= len(vecs) == len(coeffs) <= 4 and reducer() is None
+    lib = _lib.load()
+    out = torch.empty_like(vecs[0])
+    diff = torch.empty_like(vecs[0])
+    arr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(v.data_ptr()) for v in vecs])
+    cs = (ctypes.c_double * 4)(*[float(c) for c in coeffs])
+    nrm = ctypes.c_double()
+    rc = lib.xmhd_lincomb_diff(_h(ctx), _lib.ptr(out), _lib.ptr(diff), out.numel(), arr, cs,
+                               len(vecs), ctypes.byref(nrm))
+    _lib.check(rc, "xmhd_lincomb_diff")
+    return out, diff, float(nrm.value)
+
+
+def lincomb_multi(rows, vecs, ctx=None):
+    """[sum_k rows[j][k] * vecs[k] for j] (k in order, zero coefficients skipped)
+    for 2-4 combinations of the same three vectors, in one pass."""
+    assert len(vecs) == 3 and 2 <= len(rows) <= 4
+    lib = _lib.load()
+    outs = [torch.empty_like(vecs[0]) for _ in rows]
+    oarr = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(o.data_ptr()) for o in outs])
+    varr = (ctypes.c_void_p * 3)(*[ctypes.c_void_p(v.data_ptr()) for v in vecs])
+    flat = [float(c) for row in rows for c in row]
+    cs = (ctypes.c_double * 12)(*(flat + [0.0] * (12 - len(flat))))
+    rc = lib.xmhd_lincomb_multi(_h(ctx), oarr, len(rows), vecs[0].numel(), varr, cs)
+    _lib.check(rc, "xmhd_lincomb_multi")
+    return outs
 
 
 def divide(x, d, out=None, want_norm=False, ctx=None):

@@ -15,7 +15,7 @@ INCLUDE = os.path.join(REPO, "include")
 SO_NAME = "_xmhd_b200.so"
 SO_PATH = os.path.join(PKG, SO_NAME)
 
-SOURCES = ["stencil.cu", "vec.cu", "capi.cu", "divdiff.cpp", "steps.cpp"]
+SOURCES = ["stencil.cu", "vec.cu", "capi.cu", "divdiff.cpp", "steps.cpp", "hostio.cpp"]
 HEADERS = ["common.cuh", "kernels.h"]
 
 NVCC_FLAGS = [

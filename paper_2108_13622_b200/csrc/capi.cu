@@ -40,6 +40,12 @@ struct xmhd_ctx {
   long long gen_n = 0;         // vector length of the current generic Leja call
   const double* leja_u = nullptr;
   const double* leja_fu = nullptr;
+  // in-place start of the host-paced per-term path (xmhd_leja_start_inplace):
+  // the call's v is read where it lies, nothing is copied at the start
+  const double* leja_v0 = nullptr;   // v of the current in-place call
+  // caller-owned interpolant buffers (xmhd_leja_set_pbuf): the result is handed
+  // back in one of them (xmhd_leja_result_inplace) instead of being copied out
+  double* pbuf_ext[2] = {nullptr, nullptr};
   // y-strips over peer memory (P2PArgs): own region [ghost rows x 2 parities,
   // board, flags], the peers' regions mapped through CUDA IPC
   char* p2p_base = nullptr;
@@ -118,20 +124,33 @@ RedBuf redbuf(xmhd_ctx* c) {
   return rb;
 }
 
-int ensure_ws(xmhd_ctx* c, long long n) {
-  if (c->ws_n >= n) return XMHD_OK;
-  for (int k = 0; k < 2; ++k) {
-    if (c->ybuf[k]) cudaFree(c->ybuf[k]);
-    if (c->pbuf[k]) cudaFree(c->pbuf[k]);
-    c->ybuf[k] = c->pbuf[k] = nullptr;
+// Leja workspace: the y ping-pong pair, and the p pair unless the caller
+// supplied its own interpolant buffers for this call.
+int ensure_ws(xmhd_ctx* c, long long n, bool need_p = true) {
+  if (c->ws_n < n) {
+    for (int k = 0; k < 2; ++k) {
+      if (c->ybuf[k]) cudaFree(c->ybuf[k]);
+      if (c->pbuf[k]) cudaFree(c->pbuf[k]);
+      c->ybuf[k] = c->pbuf[k] = nullptr;
+    }
+    c->ws_n = 0;
+    for (int k = 0; k < 2; ++k) CK(cudaMalloc(&c->ybuf[k], sizeof(double) * n));
+    c->ws_n = n;
   }
-  c->ws_n = 0;
-  for (int k = 0; k < 2; ++k) {
-    CK(cudaMalloc(&c->ybuf[k], sizeof(double) * n));
-    CK(cudaMalloc(&c->pbuf[k], sizeof(double) * n));
+  if (need_p && !c->pbuf[0]) {
+    for (int k = 0; k < 2; ++k) CK(cudaMalloc(&c->pbuf[k], sizeof(double) * c->ws_n));
   }
-  c->ws_n = n;
   return XMHD_OK;
+}
+
+// The interpolant pair of the current call.
+inline double* pbuf_of(xmhd_ctx* c, int k) { return c->pbuf_ext[0] ? c->pbuf_ext[k] : c->pbuf[k]; }
+
+// The current direction y of the call (v itself before the first term of an
+// in-place call has completed).
+inline const double* current_y(xmhd_ctx* c) {
+  if (c->leja_v0 && c->ctl_h->m == 1 && c->ctl_h->cur == 0) return c->leja_v0;
+  return c->ybuf[c->ctl_h->cur];
 }
 
 StencilArgs base_args(xmhd_ctx* c) {
@@ -197,20 +216,13 @@ int sync_ctl(xmhd_ctx* c) {
   return XMHD_OK;
 }
 
+StencilArgs leja_args(xmhd_ctx* c);
+
 // Device-resident fused Leja loop: launch iterations in growing batches; each
 // kernel exits immediately once the control block left RUNNING, so the host
 // only synchronises once per batch.
 int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
-  StencilArgs a = base_args(c);
-  a.u = c->leja_u;
-  a.fu = c->leja_fu;
-  a.ybuf[0] = c->ybuf[0];
-  a.ybuf[1] = c->ybuf[1];
-  a.pbuf[0] = c->pbuf[0];
-  a.pbuf[1] = c->pbuf[1];
-  a.coeffs = c->coeffs_d;
-  a.xi = c->xi_d;
-  a.ctl = c->ctl;
+  StencilArgs a = leja_args(c);
   if (peer) a.p2p = c->p2p;
   // first batch: the caller's degree hint (xmhd_leja_hint; the host keys it by
   // phi order and interval scale), so most calls need a single sync
@@ -255,9 +267,15 @@ int upload_coeffs(xmhd_ctx* c, const double* coeffs, int ncoef) {
 
 int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double dt, double q,
                double theta, double tol, const double* xi, const double* coeffs, int ncoef,
-               double* ext_sums = nullptr, bool generic = false) {
-  int rc = ensure_ws(c, n);
+               double* ext_sums = nullptr, bool generic = false, bool single = false,
+               bool inplace = false) {
+  // caller-owned interpolant buffers and the in-place start belong to the
+  // single-domain fused calls with per-term launches (one-role kernel) only
+  if (!single) c->pbuf_ext[0] = c->pbuf_ext[1] = nullptr;
+  inplace = inplace && single && c->ws_grid == 0;
+  int rc = ensure_ws(c, n, !c->pbuf_ext[0]);
   if (rc) return rc;
+  c->leja_v0 = inplace ? v : nullptr;
   rc = upload_coeffs(c, coeffs, ncoef);
   if (rc) return rc;
   // the Leja points never change between calls: upload only what differs
@@ -287,8 +305,8 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   // phi-actions never race on the pinned mirror
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(LejaCtl), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
-  CK(launch_leja_init(v, n, c->ybuf[0], c->pbuf[0], c->ctl, c->coeffs_d, redbuf(c), c->stream,
-                      ext_sums));
+  CK(launch_leja_init(v, n, inplace ? nullptr : c->ybuf[0], inplace ? nullptr : pbuf_of(c, 0),
+                      c->ctl, c->coeffs_d, redbuf(c), c->stream, ext_sums));
   c->launches++;
   return XMHD_OK;
 }
@@ -299,11 +317,12 @@ StencilArgs leja_args(xmhd_ctx* c) {
   a.fu = c->leja_fu;
   a.ybuf[0] = c->ybuf[0];
   a.ybuf[1] = c->ybuf[1];
-  a.pbuf[0] = c->pbuf[0];
-  a.pbuf[1] = c->pbuf[1];
+  a.pbuf[0] = pbuf_of(c, 0);
+  a.pbuf[1] = pbuf_of(c, 1);
   a.coeffs = c->coeffs_d;
   a.xi = c->xi_d;
   a.ctl = c->ctl;
+  a.v0 = c->leja_v0;
   return a;
 }
 
@@ -536,20 +555,35 @@ int xmhd_rhs(xmhd_ctx* c, const double* u, double* f, int* bad_cells) {
   return rc ? rc : XMHD_NONFINITE;
 }
 
-int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w,
-             double* out, int* called, double* out_norm, int* bad_cells) {
-  if (!c || !u || !fu || !w || !out) return fail(XMHD_BADARG, "null arg");
+// jvp (linearize.py:56-67); wn_known >= 0: ||w|| already reduced by the caller
+// (bit for bit the norm kernel's); stage_f != null: the fused tail of a stage
+// difference, out = (stage_f - fu) - J w (integrators.py:146-153).
+static int jvp_impl(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                    const double* w, double wn_known, const double* stage_f, double* out,
+                    int* called, double* out_norm, int* bad_cells) {
   const long long n = NF * c->g.plane;
-  CK(launch_norm(w, n, redbuf(c), c->stream));
-  c->launches++;
-  int rc = fetch_doubles(c, 1);
-  if (rc) return rc;
-  const double wn = c->h_dbl[0];
+  double wn = wn_known;
+  int rc;
+  if (wn < 0.0) {
+    CK(launch_norm(w, n, redbuf(c), c->stream));
+    c->launches++;
+    rc = fetch_doubles(c, 1);
+    if (rc) return rc;
+    wn = c->h_dbl[0];
+  }
   if (called) *called = 0;
+  // (stage_f - fu) - out, in place, for the paths whose kernel wrote J w (or zeros)
+  auto tail = [&]() -> int {
+    const double* v[3] = {stage_f, fu, out};
+    const double cf[3] = {1.0, -1.0, -1.0};
+    CK(launch_lincomb(out, n, v, cf, 3, 0, redbuf(c), c->stream));
+    c->launches++;
+    return XMHD_OK;
+  };
   if (wn == 0.0) {  // linearize.py:63-64: zero vector, no RHS evaluation
     CK(cudaMemsetAsync(out, 0, sizeof(double) * n, c->stream));
     if (out_norm) *out_norm = 0.0;
-    return XMHD_OK;
+    return stage_f ? tail() : XMHD_OK;
   }
   // linearize.py:65: eps = _SQRT_EPS * max(1.0, ||u||) / max(||w||, 1e-300)
   const double eps = (1.4901161193847656e-08 * py_max(1.0, unorm)) / py_max(wn, 1e-300);
@@ -561,9 +595,15 @@ int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const
   a.out = out;
   a.eps = eps;
   a.epsd = make_divisor(eps, c->force_ieee);
+  const bool fused_tail = stage_f && c->ws_grid == 0;   // the one-role kernel's epilogue
+  a.stage_f = fused_tail ? stage_f : nullptr;
   CK(launch_stencil(MODE_JVP, a, c->grid, c->stream));
   c->launches++;
   if (called) *called = 1;
+  if (stage_f && !fused_tail) {
+    rc = tail();
+    if (rc) return rc;
+  }
   rc = fetch_doubles(c, 1);
   if (rc) return rc;
   if (out_norm) *out_norm = c->h_dbl[0];
@@ -576,6 +616,20 @@ int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const
     if (rc) return rc;
   }
   return XMHD_NONFINITE;
+}
+
+int xmhd_jvp(xmhd_ctx* c, const double* u, const double* fu, double unorm, const double* w,
+             double* out, int* called, double* out_norm, int* bad_cells) {
+  if (!c || !u || !fu || !w || !out) return fail(XMHD_BADARG, "null arg");
+  return jvp_impl(c, u, fu, unorm, w, -1.0, nullptr, out, called, out_norm, bad_cells);
+}
+
+int xmhd_stage_difference(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                          const double* d, double dnorm, const double* fstage, double* out,
+                          int* called, int* bad_cells) {
+  if (!c || !u || !fu || !d || !fstage || !out) return fail(XMHD_BADARG, "null arg");
+  if (!(dnorm >= 0.0)) return fail(XMHD_BADARG, "dnorm must be the norm of d");
+  return jvp_impl(c, u, fu, unorm, d, dnorm, fstage, out, called, nullptr, bad_cells);
 }
 
 // Device-resident power iteration of estimate_alpha (linearize.py:113-135).
@@ -726,6 +780,34 @@ int xmhd_lincomb(xmhd_ctx* c, double* out, long long n, const double* const* v, 
   return XMHD_OK;
 }
 
+int xmhd_lincomb_diff(xmhd_ctx* c, double* out, double* diff, long long n,
+                      const double* const* v, const double* cf, int nterms, double* diff_norm) {
+  if (!c || !out || !diff || !v || !cf || !diff_norm || nterms < 2 || nterms > 4)
+    return fail(XMHD_BADARG, "bad lincomb_diff args");
+  CK(launch_lincomb_diff(out, diff, n, v, cf, nterms, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 1);
+  if (rc) return rc;
+  *diff_norm = c->h_dbl[0];
+  return XMHD_OK;
+}
+
+int xmhd_lincomb_multi(xmhd_ctx* c, double* const* out, int nout, long long n,
+                       const double* const* v, const double* coef) {
+  if (!c || !out || !v || !coef || nout < 2 || nout > 4)
+    return fail(XMHD_BADARG, "bad lincomb_multi args");
+  for (int j = 0; j < nout; ++j) {
+    if (!out[j]) return fail(XMHD_BADARG, "null output");
+    if (coef[3 * j] == 0.0 && coef[3 * j + 1] == 0.0 && coef[3 * j + 2] == 0.0)
+      return fail(XMHD_BADARG, "a combination needs a non-zero coefficient");
+  }
+  for (int k = 0; k < 3; ++k)
+    if (!v[k]) return fail(XMHD_BADARG, "null input");
+  CK(launch_lincomb_multi(out, nout, n, v, coef, redbuf(c), c->stream));
+  c->launches++;
+  return XMHD_OK;
+}
+
 int xmhd_divide(xmhd_ctx* c, double* out, const double* x, double d, long long n,
                 double* norm_out) {
   if (!c || !out || !x) return fail(XMHD_BADARG, "null arg");
@@ -789,7 +871,8 @@ int xmhd_leja_start(xmhd_ctx* c, const double* u, const double* fu, double unorm
   const long long n = NF * c->g.plane;
   c->leja_u = u;
   c->leja_fu = fu;
-  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef, nullptr, false, true,
+                      true);
   if (rc) return rc;
   return leja_run(c, st);
 }
@@ -801,7 +884,19 @@ int xmhd_leja_start_async(xmhd_ctx* c, const double* u, const double* fu, double
   if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "use the strip driver for BC_HALO");
   c->leja_u = u;
   c->leja_fu = fu;
-  return leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+  return leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef, nullptr,
+                    false, true, false);
+}
+
+int xmhd_leja_start_inplace(xmhd_ctx* c, const double* u, const double* fu, double unorm,
+                            const double* v, double dt, double q, double theta, double tol,
+                            const double* xi, const double* coeffs, int ncoef) {
+  if (!c || !u || !fu || !v || !xi || !coeffs) return fail(XMHD_BADARG, "null arg");
+  if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "use the strip driver for BC_HALO");
+  c->leja_u = u;
+  c->leja_fu = fu;
+  return leja_setup(c, v, NF * c->g.plane, unorm, dt, q, theta, tol, xi, coeffs, ncoef, nullptr,
+                    false, true, true);
 }
 
 int xmhd_leja_resume(xmhd_ctx* c, const double* coeffs, int ncoef, xmhd_leja_state* st) {
@@ -878,6 +973,8 @@ static void loop_plan(xmhd_ctx* c) {
 int xmhd_leja_loop(xmhd_ctx* c) {
   if (!c) return fail(XMHD_BADARG, "null ctx");
   if (c->g.bcy == BC_HALO) return fail(XMHD_BADARG, "y-strips use the strip drivers");
+  if (c->leja_v0)
+    return fail(XMHD_BADARG, "a call started in place runs per-term launches (xmhd_leja_launch)");
   loop_plan(c);
   StencilArgs a = leja_args(c);
   if (c->tile_grid > 0) {
@@ -888,6 +985,34 @@ int xmhd_leja_loop(xmhd_ctx* c) {
     CK(launch_leja_loop(a, c->grid, c->stream));
   }
   c->launches++;
+  return XMHD_OK;
+}
+
+int xmhd_leja_set_pbuf(xmhd_ctx* c, double* p0, double* p1) {
+  if (!c || (p0 == nullptr) != (p1 == nullptr) || (p0 && p0 == p1))
+    return fail(XMHD_BADARG, "pass two distinct buffers, or two nulls");
+  c->pbuf_ext[0] = p0;
+  c->pbuf_ext[1] = p1;
+  return XMHD_OK;
+}
+
+int xmhd_leja_result_inplace(xmhd_ctx* c, int* which) {
+  if (!c || !which) return fail(XMHD_BADARG, "null arg");
+  if (!c->pbuf_ext[0]) return fail(XMHD_BADARG, "no caller-owned interpolant buffers set");
+  int rc = sync_ctl(c);
+  if (rc) return rc;
+  const LejaCtl& h = *c->ctl_h;
+  if (!h.ppend && !h.pvirt) {   // the last stored interpolant is the result
+    *which = h.pcur;
+    return XMHD_OK;
+  }
+  // p + c*y (or c0*v) into the buffer the call is not reading
+  const int dst = h.pcur ^ 1;
+  const long long n = NF * c->g.plane;
+  const double* pb[2] = {c->pbuf_ext[0], c->pbuf_ext[1]};
+  CK(launch_leja_copy_result(c->pbuf_ext[dst], pb, c->ybuf, c->leja_v0, c->ctl, n, c->stream));
+  c->launches++;
+  *which = dst;
   return XMHD_OK;
 }
 
@@ -967,7 +1092,10 @@ int xmhd_leja_finish_async(xmhd_ctx* c, double* p_out) {
   if (!c || !p_out || !c->arec) return fail(XMHD_BADARG, "null arg or no xmhd_async_begin");
   if (c->nleja_async >= ASYNC_LEJA_MAX) return fail(XMHD_BADARG, "too many phi-actions in one step");
   const long long n = NF * c->g.plane;
-  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
+  {
+    const double* pb[2] = {pbuf_of(c, 0), pbuf_of(c, 1)};
+    CK(launch_leja_copy_result(p_out, pb, c->ybuf, c->leja_v0, c->ctl, n, c->stream));
+  }
   CK(cudaMemcpyAsync(&c->arec->leja[c->nleja_async], c->ctl, sizeof(LejaCtl),
                      cudaMemcpyDeviceToDevice, c->stream));
   c->nleja_async++;
@@ -1029,7 +1157,10 @@ int xmhd_leja_result(xmhd_ctx* c, double* p_out) {
   int rc = sync_ctl(c);
   if (rc) return rc;
   const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
-  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
+  {
+    const double* pb[2] = {pbuf_of(c, 0), pbuf_of(c, 1)};
+    CK(launch_leja_copy_result(p_out, pb, c->ybuf, c->leja_v0, c->ctl, n, c->stream));
+  }
   c->launches++;
   return XMHD_OK;
 }
@@ -1057,7 +1188,8 @@ int xmhd_leja(xmhd_ctx* c, int l, const double* u, const double* fu, double unor
   const long long n = NF * c->g.plane;
   c->leja_u = u;
   c->leja_fu = fu;
-  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef);
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, tol, xi, coeffs, ncoef, nullptr, false, true,
+                      !xmhd_leja_loop_available(c));
   if (rc) return rc;
   xmhd_leja_state st;
   if (xmhd_leja_loop_available(c)) {
@@ -1080,10 +1212,13 @@ int xmhd_leja(xmhd_ctx* c, int l, const double* u, const double* fu, double unor
   if (converged) *converged = st.status == LJ_CONVERGED;
   if (residual) *residual = st.residual;
   if (st.status == LJ_RHS_BAD) {
-    rc = scan_bad_cells_shifted(c, u, c->ybuf[c->ctl_h->cur], st.eps, bad_cells);
+    rc = scan_bad_cells_shifted(c, u, current_y(c), st.eps, bad_cells);
     return rc ? rc : XMHD_NONFINITE;
   }
-  CK(launch_leja_copy_result(p_out, c->pbuf, c->ybuf, c->ctl, n, c->stream));
+  {
+    const double* pb[2] = {pbuf_of(c, 0), pbuf_of(c, 1)};
+    CK(launch_leja_copy_result(p_out, pb, c->ybuf, c->leja_v0, c->ctl, n, c->stream));
+  }
   c->launches++;
   CK(cudaStreamSynchronize(c->stream));
   return XMHD_OK;
@@ -1094,8 +1229,7 @@ int xmhd_leja_current_y(xmhd_ctx* c, double* dst) {
   int rc = sync_ctl(c);
   if (rc) return rc;
   const long long n = c->gen_n ? c->gen_n : NF * c->g.plane;
-  CK(cudaMemcpyAsync(dst, c->ybuf[c->ctl_h->cur], sizeof(double) * n, cudaMemcpyDeviceToDevice,
-                     c->stream));
+  CK(cudaMemcpyAsync(dst, current_y(c), sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   return XMHD_OK;
 }
 
@@ -1192,18 +1326,10 @@ int xmhd_time_leja_iterations(xmhd_ctx* c, const double* u, const double* fu, do
   c->leja_u = u;
   c->leja_fu = fu;
   // tol = 0: the convergence test never fires, every launch does a full term
-  int rc = leja_setup(c, v, n, unorm, dt, q, theta, 0.0, xi, coeffs500, 500);
+  int rc = leja_setup(c, v, n, unorm, dt, q, theta, 0.0, xi, coeffs500, 500, nullptr, false, true,
+                      true);
   if (rc) return rc;
-  StencilArgs a = base_args(c);
-  a.u = u;
-  a.fu = fu;
-  a.ybuf[0] = c->ybuf[0];
-  a.ybuf[1] = c->ybuf[1];
-  a.pbuf[0] = c->pbuf[0];
-  a.pbuf[1] = c->pbuf[1];
-  a.coeffs = c->coeffs_d;
-  a.xi = c->xi_d;
-  a.ctl = c->ctl;
+  StencilArgs a = leja_args(c);
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));

@@ -1,0 +1,200 @@
+// Pageable host memory -> device copies at the drop-in boundary.
+//
+// The reference's callers hand the API plain NumPy arrays (pageable memory);
+// cudaMemcpy from pageable memory is staged by the driver through one bounce
+// buffer on one thread (~11 GB/s on the B200 boxes).  Here a persistent pool of
+// host threads fills page-locked slots while the copy engine drains the slots
+// filled before, in stream order, so the copy runs at the slower of the host
+// memcpy rate and the PCIe rate.  One call = one vector; the call returns when
+// the last slot has been handed to the copy engine (the caller's array is no
+// longer read), the device side completes in stream order.
+#include <cuda_runtime.h>
+#include <emmintrin.h>
+
+#include <sched.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "xmhd_b200.h"
+
+namespace {
+
+// memcpy with streaming stores: the slot is read next by the copy engine, not
+// by this core, so it should not displace the caller's working set.
+void copy_stream(char* dst, const char* src, size_t n) {
+  while (n && (reinterpret_cast<uintptr_t>(dst) & 15)) { *dst++ = *src++; --n; }
+  size_t blocks = n / 64;
+  for (size_t b = 0; b < blocks; ++b) {
+    const __m128i a0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src));
+    const __m128i a1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 16));
+    const __m128i a2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 32));
+    const __m128i a3 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst), a0);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 16), a1);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 32), a2);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 48), a3);
+    src += 64;
+    dst += 64;
+  }
+  _mm_sfence();
+  std::memcpy(dst, src, n - blocks * 64);
+}
+
+struct Pool {
+  std::mutex mu;
+  std::condition_variable wake, done;
+  std::vector<std::thread> workers;
+  // current job: [src, src+bytes) -> dst split over `parts` workers
+  const char* src = nullptr;
+  char* dst = nullptr;
+  size_t bytes = 0;
+  int parts = 0, pending = 0;
+  unsigned long long gen = 0;
+  bool stop = false, streaming = true;
+
+  void part(int j) const {
+    // 64-byte aligned cuts
+    const size_t per = ((bytes / parts) + 63) & ~size_t(63);
+    const size_t b0 = std::min(bytes, per * j), b1 = (j == parts - 1) ? bytes : std::min(bytes, per * (j + 1));
+    if (b1 <= b0) return;
+    if (streaming) copy_stream(dst + b0, src + b0, b1 - b0);
+    else std::memcpy(dst + b0, src + b0, b1 - b0);
+  }
+
+  void worker(int j) {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        wake.wait(lk, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+      }
+      if (j < parts) part(j);
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (--pending == 0) done.notify_one();
+      }
+    }
+  }
+
+  void start(int n) {
+    for (int j = 1; j < n; ++j) workers.emplace_back([this, j] { worker(j); });
+  }
+
+  // the calling thread takes part 0
+  void run(char* d, const char* s, size_t n) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      dst = d;
+      src = s;
+      bytes = n;
+      pending = (int)workers.size();
+      ++gen;
+    }
+    wake.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(mu);
+    done.wait(lk, [&] { return pending == 0; });
+  }
+
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    wake.notify_all();
+    for (auto& t : workers) t.join();
+  }
+};
+
+struct Stager {
+  std::mutex mu;          // one staged copy at a time per process
+  std::vector<char*> slot;
+  std::vector<cudaEvent_t> ev;
+  std::vector<bool> used;
+  size_t chunk = 0;
+  int device = -1;
+  Pool* pool = nullptr;
+  int threads = 0;
+};
+
+Stager g_st;
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+}  // namespace
+
+extern "C" int xmhd_h2d_threads(void) {
+  std::lock_guard<std::mutex> lk(g_st.mu);
+  return g_st.threads;
+}
+
+extern "C" int xmhd_h2d_staged(void* dst_dev, const void* src_host, long long bytes, void* stream) {
+  if (!dst_dev || !src_host || bytes < 0) return XMHD_BADARG;
+  if (bytes == 0) return XMHD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lk(g_st.mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XMHD_CUDA_ERROR;
+  if (g_st.slot.empty()) {
+    const int nslot = std::max(2, env_int("XMHD_H2D_SLOTS", 4));
+    g_st.chunk = (size_t)std::max(1, env_int("XMHD_H2D_CHUNK_MB", 16)) << 20;
+    int hw = (int)std::thread::hardware_concurrency();
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) hw = CPU_COUNT(&set);
+    if (hw < 1) hw = 1;
+    // leave cores for the caller's other threads: half the cores, at most 12
+    g_st.threads = std::max(1, env_int("XMHD_H2D_THREADS", std::min(12, std::max(1, hw / 2))));
+    for (int k = 0; k < nslot; ++k) {
+      void* p = nullptr;
+      cudaEvent_t e;
+      if (cudaHostAlloc(&p, g_st.chunk, cudaHostAllocPortable) != cudaSuccess ||
+          cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        for (char* q : g_st.slot) cudaFreeHost(q);
+        g_st.slot.clear();
+        g_st.ev.clear();
+        return XMHD_CUDA_ERROR;
+      }
+      g_st.slot.push_back(static_cast<char*>(p));
+      g_st.ev.push_back(e);
+      g_st.used.push_back(false);
+    }
+    g_st.pool = new Pool();
+    g_st.pool->streaming = env_int("XMHD_H2D_NT", 1) != 0;
+    g_st.pool->parts = g_st.threads;
+    g_st.pool->start(g_st.threads);
+    g_st.device = dev;
+  }
+  if (dev != g_st.device) return XMHD_BADARG;   // one process per GPU: the events belong to it
+  const char* src = static_cast<const char*>(src_host);
+  char* dst = static_cast<char*>(dst_dev);
+  const size_t total = (size_t)bytes;
+  size_t off = 0;
+  int k = 0;
+  const int nslot = (int)g_st.slot.size();
+  while (off < total) {
+    const size_t m = std::min(g_st.chunk, total - off);
+    const int i = k % nslot;
+    if (g_st.used[i] && cudaEventSynchronize(g_st.ev[i]) != cudaSuccess) return XMHD_CUDA_ERROR;
+    g_st.pool->run(g_st.slot[i], src + off, m);
+    if (cudaMemcpyAsync(dst + off, g_st.slot[i], m, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaEventRecord(g_st.ev[i], s) != cudaSuccess)
+      return XMHD_CUDA_ERROR;
+    g_st.used[i] = true;
+    off += m;
+    ++k;
+  }
+  return XMHD_OK;
+}

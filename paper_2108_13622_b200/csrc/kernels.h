@@ -48,6 +48,12 @@ struct LejaCtl {
   int pmode;        // LejaPMode of the next term (= leja_pmode(m, defer))
   double pend_coef; // coefficient of the pending term
   double pend_ynorm;// ||y|| of a term whose residual is not resolved yet
+  // In-place start (single domain, host-paced terms): the caller's v is read
+  // as the first direction and the interpolant is c0 * v, formed on the fly by
+  // whoever reads it, until the first term that stores p (StencilArgs::v0).
+  int pvirt;        // 1: the stored interpolant is still c0 * v (nothing in pbuf)
+  int pad3_;
+  double c0;        // coeffs[0]
 };
 
 // What a term does with the interpolant.
@@ -145,6 +151,8 @@ struct StencilArgs {
   const double* coeffs;
   const double* xi;
   LejaCtl* ctl;
+  const double* v0;    // in-place start: the call's v (direction of term 1, c0*v = p0)
+  const double* stage_f; // MODE_JVP: F(stage); out = (F(stage) - F(u)) - J w (null: out = J w)
   // reductions / flags
   double* partials;    // [grid][2]
   unsigned* ticket;
@@ -190,6 +198,15 @@ cudaError_t launch_norm(const double* x, long long n, RedBuf rb, cudaStream_t s)
 cudaError_t launch_lincomb(double* out, long long n, const double* const* v,
                            const double* c, int nterms, int want_norm, RedBuf rb,
                            cudaStream_t s);
+// out = the combination above and diff = out - v[0] in one pass; result[0] = ||diff||
+// (a stage vector and the direction of its stage difference, integrators.py:139-153).
+cudaError_t launch_lincomb_diff(double* out, double* diff, long long n, const double* const* v,
+                                const double* c, int nterms, RedBuf rb, cudaStream_t s);
+// out[j] = sum_k coef12[3j+k] * v[k] (k = 0..2 in order, zero coefficients skipped),
+// j < nout <= 4: several combinations of the same three vectors in one pass.
+cudaError_t launch_lincomb_multi(double* const* out, int nout, long long n,
+                                 const double* const* v, const double* coef12, RedBuf rb,
+                                 cudaStream_t s);
 // out = x / d (IEEE), result[0] = ||out|| when want_norm.
 cudaError_t launch_divide(double* out, const double* x, double d, long long n,
                           int want_norm, RedBuf rb, cudaStream_t s);
@@ -258,8 +275,8 @@ int leja_tile_loop_grid(const Geom& g, int nsm, int* minb);
 // p_out = the interpolant of a finished call: pbuf[pcur], plus pend_coef *
 // ybuf[cur] when a term is pending (no host read of the control block).
 cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf,
-                                    const double* const* ybuf, const LejaCtl* ctl, long long n,
-                                    cudaStream_t s);
+                                    const double* const* ybuf, const double* v0,
+                                    const LejaCtl* ctl, long long n, cudaStream_t s);
 // jvp prologue on the device: sum(w^2) -> ||w||, eps and its divisor in jc
 // (status PW_RUNNING), or status PW_ZERO for a zero vector (linearize.py:62-65).
 cudaError_t launch_jvp_prep(const double* w, long long n, double unorm, PowerCtl* jc, RedBuf rb,
@@ -407,6 +424,7 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
     ctl->pend_coef = cm;
   } else {                 // this term stored p'
     ctl->pcur ^= 1;
+    ctl->pvirt = 0;        // a virtual interpolant (c0 * v) has now materialised
     ctl->ppend = 0;
   }
   ctl->residual = res;

@@ -86,11 +86,7 @@ __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; } 
 #ifndef XB_ONEBAR
 #define XB_ONEBAR 0   // measured: 0.282 vs 0.281 ms (2048^2), 1.088 vs 1.080 (4096^2): the larger carve-out costs more than the barrier
 #endif
-#ifndef XB_P3EARLY
-#define XB_P3EARLY 0   // output phase of row r-3 in the same phase as P1 of row r (A/B)
-#endif
-constexpr int RING_PD = XB_ONEBAR ? 3 : 2, RING_FX = 4, RING_FY = XB_P3EARLY ? 5 : 4,
-              RING_GX = 2;
+constexpr int RING_PD = XB_ONEBAR ? 3 : 2, RING_FX = 4, RING_FY = 4, RING_GX = 2;
 
 // Source of one ghost-extended row.  Element offsets are 32-bit unsigned: a
 // per-GPU vector of 8*nx*ny < 2^32 doubles (34 GB) covers every grid that fits
@@ -243,6 +239,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
   int ppend = 0;               // a term is pending (pbuf[pcur] + pcoef * y)
   int pm_rt = PM_STORE;        // LejaPMode of this term (control block)
   int zero_dir = 0;
+  int pvirt = 0;               // the stored interpolant is still c0 * v (in-place start)
+  double c0 = 0.0;
+  // MODE_JVP as the tail of a stage difference (integrators.py:146-153):
+  // out = (F(stage) - F(u)) - J w instead of J w
+  const double* sfp = (MODE == MODE_JVP) ? a.stage_f : nullptr;
   const double* hlo_dir = g.halo_lo_dir;
   const double* hhi_dir = g.halo_hi_dir;
   double* push_lo = nullptr;
@@ -270,6 +271,13 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     const int pc = c->pcur;
     pin = a.pbuf[pc];
     pout = a.pbuf[pc ^ 1];
+    if (XR == XR_NONE && a.v0) {
+      // in-place start: term 1 reads the caller's v as its direction, and until
+      // a term has stored p the interpolant read here is c0 * v
+      if (m == 1) dir = a.v0;
+      pvirt = c->pvirt;
+      if (pvirt) { pin = a.v0; c0 = c->c0; }
+    }
     ppend = c->ppend;
     pcoef = c->pend_coef;
     pm_rt = c->pmode;
@@ -311,6 +319,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       double pn = 0.0;
       if (pread) {
         double pb = ld_dir<COH>(pin + i);
+        if (XR == XR_NONE && pvirt) pb = __dmul_rn(c0, pb);
         if (padd) {   // the pending term first
           pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
           if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
@@ -328,255 +337,6 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       acc1 = __fma_rn(pn, pn, acc1);
     }
   } else {
-#if XB_P3EARLY
-    // Row loop with the output phase moved ahead: output row o = r-3 is
-    // finished (differences + epilogue) in the same phase as the primitives
-    // and ideal fluxes of row r, so two independent dependency chains share
-    // each warp's issue slots; the diffusive fluxes of row r-1 follow after
-    // the first barrier.  Inputs of P3(o) all come from earlier steps: FX(o)
-    // (P1 three steps ago), FY(o+1), FY(o-1) (5-slot ring), GX(o) (P2 two
-    // steps ago), GY(o+1), GY(o-1) (registers).  One more warm-up row per
-    // segment; same operations, same order, bitwise the same results.
-    for (int unit = bid; unit < a.nunits; unit += nblk) {
-      const int ux = unit % a.units_x, uy = unit / a.units_x;
-      const int X0 = ux * SOUT;
-      const int Y0 = uy * a.seg_rows;
-      const int Y1 = min(Y0 + a.seg_rows, g.ny);
-      const int cg = X0 - 2 + t;
-      int cs, flipx;
-      col_source(cg, g, cs, flipx);
-      const int c_out = X0 + t - 2;
-      const bool col_ok = (t >= 2) && (t < SW - 2) && (c_out < g.nx);
-      const int tl = max(t - 1, 0), tr = min(t + 1, SW - 1);
-      const double* dsrc = (MODE == MODE_RHS) ? nullptr : dir;
-
-      double gy1[NG], gy2[NG], gy3[NG];   // GY of rows r-2, r-3, r-4
-#pragma unroll
-      for (int k = 0; k < NG; ++k) gy1[k] = gy2[k] = gy3[k] = 0.0;
-      double pr1[NPD], pr2[NPD];
-#pragma unroll
-      for (int k = 0; k < NPD; ++k) pr1[k] = pr2[k] = 0.0;
-
-      double nu[NF], nd[NF];
-      int nflip;
-      {
-        const RowSrc rs = row_source(Y0 - 2, g, a.u, dsrc, hlo_dir, hhi_dir);
-        nflip = rs.flip;
-#pragma unroll
-        for (int f = 0; f < NF; ++f) {
-          nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-          if (MODE != MODE_RHS) nd[f] = ld_dir<COH>(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-        }
-      }
-
-      const int nrows = Y1 - Y0;
-      const int last_p1 = nrows + 3;     // P1 rows Y0-2 .. Y1+1, P2 rows Y0-1 .. Y1
-      const int nsteps = nrows + 5;      // outputs Y0 .. Y1-1 at steps 5 .. nrows+4
-      for (int s = 0; s < nsteps; ++s) {
-        const int r = Y0 - 2 + s;
-        const int o = r - 3;
-        const bool out_row = (s >= 5) && col_ok;
-        const unsigned obase = (unsigned)o * (unsigned)g.nx + (unsigned)c_out;
-        const unsigned plane = (unsigned)g.plane;
-        const int sfx = s & 3;           // FX slot of row r
-        const int sfy = s % RING_FY;     // FY slot of row r
-
-#if XB_L2PF
-        if (MODE != MODE_RHS) {
-          constexpr int LPR = SW / 16;
-          const int rp = r + XB_L2PF;
-          const int ro = o + XB_L2PF_E;
-          const bool do_rows = s + XB_L2PF <= last_p1 && rp >= 0 && rp < g.ny;
-          const bool do_epi = s + XB_L2PF_E < nsteps && s + XB_L2PF_E >= 5 && ro >= 0 && ro < g.ny;
-          const int seg = t % LPR, f = (t / LPR) & 7;
-          const int c0 = min(max(X0 - 2 + seg * 16, 0), g.nx - 1);
-          if (do_rows) {
-            const double* base = (t >= 8 * LPR) ? dir : a.u;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                base + ((unsigned)f * plane + (unsigned)rp * (unsigned)g.nx + (unsigned)c0)));
-          }
-          if (do_epi) {
-#pragma unroll
-            for (int k = t; k < (MODE == MODE_LEJA ? (pread ? 24 : 16) : 8) * LPR; k += SW) {
-              const double* base = (k < 8 * LPR) ? a.fu : (k < 16 * LPR ? dir : pin);
-              const int ff = (k / LPR) & 7, sg = k % LPR;
-              const int cc = min(max(X0 - 2 + sg * 16, 0), g.nx - 1);
-              asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                  base + ((unsigned)ff * plane + (unsigned)ro * (unsigned)g.nx + (unsigned)cc)));
-            }
-          }
-        }
-#endif
-        // ---- P3: output row o = r-3 (everything it reads was written before
-        // the barriers of the previous steps)
-        if (out_row) {
-          double efu[NF], ey[NF], ep[NF];
-          if (MODE != MODE_RHS) {
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const unsigned i = obase + (unsigned)f * plane;
-              efu[f] = __ldg(a.fu + i);
-              if (MODE == MODE_LEJA) {
-                ey[f] = ld_dir<COH>(dir + i);
-                if (pread) ep[f] = ld_dir<COH>(pin + i);
-              }
-            }
-          }
-          const int fxo = (s + 1) & 3;                  // FX slot of row o (s-3 mod 4)
-          const int fyu = (s + RING_FY - 2) % RING_FY;  // FY slot of row o+1
-          const int fyd = (s + RING_FY - 4) % RING_FY;  // FY slot of row o-1
-          const int gs = s & 1;                         // GX slot of row o (P2 of step s-2)
-          double F[NF];
-          {
-            double aa[NFX], bb[NFX];
-#pragma unroll
-            for (int k = 0; k < NFX; ++k) { aa[k] = fxs[fxo][k][tr]; bb[k] = fxs[fxo][k][tl]; }
-#pragma unroll
-            for (int k = 0; k < NFX; ++k)
-              F[fx_field(k)] = -qdiv<KX>(__dsub_rn(aa[k], bb[k]), g.h2x);
-          }
-          F[BX] = -0.0;
-          {
-            double aa[NFY], bb[NFY];
-#pragma unroll
-            for (int k = 0; k < NFY; ++k) { aa[k] = fys[fyu][k][t]; bb[k] = fys[fyd][k][t]; }
-#pragma unroll
-            for (int k = 0; k < NFY; ++k) {
-              const int f = fy_field(k);
-              F[f] = __dsub_rn(F[f], qdiv<KY>(__dsub_rn(aa[k], bb[k]), g.h2y));
-            }
-          }
-          F[BY] = __dsub_rn(F[BY], 0.0);
-          if (diff_on<KX>(g)) {
-            double gr[NG], gl[NG];
-#pragma unroll
-            for (int k = 0; k < NG; ++k) { gr[k] = gxs[gs][k][tr]; gl[k] = gxs[gs][k][tl]; }
-            F[RHO] = __dadd_rn(F[RHO], 0.0);
-            F[BX] = __dadd_rn(F[BX], 0.0);
-            F[MX] = __dadd_rn(F[MX], qdiv<KX>(__dsub_rn(gr[0], gl[0]), g.h2x));
-            F[MY] = __dadd_rn(F[MY], qdiv<KX>(__dsub_rn(gr[1], gl[1]), g.h2x));
-            F[MZ] = __dadd_rn(F[MZ], qdiv<KX>(__dsub_rn(gr[2], gl[2]), g.h2x));
-            F[BY] = __dadd_rn(F[BY], qdiv<KX>(__dsub_rn(gr[3], gl[3]), g.h2x));
-            F[BZ] = __dadd_rn(F[BZ], qdiv<KX>(__dsub_rn(gr[4], gl[4]), g.h2x));
-            F[EN] = __dadd_rn(F[EN], qdiv<KX>(__dsub_rn(gr[5], gl[5]), g.h2x));
-            F[RHO] = __dadd_rn(F[RHO], 0.0);
-            F[BY] = __dadd_rn(F[BY], 0.0);
-            F[MX] = __dadd_rn(F[MX], qdiv<KY>(__dsub_rn(gy1[0], gy3[0]), g.h2y));
-            F[MY] = __dadd_rn(F[MY], qdiv<KY>(__dsub_rn(gy1[1], gy3[1]), g.h2y));
-            F[MZ] = __dadd_rn(F[MZ], qdiv<KY>(__dsub_rn(gy1[2], gy3[2]), g.h2y));
-            F[BX] = __dadd_rn(F[BX], qdiv<KY>(__dsub_rn(gy1[3], gy3[3]), g.h2y));
-            F[BZ] = __dadd_rn(F[BZ], qdiv<KY>(__dsub_rn(gy1[4], gy3[4]), g.h2y));
-            F[EN] = __dadd_rn(F[EN], qdiv<KY>(__dsub_rn(gy1[5], gy3[5]), g.h2y));
-          }
-          {
-            unsigned ex = 0;
-#pragma unroll
-            for (int f = 0; f < NF; ++f)
-              ex = max(ex, (unsigned)__double2hiint(F[f]) & 0x7ff00000u);
-            bad |= (ex == 0x7ff00000u);
-          }
-#pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const unsigned i = obase + (unsigned)f * plane;
-            if (MODE == MODE_RHS) {
-              a.out[i] = F[f];
-            } else if (MODE == MODE_JVP) {
-              const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
-              a.out[i] = jv;
-              acc0 = __fma_rn(jv, jv, acc0);
-            } else {
-              const double w = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
-              const double y = ey[f];
-              const double yn = __dsub_rn(
-                  qdiv<DIV_MK2>(__dsub_rn(__dmul_rn(dt, w), __dmul_rn(q, y)), thd),
-                  __dmul_rn(xim, y));
-              yout[i] = yn;
-              double pn = 0.0;
-              if (pread) {
-                double pb = ep[f];
-                if (padd) {
-                  pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
-                  if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
-                }
-                pn = __dadd_rn(pb, __dmul_rn(cm, yn));
-                if (pstore) pout[i] = pn;
-              }
-              if (P2P)
-                push_ghost(push_lo, a.p2p.mirror_lo, push_hi, a.p2p.mirror_hi, f, o, g.ny, g.nx,
-                           c_out, yn);
-              acc0 = __fma_rn(yn, yn, acc0);
-              acc1 = __fma_rn(pn, pn, acc1);
-            }
-          }
-        }
-
-        // ---- P1: row r
-        double pn[NPD];
-        if (s <= last_p1) {
-          double x[NF];
-#pragma unroll
-          for (int f = 0; f < NF; ++f)
-            x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
-          if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-          if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
-          if (s + 1 <= last_p1) {
-            const RowSrc rs = row_source(r + 1, g, a.u, dsrc, hlo_dir, hhi_dir);
-            nflip = rs.flip;
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              nu[f] = __ldg(rs.u + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-              if (MODE != MODE_RHS) nd[f] = ld_dir<COH>(rs.d + (rs.off + (unsigned)cs + (unsigned)f * rs.fs));
-            }
-          }
-          Prim p;
-          primitives<KX == DIV_IEEE>(x, g, p);
-          pn[PD_VX] = p.vx;
-          pn[PD_VY] = p.vy;
-          pn[PD_VZ] = p.vz;
-          pn[PD_BX] = p.bx;
-          pn[PD_BY] = p.by;
-          pn[PD_BZ] = p.bz;
-          pn[PD_T] = p.temp;
-          pn[PD_B2] = p.b2;
-          double fv[NFX];
-#pragma unroll
-          for (int k = 0; k < NPD; ++k) pd[s & 1][k][t] = pn[k];
-          flux_x<KX == DIV_IEEE>(p, g, fv);
-#pragma unroll
-          for (int k = 0; k < NFX; ++k) fxs[sfx][k][t] = fv[k];
-          flux_y<KX == DIV_IEEE>(p, g, fv);
-#pragma unroll
-          for (int k = 0; k < NFY; ++k) fys[sfy][k][t] = fv[k];
-        }
-        __syncthreads();
-
-        // ---- P2: diffusive fluxes at row r-1 -> GX slot s&1 (read two steps on)
-        double gyn[NG];
-#pragma unroll
-        for (int k = 0; k < NG; ++k) gyn[k] = 0.0;
-        if (diff_on<KX>(g) && s >= 2 && s <= last_p1) {
-          double xl[NPD], xr[NPD];
-          const int sp = (s + 1) & 1;   // PD slot of row r-1
-#pragma unroll
-          for (int k = 0; k < NPD; ++k) {
-            xl[k] = pd[sp][k][tl];
-            xr[k] = pd[sp][k][tr];
-          }
-          double gxv[NG];
-          diffusive_fluxes<KX, KY>(xl, xr, pr2, pn, pr1, g, gxv, gyn);
-#pragma unroll
-          for (int k = 0; k < NG; ++k) gxs[s & 1][k][t] = gxv[k];
-        }
-        if (s <= last_p1) {
-#pragma unroll
-          for (int k = 0; k < NPD; ++k) { pr2[k] = pr1[k]; pr1[k] = pn[k]; }
-        }
-#pragma unroll
-        for (int k = 0; k < NG; ++k) { gy3[k] = gy2[k]; gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
-        __syncthreads();
-      }
-    }
-#else
     for (int unit = bid; unit < a.nunits; unit += nblk) {
       const int ux = unit % a.units_x, uy = unit / a.units_x;
       const int X0 = ux * SOUT;
@@ -665,8 +425,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
           }
           if (do_epi) {
 #pragma unroll
-            for (int k = t; k < (MODE == MODE_LEJA ? (pread ? 24 : 16) : 8) * LPR; k += SW) {
-              const double* base = (k < 8 * LPR) ? a.fu : (k < 16 * LPR ? dir : pin);
+            for (int k = t; k < (MODE == MODE_LEJA ? (pread ? 24 : 16) : (sfp ? 16 : 8)) * LPR;
+                 k += SW) {
+              const double* base = (k < 8 * LPR) ? a.fu
+                                                 : (k < 16 * LPR ? (MODE == MODE_JVP ? sfp : dir) : pin);
               const int ff = (k / LPR) & 7, sg = k % LPR;
               const int cc = min(max(X0 - 2 + sg * 16, 0), g.nx - 1);
               asm volatile("prefetch.global.L2 [%0];" ::"l"(
@@ -677,12 +439,13 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         }
 #endif
         // epilogue operands of output row r-2: issue now, consume in P3
-        double efu[NF], ey[NF], ep[NF];
+        double efu[NF], ey[NF], ep[NF], esf[NF];
         if (MODE != MODE_RHS && out_row) {
 #pragma unroll
           for (int f = 0; f < NF; ++f) {
             const unsigned i = obase + (unsigned)f * plane;
             efu[f] = __ldg(a.fu + i);
+            if (MODE == MODE_JVP && sfp) esf[f] = __ldg(sfp + i);
             if (MODE == MODE_LEJA) {
               ey[f] = ld_dir<COH>(dir + i);
               if (pread) ep[f] = ld_dir<COH>(pin + i);
@@ -822,7 +585,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
                 a.out[i] = F[f];
               } else if (MODE == MODE_JVP) {
                 const double jv = qdiv<DIV_MK2>(__dsub_rn(F[f], efu[f]), epsd);
-                a.out[i] = jv;
+                a.out[i] = sfp ? __dsub_rn(__dsub_rn(esf[f], efu[f]), jv) : jv;
                 acc0 = __fma_rn(jv, jv, acc0);
               } else {
                 // per-launch divisors (eps, theta): exact on either path
@@ -835,6 +598,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
                 double pn = 0.0;
                 if (pread) {
                   double pb = ep[f];
+                  if (XR == XR_NONE && pvirt) pb = __dmul_rn(c0, pb);
                   if (padd) {   // the pending term first
                     pb = __dadd_rn(pb, __dmul_rn(pcoef, y));
                     if (pnorm2) acc2 = __fma_rn(pb, pb, acc2);
@@ -869,7 +633,6 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       }
       __syncthreads();   // rings are reused by the next unit
     }
-#endif
   }
 
   if (bad) atomicOr(a.bad, 1);

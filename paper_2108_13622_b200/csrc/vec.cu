@@ -8,6 +8,7 @@
 // (integrators.py:146-199, linearize.py:113-127, leja.py:121-123).
 #include <cfloat>
 #include <cstring>
+#include <type_traits>
 #include "kernels.h"
 
 namespace xb {
@@ -76,90 +77,258 @@ __device__ bool grid_reduce(double (&v)[NV], const RedBuf& rb, double (&out)[NV]
   return true;
 }
 
-__global__ void __launch_bounds__(VT) norm_kernel(const double* __restrict__ x, long long n,
-                                                  RedBuf rb) {
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double v = __ldg(x + i);
-    acc[0] = __fma_rn(v, v, acc[0]);
+// ---------------------------------------------------------------------------
+// Shared traversal of a flat vector.  The vector is cut into pairs (2p, 2p+1);
+// global thread g of G visits pairs g, g+G, g+2G, ... in that order (the loop
+// is unrolled so several 128-bit loads are in flight per thread), both
+// elements of a pair in index order; an odd last element is visited by global
+// thread 0 after everything else.  Every reducing kernel below accumulates in
+// visit order, so the same data gives the same sum, bit for bit, whichever
+// kernel reduces it (||w|| of the asynchronous jvp prologue == xmhd_norm(w),
+// the flagged combination's ||out|| == xmhd_norm(out), ...).  V2: every
+// pointer is 16-byte aligned (128-bit accesses); otherwise the same order
+// with 64-bit accesses.
+// Measured at n = 1.3e8 (B200, HBM copy peak 6537 GB/s): the former one-element
+// grid-stride loops reached 51-60% of peak in every kernel that stores
+// (lincomb 3.4-4.0 TB/s, divide 3.9), 83-95% in the read-only ones.
+template <bool V2>
+__device__ __forceinline__ double2 ld2(const double* p, long long pair) {
+  if (V2) return __ldg(reinterpret_cast<const double2*>(p) + pair);
+  return make_double2(__ldg(p + 2 * pair), __ldg(p + 2 * pair + 1));
+}
+
+template <bool V2>
+__device__ __forceinline__ void st2(double* p, long long pair, double a, double b) {
+  if (V2) reinterpret_cast<double2*>(p)[pair] = make_double2(a, b);
+  else { p[2 * pair] = a; p[2 * pair + 1] = b; }
+}
+
+template <int NIN, int NOUT>
+struct Ptrs {
+  const double* in[NIN > 0 ? NIN : 1];
+  double* out[NOUT > 0 ? NOUT : 1];
+};
+
+// op(x[NIN], y[NOUT]) handles one element (its accumulators live in op).
+template <int NIN, int NOUT, bool V2, typename Op>
+__device__ __forceinline__ void stream(long long n, const Ptrs<NIN, NOUT>& P, Op& op) {
+  constexpr int U = (NIN + NOUT >= 4) ? 2 : 4;
+  constexpr int NI = NIN > 0 ? NIN : 1, NO = NOUT > 0 ? NOUT : 1;
+  const long long npairs = n >> 1, G = (long long)gridDim.x * VT;
+  long long p = (long long)blockIdx.x * VT + threadIdx.x;
+  for (; p + (U - 1) * G < npairs; p += U * G) {
+    double2 x[U][NI];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) x[u][k] = ld2<V2>(P.in[k], p + u * G);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double xa[NI], xb[NI], ya[NO], yb[NO];
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) { xa[k] = x[u][k].x; xb[k] = x[u][k].y; }
+      op(xa, ya);
+      op(xb, yb);
+#pragma unroll
+      for (int k = 0; k < NOUT; ++k) st2<V2>(P.out[k], p + u * G, ya[k], yb[k]);
+    }
   }
-  double tot[1];
+  for (; p < npairs; p += G) {
+    double xa[NI], xb[NI], ya[NO], yb[NO];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      const double2 v = ld2<V2>(P.in[k], p);
+      xa[k] = v.x;
+      xb[k] = v.y;
+    }
+    op(xa, ya);
+    op(xb, yb);
+#pragma unroll
+    for (int k = 0; k < NOUT; ++k) st2<V2>(P.out[k], p, ya[k], yb[k]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    double xa[NI], ya[NO];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) xa[k] = __ldg(P.in[k] + (n - 1));
+    op(xa, ya);
+#pragma unroll
+    for (int k = 0; k < NOUT; ++k) P.out[k][n - 1] = ya[k];
+  }
+}
+
+template <int NIN, int NOUT>
+bool aligned16(const Ptrs<NIN, NOUT>& P) {
+  unsigned long long bits = 0;
+  for (int k = 0; k < NIN; ++k) bits |= (unsigned long long)P.in[k];
+  for (int k = 0; k < NOUT; ++k) bits |= (unsigned long long)P.out[k];
+  return (bits & 15ull) == 0;
+}
+
+struct SumSqOp {
+  double acc = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[1], double (&)[1]) {
+    acc = __fma_rn(x[0], x[0], acc);
+  }
+};
+
+template <bool V2>
+__global__ void __launch_bounds__(VT) norm_kernel(Ptrs<1, 0> P, long long n, RedBuf rb) {
+  SumSqOp op;
+  stream<1, 0, V2>(n, P, op);
+  double acc[1] = {op.acc}, tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = sqrt(tot[0]);
 }
 
-struct Lin4 {
-  const double* v[4];
+// out = ((c0*v0 + c1*v1) + c2*v2) + c3*v3, one rounding per operation.
+template <int NT>
+struct LincombOp {
   double c[4];
-  int nterms;
+  double acc = 0.0, bad = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[NT], double (&y)[1]) {
+    double s = __dmul_rn(c[0], x[0]);
+#pragma unroll
+    for (int k = 1; k < NT; ++k) s = __dadd_rn(s, __dmul_rn(c[k], x[k]));
+    y[0] = s;
+    acc = __fma_rn(s, s, acc);
+    if (!isfinite(s)) bad = 1.0;
+  }
 };
 
-__global__ void __launch_bounds__(VT) lincomb_kernel(double* __restrict__ out, long long n,
-                                                     Lin4 L, int want_norm, RedBuf rb) {
-  double acc[2] = {0.0, 0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    double s = __dmul_rn(L.c[0], __ldg(L.v[0] + i));
-    if (L.nterms > 1) s = __dadd_rn(s, __dmul_rn(L.c[1], __ldg(L.v[1] + i)));
-    if (L.nterms > 2) s = __dadd_rn(s, __dmul_rn(L.c[2], __ldg(L.v[2] + i)));
-    if (L.nterms > 3) s = __dadd_rn(s, __dmul_rn(L.c[3], __ldg(L.v[3] + i)));
-    out[i] = s;
-    acc[0] = __fma_rn(s, s, acc[0]);
-    if (!isfinite(s)) acc[1] = 1.0;
-  }
+struct Coef4 {
+  double c[4];
+};
+
+template <int NT, bool V2>
+__global__ void __launch_bounds__(VT) lincomb_kernel(Ptrs<NT, 1> P, long long n, Coef4 cf,
+                                                     int want_norm, RedBuf rb) {
+  LincombOp<NT> op;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) op.c[k] = cf.c[k];
+  stream<NT, 1, V2>(n, P, op);
   if (!want_norm) return;
-  double tot[2];
+  double acc[2] = {op.acc, op.bad}, tot[2];
   if (grid_reduce<2, false>(acc, rb, tot)) {
     rb.result[0] = sqrt(tot[0]);
     rb.result[1] = tot[1] > 0.0 ? 1.0 : 0.0;
   }
 }
 
-__global__ void __launch_bounds__(VT) divide_kernel(double* __restrict__ out,
-                                                    const double* __restrict__ x, double d,
-                                                    long long n, int want_norm, RedBuf rb) {
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double q = __ddiv_rn(__ldg(x + i), d);
-    out[i] = q;
-    acc[0] = __fma_rn(q, q, acc[0]);
+// Stage vector and its offset from the base state in one pass
+// (integrators.py:139-153): out = the combination above, diff = out - v0 (v0 =
+// the base state u, coefficient 1), result[0] = ||diff|| -- the direction of
+// the stage difference's jvp and the norm its FD step needs.
+template <int NT>
+struct LincombDiffOp {
+  double c[4];
+  double acc = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[NT], double (&y)[2]) {
+    double s = __dmul_rn(c[0], x[0]);
+#pragma unroll
+    for (int k = 1; k < NT; ++k) s = __dadd_rn(s, __dmul_rn(c[k], x[k]));
+    y[0] = s;
+    const double d = __dsub_rn(s, x[0]);
+    y[1] = d;
+    acc = __fma_rn(d, d, acc);
   }
+};
+
+template <int NT, bool V2>
+__global__ void __launch_bounds__(VT) lincomb_diff_kernel(Ptrs<NT, 2> P, long long n, Coef4 cf,
+                                                          RedBuf rb) {
+  LincombDiffOp<NT> op;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) op.c[k] = cf.c[k];
+  stream<NT, 2, V2>(n, P, op);
+  double acc[1] = {op.acc}, tot[1];
+  if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = sqrt(tot[0]);
+}
+
+// Up to four combinations of the same three vectors in one pass (the w_k of
+// integrators.py:166-167, 186-189): out_j = sum over the terms of row j in
+// order, terms with a zero coefficient skipped (the reference's expressions
+// simply do not contain them).
+struct MultiCoef {
+  double c[4][3];
+  int nout;
+};
+
+template <int NOUT>
+struct MultiOp {
+  MultiCoef m;
+  __device__ __forceinline__ void operator()(const double (&x)[3], double (&y)[NOUT]) {
+#pragma unroll
+    for (int j = 0; j < NOUT; ++j) {
+      double s = 0.0;
+      bool first = true;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (m.c[j][k] != 0.0) {
+          const double t = __dmul_rn(m.c[j][k], x[k]);
+          s = first ? t : __dadd_rn(s, t);
+          first = false;
+        }
+      }
+      y[j] = s;
+    }
+  }
+};
+
+template <int NOUT, bool V2>
+__global__ void __launch_bounds__(VT) lincomb_multi_kernel(Ptrs<3, NOUT> P, long long n,
+                                                           MultiCoef mc) {
+  MultiOp<NOUT> op;
+  op.m = mc;
+  stream<3, NOUT, V2>(n, P, op);
+}
+
+struct DivideOp {
+  double d;
+  double acc = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[1], double (&y)[1]) {
+    const double q = __ddiv_rn(x[0], d);
+    y[0] = q;
+    acc = __fma_rn(q, q, acc);
+  }
+};
+
+template <bool V2>
+__global__ void __launch_bounds__(VT) divide_kernel(Ptrs<1, 1> P, double d, long long n,
+                                                    int want_norm, RedBuf rb) {
+  DivideOp op;
+  op.d = d;
+  stream<1, 1, V2>(n, P, op);
   if (!want_norm) return;
-  double tot[1];
+  double acc[1] = {op.acc}, tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = sqrt(tot[0]);
 }
 
 // One division of the device power iteration (linearize.py:115-116, 124):
 // out = x / div, then ||out|| and the next FD step in the last block.
-__global__ void __launch_bounds__(VT) power_divide_kernel(double* __restrict__ out,
-                                                          const double* __restrict__ x,
-                                                          long long n, PowerCtl* pc, RedBuf rb) {
+template <bool V2>
+__global__ void __launch_bounds__(VT) power_divide_kernel(Ptrs<1, 1> P, long long n,
+                                                          PowerCtl* pc, RedBuf rb) {
   if (pc->status != PW_RUNNING) return;
-  const double d = pc->div;
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double q = __ddiv_rn(__ldg(x + i), d);
-    out[i] = q;
-    acc[0] = __fma_rn(q, q, acc[0]);
-  }
-  double tot[1];
+  DivideOp op;
+  op.d = pc->div;
+  stream<1, 1, V2>(n, P, op);
+  double acc[1] = {op.acc}, tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) power_after_divide(pc, tot[0]);
 }
 
-__global__ void __launch_bounds__(VT) diffnorm_kernel(const double* __restrict__ a,
-                                                      const double* __restrict__ b,
-                                                      long long n, RedBuf rb) {
-  double acc[2] = {0.0, 0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double bv = __ldg(b + i);
-    const double d = __dsub_rn(__ldg(a + i), bv);
-    acc[0] = __fma_rn(d, d, acc[0]);
-    acc[1] = __fma_rn(bv, bv, acc[1]);
+struct DiffNormOp {
+  double acc0 = 0.0, acc1 = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[2], double (&)[1]) {
+    const double d = __dsub_rn(x[0], x[1]);
+    acc0 = __fma_rn(d, d, acc0);
+    acc1 = __fma_rn(x[1], x[1], acc1);
   }
-  double tot[2];
+};
+
+template <bool V2>
+__global__ void __launch_bounds__(VT) diffnorm_kernel(Ptrs<2, 0> P, long long n, RedBuf rb) {
+  DiffNormOp op;
+  stream<2, 0, V2>(n, P, op);
+  double acc[2] = {op.acc0, op.acc1}, tot[2];
   if (grid_reduce<2, false>(acc, rb, tot)) {
     rb.result[0] = sqrt(tot[0]);
     rb.result[1] = sqrt(tot[1]);
@@ -260,25 +429,46 @@ __global__ void __launch_bounds__(VT) cfl_kernel(const double* __restrict__ u, l
   }
 }
 
-// y = v (copy), p = c0*v, ||v|| -> control block (leja.py:121-123).
-__global__ void __launch_bounds__(VT) leja_init_kernel(const double* __restrict__ v, long long n,
-                                                       double* __restrict__ y0,
-                                                       double* __restrict__ p0, LejaCtl* ctl,
+// Start of a phi-action (leja.py:121-123): y = v, p = c0*v, ||v||, control
+// block.  In-place start (y0 == null): nothing is copied -- the first term
+// reads v itself as its direction and the interpolant stays "virtual" (c0 * v,
+// LejaCtl::pvirt) until the first term that stores it; one read pass for ||v||.
+struct LejaInitOp {
+  double c0;
+  double acc = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[1], double (&y)[2]) {
+    y[0] = x[0];
+    y[1] = __dmul_rn(c0, x[0]);
+    acc = __fma_rn(x[0], x[0], acc);
+  }
+};
+
+template <bool V2, bool INPLACE>
+__global__ void __launch_bounds__(VT) leja_init_kernel(Ptrs<1, 2> P, long long n, LejaCtl* ctl,
                                                        const double* __restrict__ coeffs,
                                                        RedBuf rb, double* ext_sums) {
-  const double c0 = coeffs[0];
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double x = __ldg(v + i);
-    y0[i] = x;
-    p0[i] = __dmul_rn(c0, x);
-    acc[0] = __fma_rn(x, x, acc[0]);
+  double acc[1];
+  if (INPLACE) {
+    SumSqOp op;
+    Ptrs<1, 0> Q;
+    Q.in[0] = P.in[0];
+    Q.out[0] = nullptr;
+    stream<1, 0, V2>(n, Q, op);
+    acc[0] = op.acc;
+  } else {
+    LejaInitOp op;
+    op.c0 = coeffs[0];
+    stream<1, 2, V2>(n, P, op);
+    acc[0] = op.acc;
   }
   double tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) {
     if (ext_sums) ext_sums[0] = tot[0];   // y-strips: global sum first (allreduce)
-    else leja_init_ctl(ctl, tot[0]);
+    else {
+      leja_init_ctl(ctl, tot[0]);
+      ctl->pvirt = INPLACE ? 1 : 0;
+      ctl->c0 = coeffs[0];
+    }
   }
 }
 
@@ -318,15 +508,11 @@ __global__ void leja_pack_halo_kernel(const LejaCtl* ctl, const double* y0, cons
   __threadfence_system();   // the destinations may be peer memory (y-strips over NVLink)
 }
 
-__global__ void __launch_bounds__(VT) sumsq_kernel(const double* __restrict__ x, long long n,
-                                                   RedBuf rb) {
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double v = __ldg(x + i);
-    acc[0] = __fma_rn(v, v, acc[0]);
-  }
-  double tot[1];
+template <bool V2>
+__global__ void __launch_bounds__(VT) sumsq_kernel(Ptrs<1, 0> P, long long n, RedBuf rb) {
+  SumSqOp op;
+  stream<1, 0, V2>(n, P, op);
+  double acc[1] = {op.acc}, tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) rb.result[0] = tot[0];
 }
 
@@ -435,8 +621,9 @@ __global__ void p2p_probe_kernel(const P2PArgs x, double value) {
   __threadfence_system();
 }
 
+// Blocks for a vector of n elements: the traversal hands out pairs.
 int grid_for(long long n, int maxg) {
-  long long g = (n + VT - 1) / VT;
+  long long g = ((n + 1) / 2 + VT - 1) / VT;
   if (g > maxg) g = maxg;
   if (g < 1) g = 1;
   return (int)g;
@@ -481,70 +668,168 @@ cudaError_t launch_p2p_probe(const P2PArgs& x, double value, cudaStream_t s) {
 }
 
 cudaError_t launch_norm(const double* x, long long n, RedBuf rb, cudaStream_t s) {
-  norm_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(x, n, rb);
+  Ptrs<1, 0> P;
+  P.in[0] = x;
+  P.out[0] = nullptr;
+  if (aligned16(P)) norm_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
+  else norm_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lincomb(double* out, long long n, const double* const* v, const double* c,
                            int nterms, int want_norm, RedBuf rb, cudaStream_t s) {
-  Lin4 L;
-  L.nterms = nterms;
-  for (int k = 0; k < 4; ++k) {
-    L.v[k] = k < nterms ? v[k] : nullptr;
-    L.c[k] = k < nterms ? c[k] : 0.0;
+  Coef4 cf;
+  for (int k = 0; k < 4; ++k) cf.c[k] = k < nterms ? c[k] : 0.0;
+  const int grid = grid_for(n, rb.grid);
+  auto go = [&](auto NTc) {
+    constexpr int NT = decltype(NTc)::value;
+    Ptrs<NT, 1> P;
+    for (int k = 0; k < NT; ++k) P.in[k] = v[k];
+    P.out[0] = out;
+    if (aligned16(P)) lincomb_kernel<NT, true><<<grid, VT, 0, s>>>(P, n, cf, want_norm, rb);
+    else lincomb_kernel<NT, false><<<grid, VT, 0, s>>>(P, n, cf, want_norm, rb);
+  };
+  switch (nterms) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    default: return cudaErrorInvalidValue;
   }
-  lincomb_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, n, L, want_norm, rb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb_diff(double* out, double* diff, long long n, const double* const* v,
+                                const double* c, int nterms, RedBuf rb, cudaStream_t s) {
+  Coef4 cf;
+  for (int k = 0; k < 4; ++k) cf.c[k] = k < nterms ? c[k] : 0.0;
+  const int grid = grid_for(n, rb.grid);
+  auto go = [&](auto NTc) {
+    constexpr int NT = decltype(NTc)::value;
+    Ptrs<NT, 2> P;
+    for (int k = 0; k < NT; ++k) P.in[k] = v[k];
+    P.out[0] = out;
+    P.out[1] = diff;
+    if (aligned16(P)) lincomb_diff_kernel<NT, true><<<grid, VT, 0, s>>>(P, n, cf, rb);
+    else lincomb_diff_kernel<NT, false><<<grid, VT, 0, s>>>(P, n, cf, rb);
+  };
+  switch (nterms) {
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lincomb_multi(double* const* out, int nout, long long n,
+                                 const double* const* v, const double* coef12, RedBuf rb,
+                                 cudaStream_t s) {
+  MultiCoef mc;
+  mc.nout = nout;
+  for (int j = 0; j < 4; ++j)
+    for (int k = 0; k < 3; ++k) mc.c[j][k] = j < nout ? coef12[3 * j + k] : 0.0;
+  const int grid = grid_for(n, rb.grid);
+  auto go = [&](auto NOc) {
+    constexpr int NO = decltype(NOc)::value;
+    Ptrs<3, NO> P;
+    for (int k = 0; k < 3; ++k) P.in[k] = v[k];
+    for (int j = 0; j < NO; ++j) P.out[j] = out[j];
+    if (aligned16(P)) lincomb_multi_kernel<NO, true><<<grid, VT, 0, s>>>(P, n, mc);
+    else lincomb_multi_kernel<NO, false><<<grid, VT, 0, s>>>(P, n, mc);
+  };
+  switch (nout) {
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_divide(double* out, const double* x, double d, long long n, int want_norm,
                           RedBuf rb, cudaStream_t s) {
-  divide_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, x, d, n, want_norm, rb);
+  Ptrs<1, 1> P;
+  P.in[0] = x;
+  P.out[0] = out;
+  if (aligned16(P)) divide_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, d, n, want_norm, rb);
+  else divide_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, d, n, want_norm, rb);
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(VT) fill_kernel(double* __restrict__ x, long long n, double v) {
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT)
-    x[i] = v;
+struct FillOp {
+  double v;
+  __device__ __forceinline__ void operator()(const double (&)[1], double (&y)[1]) { y[0] = v; }
+};
+
+template <bool V2>
+__global__ void __launch_bounds__(VT) fill_kernel(Ptrs<0, 1> P, long long n, double v) {
+  FillOp op;
+  op.v = v;
+  stream<0, 1, V2>(n, P, op);
 }
 
 cudaError_t launch_fill(double* x, long long n, double v, cudaStream_t s) {
-  fill_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(x, n, v);
+  Ptrs<0, 1> P;
+  P.in[0] = nullptr;
+  P.out[0] = x;
+  if (aligned16(P)) fill_kernel<true><<<grid_for(n, 4 * 148), VT, 0, s>>>(P, n, v);
+  else fill_kernel<false><<<grid_for(n, 4 * 148), VT, 0, s>>>(P, n, v);
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(VT) leja_copy_result_kernel(double* __restrict__ out,
-                                                              const double* p0, const double* p1,
-                                                              const double* y0, const double* y1,
+// The interpolant of a finished call into `out`: pbuf[pcur] (c0 * v while it
+// is still virtual), plus pend_coef * ybuf[cur] when a term is pending (p + c*y,
+// leja.py:140).
+struct CopyResultOp {
+  int pend, pvirt;
+  double c, c0;
+  __device__ __forceinline__ void operator()(const double (&x)[2], double (&y)[1]) {
+    const double p = pvirt ? __dmul_rn(c0, x[0]) : x[0];
+    y[0] = pend ? __dadd_rn(p, __dmul_rn(c, x[1])) : p;
+  }
+};
+
+template <bool V2>
+__global__ void __launch_bounds__(VT) leja_copy_result_kernel(double* out, const double* p0,
+                                                              const double* p1, const double* y0,
+                                                              const double* y1, const double* v0,
                                                               const LejaCtl* ctl, long long n) {
-  const double* __restrict__ src = ctl->pcur ? p1 : p0;
-  const double* __restrict__ y = ctl->cur ? y1 : y0;
-  const int pend = ctl->ppend;
-  const double c = ctl->pend_coef;
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT)
-    out[i] = pend ? __dadd_rn(src[i], __dmul_rn(c, y[i])) : src[i];   // p + c*y (leja.py:140)
+  CopyResultOp op;
+  op.pend = ctl->ppend;
+  op.pvirt = ctl->pvirt;
+  op.c = ctl->pend_coef;
+  op.c0 = ctl->c0;
+  Ptrs<2, 1> P;
+  P.in[0] = op.pvirt ? v0 : (ctl->pcur ? p1 : p0);
+  // the pending term's y is the current direction (v itself before any term ran)
+  P.in[1] = (v0 && ctl->m == 1 && ctl->cur == 0) ? v0 : (ctl->cur ? y1 : y0);
+  P.out[0] = out;
+  stream<2, 1, V2>(n, P, op);
 }
 
 cudaError_t launch_leja_copy_result(double* p_out, const double* const* pbuf,
-                                    const double* const* ybuf, const LejaCtl* ctl, long long n,
-                                    cudaStream_t s) {
-  leja_copy_result_kernel<<<grid_for(n, 4 * 148), VT, 0, s>>>(p_out, pbuf[0], pbuf[1], ybuf[0],
-                                                               ybuf[1], ctl, n);
+                                    const double* const* ybuf, const double* v0,
+                                    const LejaCtl* ctl, long long n, cudaStream_t s) {
+  const unsigned long long bits = (unsigned long long)p_out | (unsigned long long)pbuf[0] |
+                                  (unsigned long long)pbuf[1] | (unsigned long long)ybuf[0] |
+                                  (unsigned long long)ybuf[1] | (unsigned long long)v0;
+  if ((bits & 15ull) == 0)
+    leja_copy_result_kernel<true><<<grid_for(n, 4 * 148), VT, 0, s>>>(
+        p_out, pbuf[0], pbuf[1], ybuf[0], ybuf[1], v0, ctl, n);
+  else
+    leja_copy_result_kernel<false><<<grid_for(n, 4 * 148), VT, 0, s>>>(
+        p_out, pbuf[0], pbuf[1], ybuf[0], ybuf[1], v0, ctl, n);
   return cudaGetLastError();
 }
 
 // jvp prologue (linearize.py:62-65) without a host round trip.
-__global__ void __launch_bounds__(VT) jvp_prep_kernel(const double* __restrict__ w, long long n,
-                                                      double unorm, PowerCtl* jc, RedBuf rb) {
-  double acc[1] = {0.0};
-  for (long long i = (long long)blockIdx.x * VT + threadIdx.x; i < n;
-       i += (long long)gridDim.x * VT) {
-    const double v = __ldg(w + i);
-    acc[0] = __fma_rn(v, v, acc[0]);
-  }
-  double tot[1];
+template <bool V2>
+__global__ void __launch_bounds__(VT) jvp_prep_kernel(Ptrs<1, 0> P, long long n, double unorm,
+                                                      PowerCtl* jc, RedBuf rb) {
+  SumSqOp op;
+  stream<1, 0, V2>(n, P, op);
+  double acc[1] = {op.acc}, tot[1];
   if (grid_reduce<1, false>(acc, rb, tot)) {
     jc->stop = 0;
     jc->status = PW_RUNNING;
@@ -555,19 +840,32 @@ __global__ void __launch_bounds__(VT) jvp_prep_kernel(const double* __restrict__
 
 cudaError_t launch_jvp_prep(const double* w, long long n, double unorm, PowerCtl* jc, RedBuf rb,
                             cudaStream_t s) {
-  jvp_prep_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(w, n, unorm, jc, rb);
+  Ptrs<1, 0> P;
+  P.in[0] = w;
+  P.out[0] = nullptr;
+  if (aligned16(P)) jvp_prep_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, unorm, jc, rb);
+  else jvp_prep_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, unorm, jc, rb);
   return cudaGetLastError();
 }
 
 cudaError_t launch_power_divide(double* out, const double* x, long long n, PowerCtl* pctl,
                                 RedBuf rb, cudaStream_t s) {
-  power_divide_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(out, x, n, pctl, rb);
+  Ptrs<1, 1> P;
+  P.in[0] = x;
+  P.out[0] = out;
+  if (aligned16(P)) power_divide_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, pctl, rb);
+  else power_divide_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, pctl, rb);
   return cudaGetLastError();
 }
 
 cudaError_t launch_diffnorm(const double* a, const double* b, long long n, RedBuf rb,
                             cudaStream_t s) {
-  diffnorm_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(a, b, n, rb);
+  Ptrs<2, 0> P;
+  P.in[0] = a;
+  P.in[1] = b;
+  P.out[0] = nullptr;
+  if (aligned16(P)) diffnorm_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
+  else diffnorm_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
   return cudaGetLastError();
 }
 
@@ -591,7 +889,19 @@ cudaError_t launch_cfl(const double* u, long long plane, double gamma, double mu
 
 cudaError_t launch_leja_init(const double* v, long long n, double* y0, double* p0, LejaCtl* ctl,
                              const double* coeffs, RedBuf rb, cudaStream_t s, double* ext_sums) {
-  leja_init_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(v, n, y0, p0, ctl, coeffs, rb, ext_sums);
+  Ptrs<1, 2> P;
+  P.in[0] = v;
+  P.out[0] = y0;
+  P.out[1] = p0;
+  const int grid = grid_for(n, rb.grid);
+  const bool v2 = aligned16(P);
+  if (!y0) {   // in-place start: ||v|| only
+    if (v2) leja_init_kernel<true, true><<<grid, VT, 0, s>>>(P, n, ctl, coeffs, rb, ext_sums);
+    else leja_init_kernel<false, true><<<grid, VT, 0, s>>>(P, n, ctl, coeffs, rb, ext_sums);
+  } else {
+    if (v2) leja_init_kernel<true, false><<<grid, VT, 0, s>>>(P, n, ctl, coeffs, rb, ext_sums);
+    else leja_init_kernel<false, false><<<grid, VT, 0, s>>>(P, n, ctl, coeffs, rb, ext_sums);
+  }
   return cudaGetLastError();
 }
 
@@ -617,7 +927,11 @@ cudaError_t launch_leja_pack_halo(const LejaCtl* ctl, const double* y0, const do
 }
 
 cudaError_t launch_sumsq(const double* x, long long n, RedBuf rb, cudaStream_t s) {
-  sumsq_kernel<<<grid_for(n, rb.grid), VT, 0, s>>>(x, n, rb);
+  Ptrs<1, 0> P;
+  P.in[0] = x;
+  P.out[0] = nullptr;
+  if (aligned16(P)) sumsq_kernel<true><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
+  else sumsq_kernel<false><<<grid_for(n, rb.grid), VT, 0, s>>>(P, n, rb);
   return cudaGetLastError();
 }
 

@@ -397,6 +397,10 @@ def apply_phi_leja(l, matvec, v, dt, shift, tol):
 # microseconds, keep the host-paced batches of drive_fused (which also extend
 # the coefficient table ahead of the device without stopping it).
 LOOP_MAX_CELLS = int(os.environ.get("XMHD_LOOP_MAX_CELLS", str(1 << 20)))
+# Host-paced calls start in place (no y = v copy, no p = c0*v pass) and hand
+# the result back in one of two caller-owned interpolant buffers instead of
+# copying it out; XMHD_ZERO_COPY=0 restores the copies (A/B, tests).
+ZERO_COPY = bool(int(os.environ.get("XMHD_ZERO_COPY", "1") or "1"))
 
 
 def loop_available(mhd):
@@ -432,11 +436,11 @@ def drive_loop(lib, h, l, q, theta, coeffs):
         size = arr.size
 
 
-def _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs):
-    rc = lib.xmhd_leja_start_async(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs),
-                                   float(lin._base_norm), _lib.ptr(vd), float(dt), float(q),
-                                   float(theta), float(tol), _ptr_d(xi), _ptr_d(coeffs),
-                                   int(coeffs.size))
+def _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs, inplace=False):
+    start = lib.xmhd_leja_start_inplace if inplace else lib.xmhd_leja_start_async
+    rc = start(h, _lib.ptr(lin.base_state), _lib.ptr(lin.base_rhs), float(lin._base_norm),
+               _lib.ptr(vd), float(dt), float(q), float(theta), float(tol), _ptr_d(xi),
+               _ptr_d(coeffs), int(coeffs.size))
     _lib.check(rc, "xmhd_leja_start_async")
 
 
@@ -481,11 +485,27 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
     vd = _ops.as_device(v).reshape(-1)
     coeffs = np.ascontiguousarray(_newton_coeffs(l, q, theta, 64))
     h = mhd.ctx.bind_stream()
-    _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs)
-    if loop_available(mhd):
-        st = drive_loop(lib, h, l, q, theta, coeffs)
-    else:
-        st = drive_fused(lib, h, l, q, theta, coeffs)
+    looped = loop_available(mhd)
+    pair = None
+    if not looped and ZERO_COPY:
+        # host-paced terms (large grids): v is read in place and the interpolant
+        # lives in two caller-owned buffers, one of which becomes the result
+        pair = (torch.empty_like(vd), torch.empty_like(vd))
+        _lib.check(lib.xmhd_leja_set_pbuf(h, _lib.ptr(pair[0]), _lib.ptr(pair[1])),
+                   "xmhd_leja_set_pbuf")
+    try:
+        _start(lib, h, l, lin, vd, dt, q, theta, tol, xi, coeffs, inplace=pair is not None)
+        if looped:
+            st = drive_loop(lib, h, l, q, theta, coeffs)
+        else:
+            st = drive_fused(lib, h, l, q, theta, coeffs)
+        if pair is not None and st.status != _lib.LEJA_RHS_NONFINITE:
+            which = ctypes.c_int()
+            _lib.check(lib.xmhd_leja_result_inplace(h, ctypes.byref(which)),
+                       "xmhd_leja_result_inplace")
+    finally:
+        if pair is not None:
+            lib.xmhd_leja_set_pbuf(h, None, None)
     lin.rhs.calls += st.rhs_calls
     if st.status == _lib.LEJA_RHS_NONFINITE:
         # the reference raises from inside the matvec (mhd.py:225-231); rebuild
@@ -498,8 +518,11 @@ def _apply_fused(l, lin, v, dt, shift, tol, xi):
         except RhsBlowupError as err:
             raise err
         raise RhsBlowupError("non-finite rhs inside the fused Leja iteration")
-    p = torch.empty_like(vd)
-    _lib.check(lib.xmhd_leja_result(h, _lib.ptr(p)), "xmhd_leja_result")
+    if pair is not None:
+        p = pair[which.value]
+    else:
+        p = torch.empty_like(vd)
+        _lib.check(lib.xmhd_leja_result(h, _lib.ptr(p)), "xmhd_leja_result")
     return PhiApplyResult(vector=_ops.like(p, v), iterations=int(st.iterations),
                           converged=st.status == _lib.LEJA_CONVERGED,
                           residual=float(st.residual))

@@ -53,8 +53,9 @@ gaps = []
 per = collections.defaultdict(lambda: [0, 0.0])
 for st, en, name in ks:
     busy += en - st
-    per[name.split("(")[0][:60]][0] += 1
-    per[name.split("(")[0][:60]][1] += en - st
+    key = name.replace("(anonymous namespace)::", "").split("(")[0][:70]
+    per[key][0] += 1
+    per[key][1] += en - st
     if last_end is not None:
         gaps.append(st - last_end)
     last_end = en if last_end is None else max(last_end, en)
