@@ -77,3 +77,33 @@ for g, a, b in sorted(big, reverse=True)[:12]:
     print(f"  gap {g/1e3:8.2f} ms after {a} before {b}")
 for name, (c, t) in sorted(per.items(), key=lambda x: -x[1][1])[:15]:
     print(f"  {name:60s} {c:6d} {t/1e3:9.3f} ms  avg {t/c:7.2f} us")
+# steady state: the stepping phase (between the start-up pauses -- RNG draw, first
+# estimate -- and the final checksum copy); idle time by the kernels around it
+segs, cur_seg, prev_end = [], [], None
+for st, en, name in ks:
+    if prev_end is not None and st - prev_end > 2e5:
+        segs.append(cur_seg)
+        cur_seg = []
+    cur_seg.append((st, en, name))
+    prev_end = en if prev_end is None else max(prev_end, en)
+segs.append(cur_seg)
+# the stepping phase: the run without a 0.2 s pause that holds most Leja terms
+tail = max(segs, key=lambda sg: sum('stencil_kernel<2' in k[2] for k in sg))
+if len(tail) > 2:
+    sspan = tail[-1][1] - tail[0][0]
+    sbusy = sum(en - st for st, en, _ in tail)
+    pairs = collections.defaultdict(lambda: [0, 0.0])
+    pe, pn = tail[0][1], tail[0][2]
+    for st, en, name in tail[1:]:
+        g = st - pe
+        if g > 5:
+            key = (pn.replace("(anonymous namespace)::", "").split("(")[0][:34],
+                   name.replace("(anonymous namespace)::", "").split("(")[0][:34])
+            pairs[key][0] += 1
+            pairs[key][1] += g
+        if en > pe:
+            pe, pn = en, name
+    print(f"steady state: span {sspan/1e3:.1f} ms, busy {sbusy/1e3:.1f} ms, idle {(sspan-sbusy)/1e3:.1f} ms "
+          f"({len(tail)} events)")
+    for (a, b), (c, t) in sorted(pairs.items(), key=lambda x: -x[1][1])[:14]:
+        print(f"  idle {t/1e3:8.2f} ms in {c:4d} gaps  after {a:34s} before {b}")
