@@ -165,6 +165,14 @@ int xmhd_set_loop_kind(xmhd_ctx* ctx, int kind);
  * reference's order (same bits): 320 instead of 384 B/cell per term.  A call
  * that converged on the odd term discards the even one (not counted). */
 int xmhd_set_leja_defer(xmhd_ctx* ctx, int on);
+/* Adaptive lookahead for the started single-domain call run by xmhd_leja_launch:
+ * from term m0 on (0: never; xmhd_leja / xmhd_leja_start pick m0 from
+ * xmhd_leja_hint) every term is enqueued as the pair {scheduled variant,
+ * store variant}.  An odd term that may be the last one (the residual before
+ * it was already <= tol) then resolves its own residual instead of leaving it
+ * to one more full launch; exactly one kernel of a pair runs, the other exits.
+ * Same terms, same bits, same counters.  XMHD_ADAPTIVE=0 disables it. */
+int xmhd_leja_set_dual_from(xmhd_ctx* ctx, int m0);
 /* xmhd_leja_start_async with an in-place start, for calls run by per-term
  * launches (xmhd_leja_launch; not xmhd_leja_loop): nothing is copied -- the
  * first term reads v where it lies (leja.py:121 `y = v`) and the interpolant

@@ -132,6 +132,7 @@ _SIGS = {
                                       _D, _PD, _PD, _I]),
     "xmhd_leja_p2p_emul_run": (_I, [ctypes.POINTER(_P), _I, ctypes.POINTER(LejaState)]),
     "xmhd_leja_start_inplace": (_I, [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I]),
+    "xmhd_leja_set_dual_from": (_I, [_P, _I]),
     "xmhd_leja_set_pbuf": (_I, [_P, _P, _P]),
     "xmhd_leja_result_inplace": (_I, [_P, _PI]),
     "xmhd_stage_difference": (_I, [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI]),

@@ -72,10 +72,12 @@ struct xmhd_ctx {
   double xi_h[500];            // host copy of the Leja points on the device
   bool xi_valid = false;
   bool leja_defer = true;      // deferred interpolant stores (XMHD_PDEFER=0: off)
+  bool leja_adaptive = true;   // variant pairs near the expected end (XMHD_ADAPTIVE=0: off)
   int leja_next_term = 1;      // Newton term index of the next iteration launch
   long long launches = 0;
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
+  int dual_from = 0;           // first term enqueued as a variant pair (0: parity schedule only)
   bool force_ieee = false;
   unsigned long long* scan_d = nullptr;   // [2] non-finite scan (min index, count)
   unsigned long long* scan_h = nullptr;   // pinned [2]
@@ -202,9 +204,28 @@ void fill_state(const LejaCtl& h, xmhd_leja_state* st) {
 // interpolant mode (single-domain lookahead pairs), else the generic one.
 int launch_term(xmhd_ctx* c, const StencilArgs& a, bool peer = false) {
   const int defer = c->ctl_h->defer;
-  const int pm = (defer == 2) ? leja_pmode(c->leja_next_term, 2) : PM_ANY;
-  if (peer) CK(launch_leja_peer(a, c->grid, pm, c->stream));
-  else CK(launch_leja_term(a, c->grid, pm, c->stream));
+  const int m = c->leja_next_term;
+  const int pm = (defer == 2) ? leja_pmode(m, 2) : PM_ANY;
+  if (peer) {
+    CK(launch_leja_peer(a, c->grid, pm, c->stream));
+  } else if (defer == 2 && c->dual_from > 0 && c->ws_grid == 0 && c->g.bcy != BC_HALO) {
+    // adaptive lookahead (kernels.h, leja_next_pmode): from term dual_from on, a
+    // term is the pair {scheduled variant, PM_STORE}; exactly one of them runs
+    StencilArgs b = a;
+    b.dual_next = (m + 1 >= c->dual_from) ? 1 : 0;
+    if (m >= c->dual_from) {
+      b.term = m;
+      if (pm != PM_STORE) {
+        CK(launch_leja_term(b, c->grid, pm, c->stream));
+        c->launches++;
+      }
+      CK(launch_leja_term(b, c->grid, PM_STORE, c->stream));
+    } else {
+      CK(launch_leja_term(b, c->grid, pm, c->stream));
+    }
+  } else {
+    CK(launch_leja_term(a, c->grid, pm, c->stream));
+  }
   c->leja_next_term++;
   c->launches++;
   return XMHD_OK;
@@ -218,6 +239,14 @@ int sync_ctl(xmhd_ctx* c) {
 
 StencilArgs leja_args(xmhd_ctx* c);
 
+// First term of the variant pairs for a call expected to take `hint` terms: a
+// few terms before the expected end (odd, >= 1); the pairs cost one empty
+// launch per term, so long calls run the plain parity schedule until then.
+inline int dual_start(int hint) {
+  const int m0 = hint - 6;
+  return m0 < 1 ? 1 : (m0 | 1);
+}
+
 // Device-resident fused Leja loop: launch iterations in growing batches; each
 // kernel exits immediately once the control block left RUNNING, so the host
 // only synchronises once per batch.
@@ -228,6 +257,7 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   // phi order and interval scale), so most calls need a single sync
   const int done = c->ctl_h->iters;
   if (c->ctl_h->m > 0) c->leja_next_term = c->ctl_h->m;   // resume after a stop
+  if (!peer && done == 0 && c->leja_adaptive) c->dual_from = dual_start(c->hint_iters);
   int batch = c->hint_iters - done;
   if (batch < 2) batch = 2;
   if (batch > c->batch_max) batch = c->batch_max;
@@ -273,6 +303,7 @@ int leja_setup(xmhd_ctx* c, const double* v, long long n, double unorm, double d
   // single-domain fused calls with per-term launches (one-role kernel) only
   if (!single) c->pbuf_ext[0] = c->pbuf_ext[1] = nullptr;
   inplace = inplace && single && c->ws_grid == 0;
+  c->dual_from = 0;
   int rc = ensure_ws(c, n, !c->pbuf_ext[0]);
   if (rc) return rc;
   c->leja_v0 = inplace ? v : nullptr;
@@ -347,6 +378,7 @@ int xmhd_create(xmhd_ctx** out, int nx, int ny, double dx, double dy, double mu,
   const bool ieee = std::getenv("XMHD_DIV_IEEE") && std::atoi(std::getenv("XMHD_DIV_IEEE"));
   c->force_ieee = ieee;
   if (const char* e = std::getenv("XMHD_PDEFER")) c->leja_defer = std::atoi(e) != 0;
+  if (const char* e = std::getenv("XMHD_ADAPTIVE")) c->leja_adaptive = std::atoi(e) != 0;
   Geom& g = c->g;
   std::memset(&g, 0, sizeof(g));
   g.nx = nx;
@@ -1013,6 +1045,12 @@ int xmhd_leja_result_inplace(xmhd_ctx* c, int* which) {
   CK(launch_leja_copy_result(c->pbuf_ext[dst], pb, c->ybuf, c->leja_v0, c->ctl, n, c->stream));
   c->launches++;
   *which = dst;
+  return XMHD_OK;
+}
+
+int xmhd_leja_set_dual_from(xmhd_ctx* c, int m0) {
+  if (!c || m0 < 0) return fail(XMHD_BADARG, "bad term index");
+  c->dual_from = (c->leja_adaptive && m0 > 0) ? (m0 | 1) : 0;
   return XMHD_OK;
 }
 

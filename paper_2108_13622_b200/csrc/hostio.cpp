@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
@@ -48,17 +49,29 @@ void copy_stream(char* dst, const char* src, size_t n) {
   std::memcpy(dst, src, n - blocks * 64);
 }
 
+// Fork-join pool for the slot fills.  A fill takes ~0.3 ms and the next one
+// follows at once, so between the fills of one copy the workers spin (a
+// condition-variable wake-up costs tens of microseconds per worker and chunk);
+// they only sleep when no job has arrived for a while.
 struct Pool {
   std::mutex mu;
-  std::condition_variable wake, done;
+  std::condition_variable wake;
   std::vector<std::thread> workers;
   // current job: [src, src+bytes) -> dst split over `parts` workers
   const char* src = nullptr;
   char* dst = nullptr;
   size_t bytes = 0;
-  int parts = 0, pending = 0;
-  unsigned long long gen = 0;
-  bool stop = false, streaming = true;
+  int parts = 0;
+  std::atomic<int> pending{0};
+  std::atomic<unsigned long long> gen{0};
+  std::atomic<bool> stop{false};
+  bool streaming = true;
+  static constexpr long long kSpinNs = 400000;   // spin this long for the next fill
+
+  static long long now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
 
   void part(int j) const {
     // 64-byte aligned cuts
@@ -72,17 +85,19 @@ struct Pool {
   void worker(int j) {
     unsigned long long seen = 0;
     for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu);
-        wake.wait(lk, [&] { return stop || gen != seen; });
-        if (stop) return;
-        seen = gen;
+      const long long t0 = now_ns();
+      while (gen.load(std::memory_order_acquire) == seen && !stop.load(std::memory_order_relaxed)) {
+        if (now_ns() - t0 > kSpinNs) {
+          std::unique_lock<std::mutex> lk(mu);
+          wake.wait(lk, [&] { return stop.load() || gen.load(std::memory_order_acquire) != seen; });
+          break;
+        }
+        _mm_pause();
       }
+      if (stop.load()) return;
+      seen = gen.load(std::memory_order_acquire);
       if (j < parts) part(j);
-      {
-        std::lock_guard<std::mutex> lk(mu);
-        if (--pending == 0) done.notify_one();
-      }
+      pending.fetch_sub(1, std::memory_order_acq_rel);
     }
   }
 
@@ -92,24 +107,27 @@ struct Pool {
 
   // the calling thread takes part 0
   void run(char* d, const char* s, size_t n) {
+    dst = d;
+    src = s;
+    bytes = n;
+    pending.store((int)workers.size(), std::memory_order_relaxed);
     {
-      std::lock_guard<std::mutex> lk(mu);
-      dst = d;
-      src = s;
-      bytes = n;
-      pending = (int)workers.size();
-      ++gen;
+      std::lock_guard<std::mutex> lk(mu);   // a worker about to sleep sees the new job
+      gen.fetch_add(1, std::memory_order_release);
     }
     wake.notify_all();
     part(0);
-    std::unique_lock<std::mutex> lk(mu);
-    done.wait(lk, [&] { return pending == 0; });
+    long long spins = 0;
+    while (pending.load(std::memory_order_acquire) != 0) {
+      if (++spins > 20000) std::this_thread::yield();
+      else _mm_pause();
+    }
   }
 
   ~Pool() {
     {
       std::lock_guard<std::mutex> lk(mu);
-      stop = true;
+      stop.store(true);
     }
     wake.notify_all();
     for (auto& t : workers) t.join();

@@ -65,12 +65,26 @@ enum LejaPMode {
   PM_LOOK = 3,    // read p, add the pending term (||.|| of it), add c*y', store
 };
 
-// The mode of term m: a pure function of m, so the host launches the kernel
-// variant compiled for it (and the kernel checks it against the device's).
+// The scheduled mode of term m: a pure function of m, so the host launches the
+// kernel variant compiled for it (and the kernel checks it against the device's).
 __host__ __device__ __forceinline__ int leja_pmode(int m, int defer) {
   if (defer == 2) return m >= 499 ? PM_STORE : ((m & 1) ? PM_SKIP : PM_LOOK);
   if (defer == 1) return (m & 1) ? PM_KEEP : PM_STORE;
   return PM_STORE;
+}
+
+// The mode the device picks for the next term m.  With the lookahead schedule
+// a call that converges on an odd (PM_SKIP) term only finds out in the next
+// launch, which then was a full term computed for nothing.  When the host
+// enqueues term m as a {scheduled variant, PM_STORE} pair (`dual`), an odd term
+// that could be the last one (the residual before it was already small) runs
+// as PM_STORE instead: it reads and stores p and resolves its own residual.
+// The even term after such a term has no pending term to resolve: PM_STORE.
+__host__ __device__ __forceinline__ int leja_next_pmode(int m, int defer, int dual, int small_prev,
+                                                        int ppend) {
+  if (defer != 2 || m >= 499) return leja_pmode(m, defer);
+  if (m & 1) return (dual && small_prev) ? PM_STORE : PM_SKIP;
+  return ppend ? PM_LOOK : PM_STORE;
 }
 
 enum LejaStatus {
@@ -153,6 +167,12 @@ struct StencilArgs {
   LejaCtl* ctl;
   const double* v0;    // in-place start: the call's v (direction of term 1, c0*v = p0)
   const double* stage_f; // MODE_JVP: F(stage); out = (F(stage) - F(u)) - J w (null: out = J w)
+  // Adaptive lookahead (single domain, per-term launches): near the expected
+  // end of a call every term is enqueued as a pair of variants -- the one the
+  // parity schedule names and PM_STORE -- carrying the term index they are
+  // meant for; the variant whose mode the control block does not name exits.
+  int term;            // > 0: run only if the control block is at this term, silently
+  int dual_next;       // the next term is enqueued as such a pair (mode rule below)
   // reductions / flags
   double* partials;    // [grid][2]
   unsigned* ticket;
@@ -366,7 +386,8 @@ __device__ __forceinline__ void leja_next_eps(LejaCtl* ctl, double ny) {
 // sy = sum y'^2, sp = sum p'^2 of this term; sp_prev = sum p_{m-1}^2 of the
 // pending term a PM_LOOK term resolves first.
 __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp, double sp_prev,
-                                              int bad, int counted, double cm) {
+                                              int bad, int counted, double cm,
+                                              int dual_next = 0) {
   const int mode = ctl->pmode;
   if (mode == PM_LOOK) {
     // the previous (odd) term's residual (leja.py:141-145), in the reference's order
@@ -411,7 +432,7 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
     ctl->pend_ynorm = ny;
     ctl->ynorm = ny;
     ctl->m += 1;   // <= 498
-    ctl->pmode = leja_pmode(ctl->m, ctl->defer);
+    ctl->pmode = leja_next_pmode(ctl->m, ctl->defer, dual_next, 0, 1);
     if (ctl->m >= ctl->ncoef) ctl->status = LJ_NEED_COEFFS;
     leja_next_eps(ctl, ny);
     return;
@@ -445,7 +466,7 @@ __device__ __forceinline__ void leja_finalize(LejaCtl* ctl, double sy, double sp
     return;
   }
   if (ctl->m >= ctl->ncoef) ctl->status = LJ_NEED_COEFFS;
-  ctl->pmode = leja_pmode(ctl->m, ctl->defer);
+  ctl->pmode = leja_next_pmode(ctl->m, ctl->defer, dual_next, ctl->small_prev, ctl->ppend);
   leja_next_eps(ctl, ny);
 }
 

@@ -252,6 +252,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     const volatile LejaCtl* c = a.ctl;   // rewritten by the last block of every term
     if (c->status != LJ_RUNNING) return;
     const int cur = c->cur, m = c->m;
+    if (XR == XR_NONE && a.term && m != a.term) return;   // a pair's variant for another term
     if (P2P) {
       hlo_dir = a.p2p.halo_lo_dir[cur];
       hhi_dir = a.p2p.halo_hi_dir[cur];
@@ -282,6 +283,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
     pcoef = c->pend_coef;
     pm_rt = c->pmode;
     if (PM != PM_ANY && pm_rt != PM) {   // variant launched for another mode
+      if (XR == XR_NONE && a.term) return;   // the other variant of the pair runs this term
       if (bid == 0 && threadIdx.x == 0) a.ctl->status = LJ_MODE_ERROR;
       return;
     }
@@ -687,7 +689,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
         a.ext_sums[3] = *((volatile int*)a.bad) ? 1.0 : 0.0;
       } else {
         const int flag = *((volatile int*)a.bad);
-        leja_finalize(a.ctl, sy, sp, sp2, flag, !zero_dir, cm);
+        leja_finalize(a.ctl, sy, sp, sp2, flag, !zero_dir, cm, XR == XR_NONE ? a.dual_next : 0);
       }
       if (MODE == MODE_JVP) a.result[1] = sy;   // local sum of squares (y-strips)
       *a.ticket = 0u;
@@ -1820,6 +1822,7 @@ cudaError_t launch_leja_term(const StencilArgs& a, int grid, int pmode, cudaStre
   switch (pmode) {
     case PM_SKIP: return launch_mode<MODE_LEJA, PM_SKIP>(a, grid, s);
     case PM_LOOK: return launch_mode<MODE_LEJA, PM_LOOK>(a, grid, s);
+    case PM_STORE: return launch_mode<MODE_LEJA, PM_STORE>(a, grid, s);
     default: return launch_mode<MODE_LEJA>(a, grid, s);
   }
 }

@@ -319,6 +319,11 @@ def drive_fused(lib, h, l, q, theta, coeffs, peer=False):
 
     hkey = (l, int(round(4.0 * np.log2(theta))) if theta > 0 else 0)
     batch = max(2, int(_degree_hint.get(hkey, 2)))
+    if not peer:
+        # variant pairs from a few terms before the expected end (csrc/kernels.h,
+        # leja_next_pmode): a call ending on an odd term costs no extra launch
+        _lib.check(lib.xmhd_leja_set_dual_from(h, max(1, batch - 6) if ADAPTIVE else 0),
+                   "xmhd_leja_set_dual_from")
     # every chunk the expected degree will reach is computed from the start, in
     # parallel (the divided differences release the GIL), so a slow host core
     # never makes the device wait at a chunk boundary
@@ -401,6 +406,9 @@ LOOP_MAX_CELLS = int(os.environ.get("XMHD_LOOP_MAX_CELLS", str(1 << 20)))
 # the result back in one of two caller-owned interpolant buffers instead of
 # copying it out; XMHD_ZERO_COPY=0 restores the copies (A/B, tests).
 ZERO_COPY = bool(int(os.environ.get("XMHD_ZERO_COPY", "1") or "1"))
+# Variant pairs near the expected end of a host-paced call (adaptive lookahead);
+# XMHD_ADAPTIVE=0: the plain parity schedule (A/B, tests).
+ADAPTIVE = bool(int(os.environ.get("XMHD_ADAPTIVE", "1") or "1"))
 
 
 def loop_available(mhd):

@@ -107,22 +107,24 @@ def _problem(n=24, seed=4, harris=False):
 
 
 @contextlib.contextmanager
-def sync_per_term(fuse=True, zero_copy=True):
+def sync_per_term(fuse=True, zero_copy=True, adaptive=True):
     """Synchronous steps with one launch per Newton term (the large-grid path),
     on whatever grid the test uses."""
     from paper_2108_13622_b200 import integrators, leja, mhd
-    old = (integrators.ASYNC, integrators.FUSE_STAGES, leja.LOOP_MAX_CELLS, leja.ZERO_COPY)
+    old = (integrators.ASYNC, integrators.FUSE_STAGES, leja.LOOP_MAX_CELLS, leja.ZERO_COPY,
+           leja.ADAPTIVE)
     integrators.ASYNC = False
     integrators.FUSE_STAGES = fuse
     leja.LOOP_MAX_CELLS = 0
     leja.ZERO_COPY = zero_copy
+    leja.ADAPTIVE = adaptive
     for c in mhd._ctx_cache.values():
         c.loop_ok = None
     try:
         yield
     finally:
         (integrators.ASYNC, integrators.FUSE_STAGES, leja.LOOP_MAX_CELLS,
-         leja.ZERO_COPY) = old
+         leja.ZERO_COPY, leja.ADAPTIVE) = old
         for c in mhd._ctx_cache.values():
             c.loop_ok = None
 
@@ -198,6 +200,46 @@ def test_zero_copy_leja_calls_are_bitwise(l):
                                   xb.shift_and_scale(1.0), 1e-10)
             assert r.converged and r.iterations == 2
             assert not r.vector.any()
+
+
+@pytest.mark.parametrize("l", [1, 4])
+def test_adaptive_lookahead_is_bitwise(l):
+    """Variant pairs near the expected end (an odd term that may be the last
+    one stores p and resolves its own residual) against the plain parity
+    schedule (the next launch resolves it): same vector, degree, residual,
+    RHS count and coefficient cache, whatever the degree hint says -- no hint
+    (pairs from term 1), an exact hint, a hint far too low and far too high --
+    for calls ending on odd and on even terms, across the chunk growth."""
+    from paper_2108_13622_b200 import leja
+    xb, st, op = _problem(n=40)
+    u = st.flat()
+    with sync_per_term():
+        lin = xb.FrozenLinearization(op, u)
+        alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+    v = _dev(np.random.default_rng(11).standard_normal(u.numel()))
+    parities = set()
+    for adt, tol in ((0.5, 1e-6), (3.0, 1e-10), (3.0, 1e-9), (7.0, 1e-8), (20.0, 1e-9),
+                     (80.0, 1e-10)):
+        sh = xb.shift_and_scale(adt)
+        hkey = (l, int(round(4.0 * np.log2(sh.theta))))
+
+        def call(adaptive, hint):
+            with sync_per_term(adaptive=adaptive):
+                leja._coeff_cache.clear()
+                leja._degree_hint.pop(hkey, None)
+                if hint is not None:
+                    leja._degree_hint[hkey] = hint
+                c0 = op.calls
+                r = xb.apply_phi_leja(l, xb.JacobianAction(lin), v, adt / alpha, sh, tol)
+                return (r, op.calls - c0, [(k, c.size) for k, c in leja._coeff_cache.items()])
+        a, ca, ka = call(False, None)
+        parities.add(a.iterations & 1)
+        for hint in (None, a.iterations + 1, 2, a.iterations + 40):
+            b, cb, kb = call(True, hint)
+            assert (a.iterations, a.converged, a.residual, ca, ka) == \
+                (b.iterations, b.converged, b.residual, cb, kb), (adt, tol, hint)
+            assert torch.equal(a.vector, b.vector), (adt, tol, hint)
+    assert parities == {0, 1}
 
 
 def test_zero_copy_call_reports_a_nonfinite_rhs_like_the_copying_call():
