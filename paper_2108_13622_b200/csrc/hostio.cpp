@@ -173,8 +173,10 @@ extern "C" int xmhd_h2d_staged(void* dst_dev, const void* src_host, long long by
     cpu_set_t set;
     if (sched_getaffinity(0, sizeof(set), &set) == 0) hw = CPU_COUNT(&set);
     if (hw < 1) hw = 1;
-    // leave cores for the caller's other threads: half the cores, at most 12
-    g_st.threads = std::max(1, env_int("XMHD_H2D_THREADS", std::min(12, std::max(1, hw / 2))));
+    // three quarters of the cores, at most 12 (16-core B200 hosts: 8 threads gave
+    // 44-48 GB/s in isolation but 180-196 ms per bench e2e step on one box against
+    // 160-161 ms with 12, profiles/r02_e2e_threads.txt)
+    g_st.threads = std::max(1, env_int("XMHD_H2D_THREADS", std::min(12, std::max(1, (3 * hw) / 4))));
     for (int k = 0; k < nslot; ++k) {
       void* p = nullptr;
       cudaEvent_t e;
