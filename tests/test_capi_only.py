@@ -46,6 +46,19 @@ def so():
         "xmhd_newton_coeffs": [_I, _D, _D, _PD, _I, _PD],
         "xmhd_leja_schedule": [_I, _D, _D, _PD, _PD],
     }
+    _L = ctypes.c_longlong
+    sigs.update({
+        "xmhd_h2d_staged": [_P, _P, _L, _P],
+        "xmhd_lincomb_diff": [_P, _P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD],
+        "xmhd_lincomb_multi": [_P, ctypes.POINTER(_P), _I, _L, ctypes.POINTER(_P), _PD],
+        "xmhd_stage_difference": [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI],
+        "xmhd_leja_start_inplace": [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I],
+        "xmhd_leja_set_pbuf": [_P, _P, _P],
+        "xmhd_leja_set_dual_from": [_P, _I],
+        "xmhd_leja_launch": [_P, _I, _I],
+        "xmhd_leja_sync": [_P, _P],
+        "xmhd_leja_result_inplace": [_P, _PI],
+    })
     for name, args in sigs.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -268,3 +281,144 @@ def test_leja_one_call_high_degree_and_short_table(so):
                     assert b"coefficient table ended" in so.xmhd_last_error()
         finally:
             ctx.close()
+
+
+class LejaState(ctypes.Structure):
+    """xmhd_leja_state (include/xmhd_b200.h)."""
+    _fields_ = [("status", _I), ("iterations", _I), ("rhs_calls", _I), ("m", _I),
+                ("residual", _D), ("eps", _D), ("ynorm", _D)]
+
+
+@pytest.mark.gpu
+def test_stage_algebra_entry_points(so):
+    """integrators.py:139-153 through the fewer-pass entry points, ctypes only:
+    stage = u + c*p with d = stage - u and ||d|| from one call, then
+    (F(stage) - F(u)) - jvp(d) from the JVP stencil's epilogue, against the same
+    expression assembled from xmhd_rhs / xmhd_jvp outputs in NumPy (bit for
+    bit), and the shared pass of the w_k combinations against NumPy."""
+    torch = _torch()
+    g = golden_io.arrays("leja_cases")
+    meta = next(c for c in golden_io.meta()["leja"] if c["name"] == "kh32")
+    u = np.array(g["kh32__u"])
+    ny, nx = u.shape[1:]
+    pvec = np.array(g["kh32__w"]).reshape(-1)
+    ctx = Ctx(so, nx, ny, meta["dx"], meta["dy"], meta["mu"], meta["eta"], meta["kappa"])
+    try:
+        n = u.size
+        # pageable upload through the staging pipeline
+        ud = torch.empty(n, dtype=torch.float64, device="cuda")
+        flat = np.ascontiguousarray(u.reshape(-1))
+        assert so.xmhd_h2d_staged(vp(ud), flat.ctypes.data, flat.nbytes, None) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(ud.cpu().numpy(), flat)
+        pd = dev(pvec)
+        fu = torch.empty_like(ud)
+        assert so.xmhd_rhs(ctx.h, vp(ud), vp(fu), None) == 0
+        un = ctypes.c_double()
+        assert so.xmhd_norm(ctx.h, vp(ud), n, ctypes.byref(un)) == 0
+        # stage, d = stage - u, ||d||
+        c = 0.37e-3
+        stage, d = torch.empty_like(ud), torch.empty_like(ud)
+        vecs = (_P * 4)(vp(ud), vp(pd), None, None)
+        coef = (ctypes.c_double * 4)(1.0, c, 0.0, 0.0)
+        dn = ctypes.c_double()
+        assert so.xmhd_lincomb_diff(ctx.h, vp(stage), vp(d), n, vecs, coef, 2,
+                                    ctypes.byref(dn)) == 0
+        stage_ref = flat + c * pvec
+        assert np.array_equal(stage.cpu().numpy(), stage_ref)
+        assert np.array_equal(d.cpu().numpy(), stage_ref - flat)
+        dn2 = ctypes.c_double()
+        assert so.xmhd_norm(ctx.h, vp(d), n, ctypes.byref(dn2)) == 0
+        assert dn.value == dn2.value
+        # the stage difference: separate calls assembled on the host vs one fused tail
+        fs, jd, out = torch.empty_like(ud), torch.empty_like(ud), torch.empty_like(ud)
+        assert so.xmhd_rhs(ctx.h, vp(stage), vp(fs), None) == 0
+        called = ctypes.c_int()
+        assert so.xmhd_jvp(ctx.h, vp(ud), vp(fu), un.value, vp(d), vp(jd), ctypes.byref(called),
+                           None, None) == 0
+        assert called.value == 1
+        ref = (fs.cpu().numpy() - fu.cpu().numpy()) - jd.cpu().numpy()
+        assert so.xmhd_stage_difference(ctx.h, vp(ud), vp(fu), un.value, vp(d), dn.value, vp(fs),
+                                        vp(out), ctypes.byref(called), None) == 0
+        assert called.value == 1
+        assert np.array_equal(out.cpu().numpy(), ref)
+        # zero offset: jvp of zeros costs no RHS call (linearize.py:63-64)
+        zero = torch.zeros_like(ud)
+        assert so.xmhd_stage_difference(ctx.h, vp(ud), vp(fu), un.value, vp(zero), 0.0, vp(fs),
+                                        vp(out), ctypes.byref(called), None) == 0
+        assert called.value == 0
+        assert np.array_equal(out.cpu().numpy(), fs.cpu().numpy() - fu.cpu().numpy())
+        # w_k of EXPRB54s4 (integrators.py:186-189) in one pass
+        a, b, cc = fs.cpu().numpy(), jd.cpu().numpy(), out.cpu().numpy()
+        rows = ((64.0, -8.0, 0.0), (-60.0, -(285.0 / 8.0), 125.0 / 8.0),
+                (0.0, 18.0, -(250.0 / 81.0)), (0.0, -60.0, 500.0 / 27.0))
+        outs = [torch.empty_like(ud) for _ in rows]
+        oarr = (_P * 4)(*[vp(o) for o in outs])
+        varr = (_P * 3)(vp(fs), vp(jd), vp(out))
+        flatc = (ctypes.c_double * 12)(*[x for r in rows for x in r])
+        assert so.xmhd_lincomb_multi(ctx.h, oarr, 4, n, varr, flatc) == 0
+        refs = (64.0 * a + -8.0 * b, (-60.0 * a + -(285.0 / 8.0) * b) + (125.0 / 8.0) * cc,
+                18.0 * b + -(250.0 / 81.0) * cc, -60.0 * b + (500.0 / 27.0) * cc)
+        for o, r in zip(outs, refs):
+            assert np.array_equal(o.cpu().numpy(), r)
+        assert so.xmhd_lincomb_multi(ctx.h, oarr, 5, n, varr, flatc) == 2   # XMHD_BADARG
+    finally:
+        ctx.close()
+
+
+@pytest.mark.gpu
+def test_leja_inplace_protocol_matches_the_one_call(so):
+    """xmhd_leja_start_inplace + xmhd_leja_set_pbuf + xmhd_leja_launch (with the
+    variant pairs of xmhd_leja_set_dual_from) + xmhd_leja_result_inplace on
+    golden phi-calls: the reference's counters and vector, the caller's v left
+    untouched, the result in one of the caller's two buffers, and the same bits
+    with and without the variant pairs."""
+    torch = _torch()
+    xi = np.ascontiguousarray(golden_io.arrays("coeff_cases")["leja_points"])
+    g = golden_io.arrays("leja_cases")
+    rec = next(c for c in golden_io.meta()["leja"] if c["name"] == "kh32")
+    u, v = g["kh32__u"], g["kh32__v"]
+    ctx = Ctx(so, u.shape[2], u.shape[1], rec["dx"], rec["dy"], rec["mu"], rec["eta"],
+              rec["kappa"])
+    try:
+        for ph in rec["phi"]:
+            if ph["l"] != 1:
+                continue
+            table = np.empty(500)
+            assert so.xmhd_leja_schedule(1, ph["q"], ph["theta"], dptr(xi), dptr(table)) == 0
+            it, conv, calls = ph["iterations"], ph["converged"], ph["rhs_calls"]
+            ud, vd = dev(u), dev(v)
+            v_keep = vd.clone()
+            fu = torch.empty_like(ud)
+            assert so.xmhd_rhs(ctx.h, vp(ud), vp(fu), None) == 0
+            un = ctypes.c_double()
+            assert so.xmhd_norm(ctx.h, vp(ud), ud.numel(), ctypes.byref(un)) == 0
+            pair = (torch.empty_like(ud), torch.empty_like(ud))
+            first = None
+            for dual_from in (0, 1, max(1, it - 3)):
+                assert so.xmhd_leja_set_pbuf(ctx.h, vp(pair[0]), vp(pair[1])) == 0
+                assert so.xmhd_leja_start_inplace(ctx.h, vp(ud), vp(fu), un.value, vp(vd),
+                                                  ph["dt"], ph["q"], ph["theta"], ph["tol"],
+                                                  dptr(xi), dptr(table), 500) == 0
+                assert so.xmhd_leja_set_dual_from(ctx.h, dual_from) == 0
+                st = LejaState()
+                while True:
+                    assert so.xmhd_leja_launch(ctx.h, 8, 0) == 0
+                    assert so.xmhd_leja_sync(ctx.h, ctypes.byref(st)) == 0
+                    if st.status != 0:
+                        break
+                which = ctypes.c_int(-1)
+                assert so.xmhd_leja_result_inplace(ctx.h, ctypes.byref(which)) == 0
+                torch.cuda.synchronize()
+                assert which.value in (0, 1)
+                assert (st.iterations, st.status == 1, st.rhs_calls) == (it, conv, calls)
+                p = pair[which.value].cpu().numpy()
+                assert _rel(p, g[ph["key"]]) <= 1e-10, ph["key"]
+                if first is None:
+                    first = (p.copy(), st.residual)
+                else:   # the variant pairs change no bit
+                    assert np.array_equal(p, first[0]) and st.residual == first[1]
+                assert torch.equal(vd, v_keep)
+                assert so.xmhd_leja_set_pbuf(ctx.h, None, None) == 0
+    finally:
+        ctx.close()
