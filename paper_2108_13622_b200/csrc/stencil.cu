@@ -68,7 +68,16 @@ namespace cg = cooperative_groups;
 // interpolant schedule with runtime mode branches in one kernel (0.338 vs
 // 0.305 ms at 2048^2: hence one compiled variant per mode), 64-thread strips
 // (0.327 vs 0.315 ms), the row loop unrolled by 3 so the PD / GY register
-// rings need no copies (-30% MOVs, but 0.337 ms: code size and scheduling).
+// rings need no copies (-30% MOVs, but 0.337 ms: code size and scheduling), the
+// output phase of row r-3 moved into the same barrier phase as the primitives
+// of row r (two independent chains per phase, 5-slot FY ring; commit 40988eb:
+// odd / even term 0.286 / 0.396 ms vs 0.250 / 0.320 ms on the same box), an
+// interior-row fast path around row_source plus a launch-uniform test around
+// the mirror negations (~100 fewer integer / branch instructions of the ~1060
+// per row step, yet odd / even term 0.2527 / 0.3241 ms vs 0.2491 / 0.3206 ms,
+// 4096^2 0.9396 / 1.2419 vs 0.9257 / 1.2272: the integer work is not on the
+// critical path, the fp64 and shared-memory dependency chains of two warps per
+// scheduler are).
 
 namespace xb {
 
@@ -83,9 +92,6 @@ __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; } 
 // next P1 goes; every other ring hazard is still separated by the barrier
 // after P1 (FX: P3(s) reads slot s-2 while P1(s+1) writes s+1; GX: P2(s)
 // writes s+1 while P3(s) reads s; FY is read by its own column only).
-#ifndef XB_FASTROW
-#define XB_FASTROW 1   // interior-row fast path + launch-uniform mirror test (A/B knob)
-#endif
 #ifndef XB_ONEBAR
 #define XB_ONEBAR 0   // measured: 0.282 vs 0.281 ms (2048^2), 1.088 vs 1.080 (4096^2): the larger carve-out costs more than the barrier
 #endif
@@ -379,7 +385,6 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       }
 
       const int nsteps = (Y1 - Y0) + 4;
-      const bool mirrors = (g.bcx != BC_PERIODIC) || (g.bcy == BC_REFLECT);
       int s4 = 0;  // s % 4
       for (int s = 0; s < nsteps; ++s) {
         const int r = Y0 - 2 + s;
@@ -466,33 +471,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 #pragma unroll
           for (int f = 0; f < NF; ++f)
             x[f] = (MODE == MODE_RHS) ? nu[f] : __dadd_rn(nu[f], __dmul_rn(eps, nd[f]));
-#if XB_FASTROW
-          if (mirrors) {   // launch-uniform: periodic grids never negate ghost cells
-            if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
-            if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
-          }
-#else
           if (flipx) { x[MX] = -x[MX]; x[BX] = -x[BX]; }
           if (nflip) { x[MY] = -x[MY]; x[BY] = -x[BY]; }
-#endif
           if (s + 1 < nsteps) {
-#if XB_FASTROW
-            // interior rows (all but the first / last two of the grid) need none
-            // of row_source's wrap / mirror / halo logic: ~85 of the ~1060
-            // instructions per row step were spent there
-            RowSrc rs;
-            if ((unsigned)(r + 1) < (unsigned)g.ny) {
-              rs.u = a.u;
-              rs.d = dsrc;
-              rs.off = (unsigned)(r + 1) * (unsigned)g.nx;
-              rs.fs = plane;
-              rs.flip = 0;
-            } else {
-              rs = row_source(r + 1, g, a.u, dsrc, hlo_dir, hhi_dir);
-            }
-#else
             const RowSrc rs = row_source(r + 1, g, a.u, dsrc, hlo_dir, hhi_dir);
-#endif
             nflip = rs.flip;
 #pragma unroll
             for (int f = 0; f < NF; ++f) {
