@@ -77,7 +77,10 @@ namespace cg = cooperative_groups;
 // per row step, yet odd / even term 0.2527 / 0.3241 ms vs 0.2491 / 0.3206 ms,
 // 4096^2 0.9396 / 1.2419 vs 0.9257 / 1.2272: the integer work is not on the
 // critical path, the fp64 and shared-memory dependency chains of two warps per
-// scheduler are).
+// scheduler are), the epilogue operand loads issued after P2 instead of at the
+// step start (same 238 / 252 registers; odd term 0.245 vs 0.250 ms but even
+// term 0.342 vs 0.322 ms, 4096^2 1.000 / 1.339 vs 0.927 / 1.222 ms: their L2
+// latency needs the whole step to hide).
 
 namespace xb {
 
