@@ -156,7 +156,9 @@ int xmhd_jvp_async(xmhd_ctx* ctx, const double* u, const double* fu, double unor
 int xmhd_leja_loop(xmhd_ctx* ctx);
 int xmhd_leja_loop_available(xmhd_ctx* ctx);
 /* Loop kernel of xmhd_leja_loop: 0 = 2D tiles (default; XMHD_TILE=0 in the
- * environment selects 1), 1 = the sliding-window iteration kernel in a loop. */
+ * environment selects 1), 1 = the sliding-window iteration kernel in a loop,
+ * 2 = none (xmhd_leja_loop_available reports 0: xmhd_leja runs per-term
+ * launches, the large-grid path, on any grid). */
 int xmhd_set_loop_kind(xmhd_ctx* ctx, int kind);
 /* Deferred interpolant stores of the fused Leja kernels (default on; XMHD_PDEFER=0
  * in the environment turns them off): an odd Newton term neither reads nor

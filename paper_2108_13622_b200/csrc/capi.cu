@@ -68,6 +68,7 @@ struct xmhd_ctx {
   int loop_blocks = -1;        // co-resident blocks of the Leja loop kernel (-1: unknown)
   int tile_grid = -1;          // grid of the 2D-tile Leja loop (0: unavailable, -1: unknown)
   int tile_minb = 2;           // its occupancy variant
+  bool loop_off = false;       // xmhd_set_loop_kind(2): phi-actions run per-term launches
   int partial_slots = 0;       // doubles in `partials`
   double xi_h[500];            // host copy of the Leja points on the device
   bool xi_valid = false;
@@ -1061,14 +1062,15 @@ int xmhd_set_leja_defer(xmhd_ctx* c, int on) {
 }
 
 int xmhd_set_loop_kind(xmhd_ctx* c, int kind) {
-  if (!c || kind < 0 || kind > 1) return fail(XMHD_BADARG, "bad loop kind");
+  if (!c || kind < 0 || kind > 2) return fail(XMHD_BADARG, "bad loop kind");
   c->tile_grid = -1;
   if (kind == 1) c->tile_grid = 0;   // sliding-window loop
+  c->loop_off = (kind == 2);         // no cooperative loop: per-term launches
   return XMHD_OK;
 }
 
 int xmhd_leja_loop_available(xmhd_ctx* c) {
-  if (!c || c->g.bcy == BC_HALO) return 0;
+  if (!c || c->g.bcy == BC_HALO || c->loop_off) return 0;
   loop_plan(c);
   return (c->tile_grid > 0 || c->grid <= c->loop_blocks) ? 1 : 0;
 }

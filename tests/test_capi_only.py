@@ -52,6 +52,8 @@ def so():
         "xmhd_lincomb_diff": [_P, _P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD],
         "xmhd_lincomb_multi": [_P, ctypes.POINTER(_P), _I, _L, ctypes.POINTER(_P), _PD],
         "xmhd_stage_difference": [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI],
+        "xmhd_set_loop_kind": [_P, _I],
+        "xmhd_leja_hint": [_P, _I],
         "xmhd_leja_start_inplace": [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I],
         "xmhd_leja_set_pbuf": [_P, _P, _P],
         "xmhd_leja_set_dual_from": [_P, _I],
@@ -422,3 +424,47 @@ def test_leja_inplace_protocol_matches_the_one_call(so):
                 assert so.xmhd_leja_set_pbuf(ctx.h, None, None) == 0
     finally:
         ctx.close()
+
+
+@pytest.mark.gpu
+def test_leja_one_call_per_term_path_matches_golden(so):
+    """xmhd_leja on the large-grid path (xmhd_set_loop_kind(ctx, 2): per-term
+    launches with the in-place start and the variant pairs chosen from
+    xmhd_leja_hint) on golden phi-calls of degree 11..170: the reference's
+    counters and vectors whatever the hint, and the same bits for every hint."""
+    xi = np.ascontiguousarray(golden_io.arrays("coeff_cases")["leja_points"])
+    meta = json.load(open(os.path.join(golden_io.GOLDEN, "large", "degree.json")))
+    g = np.load(os.path.join(golden_io.GOLDEN, "large", "degree.npz"))
+    seen = 0
+    for case in meta["cases"]:
+        name = case["name"]
+        u, v = g[f"{name}__u"], g[f"{name}__v"]
+        ctx = Ctx(so, case["nx"], case["ny"], case["dx"], case["dy"], case["mu"], case["eta"],
+                  case["kappa"])
+        try:
+            assert so.xmhd_set_loop_kind(ctx.h, 2) == 0
+            for ph in case["phi"]:
+                if ph["l"] != 1:
+                    continue
+                table = np.empty(500)
+                assert so.xmhd_leja_schedule(1, ph["q"], ph["theta"], dptr(xi),
+                                             dptr(table)) == 0
+                first = None
+                for hint in (2, ph["iterations"] + 1, 400):
+                    assert so.xmhd_leja_hint(ctx.h, hint) == 0
+                    rc, p, it, conv, res, calls = _leja_one_call(
+                        so, ctx, u, v, ph["dt"], ph["q"], ph["theta"], ph["tol"], xi, table)
+                    assert rc == 0, so.xmhd_last_error()
+                    assert (it, conv, calls) == (ph["iterations"], ph["converged"],
+                                                 ph["rhs_calls"]), (ph["key"], hint)
+                    if conv:
+                        bound = max(1e-10, 10.0 * ph["floor_rel"])
+                        assert _rel(p, g[ph["key"]]) <= bound, ph["key"]
+                    if first is None:
+                        first = (p.copy(), res)
+                    else:
+                        assert np.array_equal(p, first[0]) and res == first[1], (ph["key"], hint)
+                    seen += 1
+        finally:
+            ctx.close()
+    assert seen >= 6
