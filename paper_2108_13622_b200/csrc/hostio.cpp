@@ -172,7 +172,10 @@ extern "C" int xmhd_h2d_staged(void* dst_dev, const void* src_host, long long by
     int hw = (int)std::thread::hardware_concurrency();
     cpu_set_t set;
     if (sched_getaffinity(0, sizeof(set), &set) == 0) hw = CPU_COUNT(&set);
-    if (hw < 1) hw = 1;
+    // one process per GPU: the ranks of a node share its cores (torchrun exports
+    // LOCAL_WORLD_SIZE)
+    const int local_world = std::max(1, env_int("LOCAL_WORLD_SIZE", 1));
+    hw = std::max(1, hw / local_world);
     // three quarters of the cores, at most 12 (16-core B200 hosts: 8 threads gave
     // 44-48 GB/s in isolation but 180-196 ms per bench e2e step on one box against
     // 160-161 ms with 12, profiles/r02_e2e_threads.txt)
