@@ -259,6 +259,18 @@ int xmhd_lincomb_diff(xmhd_ctx* ctx, double* out, double* diff, long long n,
  * zero coefficients skipped (a term the reference's expression does not have). */
 int xmhd_lincomb_multi(xmhd_ctx* ctx, double* const* out, int nout, long long n,
                        const double* const* v, const double* coef);
+/* The two embedded solutions of an exponential Rosenbrock step and their
+ * distance in one pass (integrators.py:168-171 / 190-199 with error_norm,
+ * 88-96): the lower-order solution is formed on the fly, the higher-order one
+ * goes to out_hi; err_out[0] = ||lo - hi||, err_out[1] = ||hi||, *nonfinite = hi
+ * has a non-finite entry.  Same operations, order and reductions as the
+ * separate xmhd_lincomb calls followed by xmhd_diff_norms.
+ *   XMHD_SCHEME_EXPRB43:   v = {u, phi1, p3, p4},            c = {1, dt, dt, dt}:
+ *     lo = (c0*v0 + c1*v1) + c2*v2;  hi = 1.0*lo + c3*v3
+ *   XMHD_SCHEME_EXPRB54S4: v = {u, phi1, p3, p4, p3', p4'},  c = {1, dt, dt, dt, dt, dt}:
+ *     s = c0*v0 + c1*v1;  lo = (s + c2*v2) + c3*v3;  hi = (s + c4*v4) + c5*v5 */
+int xmhd_final_pair(xmhd_ctx* ctx, int scheme, double* out_hi, long long n,
+                    const double* const* v, const double* c, double* err_out, int* nonfinite);
 
 /* out = x / d elementwise (IEEE), optionally ||out|| (w/||w||, jw/mag, v/l!). */
 int xmhd_divide(xmhd_ctx* ctx, double* out, const double* x, double d, long long n,

@@ -138,6 +138,7 @@ _SIGS = {
     "xmhd_stage_difference": (_I, [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI]),
     "xmhd_lincomb_diff": (_I, [_P, _P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD]),
     "xmhd_lincomb_multi": (_I, [_P, ctypes.POINTER(_P), _I, _L, ctypes.POINTER(_P), _PD]),
+    "xmhd_final_pair": (_I, [_P, _I, _P, _L, ctypes.POINTER(_P), _PD, _PD, _PI]),
     "xmhd_h2d_staged": (_I, [_P, _P, _L, _P]),
     "xmhd_h2d_threads": (_I, []),
 }

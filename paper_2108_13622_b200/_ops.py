@@ -270,6 +270,23 @@ def lincomb_multi(rows, vecs, ctx=None):
     return outs
 
 
+def final_pair(scheme_code, coeffs, vecs, ctx=None):
+    """(hi, ||lo - hi||, ||hi||, nonfinite) of a step's two embedded solutions in
+    one pass (csrc/vec.cu FinalPairOp; scheme_code 0 = EXPRB43 with 4 vectors,
+    1 = EXPRB54s4 with 6).  Single domain only (the norms are local)."""
+    assert reducer() is None and len(vecs) == len(coeffs) == (4 if scheme_code == 0 else 6)
+    lib = _lib.load()
+    out = torch.empty_like(vecs[0])
+    arr = (ctypes.c_void_p * 6)(*[ctypes.c_void_p(v.data_ptr()) for v in vecs])
+    cs = (ctypes.c_double * 6)(*[float(c) for c in coeffs])
+    err = (ctypes.c_double * 2)()
+    bad = ctypes.c_int()
+    rc = lib.xmhd_final_pair(_h(ctx), int(scheme_code), _lib.ptr(out), out.numel(), arr, cs, err,
+                             ctypes.byref(bad))
+    _lib.check(rc, "xmhd_final_pair")
+    return out, float(err[0]), float(err[1]), bool(bad.value)
+
+
 def divide(x, d, out=None, want_norm=False, ctx=None):
     """x / d element-wise (IEEE); optionally also ||x / d||."""
     lib = _lib.load()

@@ -864,6 +864,24 @@ int xmhd_diff_norms(xmhd_ctx* c, const double* a, const double* b, long long n, 
   return XMHD_OK;
 }
 
+int xmhd_final_pair(xmhd_ctx* c, int scheme, double* out_hi, long long n,
+                    const double* const* v, const double* cf, double* err_out,
+                    int* nonfinite) {
+  if (!c || !out_hi || !v || !cf || !err_out || !nonfinite) return fail(XMHD_BADARG, "null arg");
+  const int kind = scheme == XMHD_SCHEME_EXPRB43 ? 43 : (scheme == XMHD_SCHEME_EXPRB54S4 ? 54 : 0);
+  if (!kind) return fail(XMHD_BADARG, "scheme must be EXPRB43 or EXPRB54s4");
+  for (int k = 0; k < (kind == 43 ? 4 : 6); ++k)
+    if (!v[k]) return fail(XMHD_BADARG, "null input vector");
+  CK(launch_final_pair(kind, out_hi, n, v, cf, redbuf(c), c->stream));
+  c->launches++;
+  int rc = fetch_doubles(c, 3);
+  if (rc) return rc;
+  err_out[0] = c->h_dbl[0];
+  err_out[1] = c->h_dbl[1];
+  *nonfinite = c->h_dbl[2] > 0.0 ? 1 : 0;
+  return XMHD_OK;
+}
+
 int xmhd_divb(xmhd_ctx* c, const double* u, double* field, double* out) {
   if (!c || !u || !out) return fail(XMHD_BADARG, "null arg");
   CK(launch_divb_max(c->g, u, field, redbuf(c), c->stream));

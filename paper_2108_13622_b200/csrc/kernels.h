@@ -227,6 +227,12 @@ cudaError_t launch_lincomb_diff(double* out, double* diff, long long n, const do
 cudaError_t launch_lincomb_multi(double* const* out, int nout, long long n,
                                  const double* const* v, const double* coef12, RedBuf rb,
                                  cudaStream_t s);
+// The two embedded solutions of a step in one pass (vec.cu, FinalPairOp): the
+// higher-order one into out_hi; result[0] = ||lo - hi||, result[1] = ||hi||,
+// result[2] = 1 if hi has a non-finite entry.  kind 43: v[0..3], c[0..3];
+// kind 54: v[0..5], c[0..5].
+cudaError_t launch_final_pair(int kind, double* out_hi, long long n, const double* const* v,
+                              const double* c, RedBuf rb, cudaStream_t s);
 // out = x / d (IEEE), result[0] = ||out|| when want_norm.
 cudaError_t launch_divide(double* out, const double* x, double d, long long n,
                           int want_norm, RedBuf rb, cudaStream_t s);

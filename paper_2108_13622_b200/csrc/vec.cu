@@ -281,6 +281,56 @@ __global__ void __launch_bounds__(VT) lincomb_multi_kernel(Ptrs<3, NOUT> P, long
   stream<3, NOUT, V2>(n, P, op);
 }
 
+// The two embedded solutions of a step and their distance in one pass
+// (integrators.py:168-171, 190-199): the lower-order solution `lo` is formed
+// in registers only, the higher-order one is stored, and ||lo - hi||, ||hi|| and
+// the non-finite flag of hi are reduced like diffnorm_kernel / the flagged
+// combination would reduce them on materialised vectors (same traversal).
+//   KIND 43: lo = (c0*v0 + c1*v1) + c2*v2;  hi = 1.0*lo + c3*v3
+//   KIND 54: s = c0*v0 + c1*v1;  lo = (s + c2*v2) + c3*v3;  hi = (s + c4*v4) + c5*v5
+struct Coef6 {
+  double c[6];
+};
+
+template <int KIND>
+struct FinalPairOp {
+  static constexpr int NIN = (KIND == 43) ? 4 : 6;
+  double c[6];
+  double acc_d = 0.0, acc_h = 0.0, bad = 0.0;
+  __device__ __forceinline__ void operator()(const double (&x)[NIN], double (&y)[1]) {
+    double lo, hi;
+    if (KIND == 43) {
+      lo = __dadd_rn(__dadd_rn(__dmul_rn(c[0], x[0]), __dmul_rn(c[1], x[1])), __dmul_rn(c[2], x[2]));
+      hi = __dadd_rn(__dmul_rn(1.0, lo), __dmul_rn(c[3], x[3 < NIN ? 3 : 0]));
+    } else {
+      const double s = __dadd_rn(__dmul_rn(c[0], x[0]), __dmul_rn(c[1], x[1]));
+      lo = __dadd_rn(__dadd_rn(s, __dmul_rn(c[2], x[2])), __dmul_rn(c[3], x[3]));
+      hi = __dadd_rn(__dadd_rn(s, __dmul_rn(c[4], x[4 < NIN ? 4 : 0])),
+                     __dmul_rn(c[5], x[5 < NIN ? 5 : 0]));
+    }
+    y[0] = hi;
+    const double d = __dsub_rn(lo, hi);
+    acc_d = __fma_rn(d, d, acc_d);
+    acc_h = __fma_rn(hi, hi, acc_h);
+    if (!isfinite(hi)) bad = 1.0;
+  }
+};
+
+template <int KIND, bool V2>
+__global__ void __launch_bounds__(VT) final_pair_kernel(Ptrs<FinalPairOp<KIND>::NIN, 1> P,
+                                                        long long n, Coef6 cf, RedBuf rb) {
+  FinalPairOp<KIND> op;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) op.c[k] = cf.c[k];
+  stream<FinalPairOp<KIND>::NIN, 1, V2>(n, P, op);
+  double acc[3] = {op.acc_d, op.acc_h, op.bad}, tot[3];
+  if (grid_reduce<3, false>(acc, rb, tot)) {
+    rb.result[0] = sqrt(tot[0]);
+    rb.result[1] = sqrt(tot[1]);
+    rb.result[2] = tot[2] > 0.0 ? 1.0 : 0.0;
+  }
+}
+
 struct DivideOp {
   double d;
   double acc = 0.0;
@@ -743,6 +793,29 @@ cudaError_t launch_lincomb_multi(double* const* out, int nout, long long n,
     case 3: go(std::integral_constant<int, 3>{}); break;
     case 4: go(std::integral_constant<int, 4>{}); break;
     default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final_pair(int kind, double* out_hi, long long n, const double* const* v,
+                              const double* c, RedBuf rb, cudaStream_t s) {
+  Coef6 cf;
+  for (int k = 0; k < 6; ++k) cf.c[k] = c[k];
+  const int grid = grid_for(n, rb.grid);
+  if (kind == 43) {
+    Ptrs<4, 1> P;
+    for (int k = 0; k < 4; ++k) P.in[k] = v[k];
+    P.out[0] = out_hi;
+    if (aligned16(P)) final_pair_kernel<43, true><<<grid, VT, 0, s>>>(P, n, cf, rb);
+    else final_pair_kernel<43, false><<<grid, VT, 0, s>>>(P, n, cf, rb);
+  } else if (kind == 54) {
+    Ptrs<6, 1> P;
+    for (int k = 0; k < 6; ++k) P.in[k] = v[k];
+    P.out[0] = out_hi;
+    if (aligned16(P)) final_pair_kernel<54, true><<<grid, VT, 0, s>>>(P, n, cf, rb);
+    else final_pair_kernel<54, false><<<grid, VT, 0, s>>>(P, n, cf, rb);
+  } else {
+    return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

@@ -52,6 +52,8 @@ def so():
         "xmhd_lincomb_diff": [_P, _P, _P, _L, ctypes.POINTER(_P), _PD, _I, _PD],
         "xmhd_lincomb_multi": [_P, ctypes.POINTER(_P), _I, _L, ctypes.POINTER(_P), _PD],
         "xmhd_stage_difference": [_P, _P, _P, _D, _P, _D, _P, _P, _PI, _PI],
+        "xmhd_final_pair": [_P, _I, _P, _L, ctypes.POINTER(_P), _PD, _PD, _PI],
+        "xmhd_diff_norms": [_P, _P, _P, _L, _PD],
         "xmhd_set_loop_kind": [_P, _I],
         "xmhd_leja_hint": [_P, _I],
         "xmhd_leja_start_inplace": [_P, _P, _P, _D, _P, _D, _D, _D, _D, _PD, _PD, _I],
@@ -364,6 +366,37 @@ def test_stage_algebra_entry_points(so):
         for o, r in zip(outs, refs):
             assert np.array_equal(o.cpu().numpy(), r)
         assert so.xmhd_lincomb_multi(ctx.h, oarr, 5, n, varr, flatc) == 2   # XMHD_BADARG
+        # the embedded pair of a step in one pass (integrators.py:168-171, 190-199):
+        # the higher-order solution, ||lo - hi|| and ||hi|| as xmhd_diff_norms
+        # reduces them on the materialised vectors
+        dt = 0.0375
+        h = [flat, a, b, cc, outs[0].cpu().numpy(), outs[1].cpu().numpy()]
+        hv = [ud, fs, jd, out, outs[0], outs[1]]
+        for scheme, nin in ((0, 4), (1, 6)):
+            if scheme == 0:
+                lo = (1.0 * h[0] + dt * h[1]) + dt * h[2]
+                hi = 1.0 * lo + dt * h[3]
+            else:
+                lo = ((1.0 * h[0] + dt * h[1]) + dt * h[2]) + dt * h[3]
+                hi = ((1.0 * h[0] + dt * h[1]) + dt * h[4]) + dt * h[5]
+            varr6 = (_P * 6)(*[vp(x) for x in hv])
+            c6 = (ctypes.c_double * 6)(1.0, dt, dt, dt, dt, dt)
+            got = torch.empty_like(ud)
+            err = (ctypes.c_double * 2)()
+            bad = ctypes.c_int(-1)
+            assert so.xmhd_final_pair(ctx.h, scheme, vp(got), n, varr6, c6, err,
+                                      ctypes.byref(bad)) == 0
+            assert np.array_equal(got.cpu().numpy(), hi) and bad.value == 0
+            lo_d = torch.from_numpy(lo).cuda()
+            two = (ctypes.c_double * 2)()
+            assert so.xmhd_diff_norms(ctx.h, vp(lo_d), vp(got), n, two) == 0
+            assert (err[0], err[1]) == (two[0], two[1])
+            assert abs(err[0] - np.linalg.norm(lo - hi)) <= 1e-12 * err[0]
+        hv[3] = torch.full_like(ud, float("inf"))
+        varr6 = (_P * 6)(*[vp(x) for x in hv])
+        assert so.xmhd_final_pair(ctx.h, 0, vp(got), n, varr6, c6, err, ctypes.byref(bad)) == 0
+        assert bad.value == 1
+        assert so.xmhd_final_pair(ctx.h, 7, vp(got), n, varr6, c6, err, ctypes.byref(bad)) == 2
     finally:
         ctx.close()
 
