@@ -95,6 +95,9 @@ __host__ __device__ constexpr int fy_field(int k) { return k < 5 ? k : k + 1; } 
 // next P1 goes; every other ring hazard is still separated by the barrier
 // after P1 (FX: P3(s) reads slot s-2 while P1(s+1) writes s+1; GX: P2(s)
 // writes s+1 while P3(s) reads s; FY is read by its own column only).
+#ifndef XB_FYREG
+#define XB_FYREG 1
+#endif
 #ifndef XB_ONEBAR
 #define XB_ONEBAR 0   // measured: 0.282 vs 0.281 ms (2048^2), 1.088 vs 1.080 (4096^2): the larger carve-out costs more than the barrier
 #endif
@@ -225,6 +228,11 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
                                              const int nblk) {
   constexpr bool P2P = (XR == XR_PEER || XR == XR_EMUL);
   constexpr bool COH = (XR == XR_LOOP);
+  // The ideal y-fluxes are read by their own column only.  The RHS kernel has
+  // the registers (170 of 255) to keep its three pending rows there instead of
+  // in the shared-memory ring: 21 of its 84 shared-memory accesses per cell and
+  // row step go, and the L1 data pipe is its busiest unit.
+  constexpr bool FYREG = XB_FYREG && (MODE == MODE_RHS);
   extern __shared__ __align__(16) double smem[];
   double (*pd)[NPD][SW] = reinterpret_cast<double (*)[NPD][SW]>(smem);
   double (*fxs)[NFX][SW] = reinterpret_cast<double (*)[NFX][SW]>(smem + RING_PD * NPD * SW);
@@ -373,6 +381,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
       double pr1[NPD], pr2[NPD];
 #pragma unroll
       for (int k = 0; k < NPD; ++k) pr1[k] = pr2[k] = 0.0;
+      // FYREG: ideal y-fluxes of rows r-1, r-2, r-3 of this column
+      double fq1[NFY], fq2[NFY], fq3[NFY];
+#pragma unroll
+      for (int k = 0; k < NFY; ++k) fq1[k] = fq2[k] = fq3[k] = 0.0;
 
       // prefetch registers: state (and direction) of the next row to consume
       double nu[NF], nd[NF];
@@ -469,6 +481,7 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 
         // ---- P1: state at (r, cg) from the prefetch registers
         double pn[NPD];
+        double fyn[NFY];   // FYREG: ideal y-fluxes of row r
         {
           double x[NF];
 #pragma unroll
@@ -502,8 +515,13 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 #pragma unroll
           for (int k = 0; k < NFX; ++k) fxs[s4][k][t] = fv[k];
           flux_y<KX == DIV_IEEE>(p, g, fv);
+          if (FYREG) {
 #pragma unroll
-          for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
+            for (int k = 0; k < NFY; ++k) fyn[k] = fv[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < NFY; ++k) fys[s4][k][t] = fv[k];
+          }
         }
         __syncthreads();
 
@@ -548,7 +566,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
           {
             double a[NFY], b[NFY];
 #pragma unroll
-            for (int k = 0; k < NFY; ++k) { a[k] = fys[fy1][k][t]; b[k] = fys[fy3][k][t]; }
+            for (int k = 0; k < NFY; ++k) {
+              a[k] = FYREG ? fq1[k] : fys[fy1][k][t];
+              b[k] = FYREG ? fq3[k] : fys[fy3][k][t];
+            }
 #pragma unroll
             for (int k = 0; k < NFY; ++k) {
               const int f = fy_field(k);
@@ -642,6 +663,10 @@ __device__ __forceinline__ void stencil_body(const StencilArgs& a, const int bid
 
 #pragma unroll
         for (int k = 0; k < NG; ++k) { gy2[k] = gy1[k]; gy1[k] = gyn[k]; }
+        if (FYREG) {
+#pragma unroll
+          for (int k = 0; k < NFY; ++k) { fq3[k] = fq2[k]; fq2[k] = fq1[k]; fq1[k] = fyn[k]; }
+        }
         s3 = (s3 == 2) ? 0 : s3 + 1;
         s4 = (s4 + 1) & 3;
       }

@@ -318,6 +318,7 @@ class StripMhd:
         self.state_halo = HaloSet(self.nx, dev)
         self.dir_halo = HaloSet(self.nx, dev)
         self._peer = False
+        self._peer_off = False   # set when the peer link could not be verified
 
     def peer_transport(self):
         """True when the Leja loop runs over peer memory (and the link is set up).
@@ -332,13 +333,50 @@ class StripMhd:
         if (os.environ.get("XMHD_STRIP_TRANSPORT", "peer") != "peer" or self.comm.size < 2
                 or not isinstance(self.comm, Comm) or self.comm.size > 8):
             return False
+        if self._peer_off:
+            return False
+        # Every rank takes part in every gather below whatever happened on it, and
+        # all ranks read the same gathered lists, so they agree on the outcome: any
+        # failure (allocation, IPC mapping, a probe write that did not arrive) on
+        # any rank puts the whole job on the NCCL transport instead of hanging it.
         lib = _lib.load()
         handle = (ctypes.c_char * 64)()
-        _lib.check(lib.xmhd_p2p_alloc(self.ctx.h, handle), "xmhd_p2p_alloc")
-        handles = self.comm.gather_host(bytes(handle))
-        blob = (ctypes.c_char * (64 * len(handles))).from_buffer_copy(b"".join(handles))
-        _lib.check(lib.xmhd_p2p_connect(self.ctx.h, self.comm.rank, self.comm.size, blob,
-                                        int(self.periodic_y)), "xmhd_p2p_connect")
+        err = None
+        try:
+            _lib.check(lib.xmhd_p2p_alloc(self.ctx.h, handle), "xmhd_p2p_alloc")
+        except (RuntimeError, OSError) as exc:
+            err = str(exc)
+        got = self.comm.gather_host((err, bytes(handle)))
+        errs = [e for e, _ in got if e]
+        if not errs:
+            try:
+                blob = (ctypes.c_char * (64 * len(got))).from_buffer_copy(
+                    b"".join(h for _, h in got))
+                _lib.check(lib.xmhd_p2p_connect(self.ctx.h, self.comm.rank, self.comm.size, blob,
+                                                int(self.periodic_y)), "xmhd_p2p_connect")
+                # (probe value, rank) into row `rank` of every rank's board
+                _lib.check(lib.xmhd_p2p_probe(self.ctx.h, 1000.0 + self.comm.rank),
+                           "xmhd_p2p_probe")
+            except (RuntimeError, OSError) as exc:
+                err = str(exc)
+            errs = [e for e in self.comm.gather_host(err) if e]   # also: every probe has landed
+        if not errs:
+            board = (ctypes.c_double * 32)()
+            try:
+                _lib.check(lib.xmhd_p2p_read_board(self.ctx.h, board), "xmhd_p2p_read_board")
+                seen = [(board[4 * q], board[4 * q + 1]) for q in range(self.comm.size)]
+                if seen != [(1000.0 + q, float(q)) for q in range(self.comm.size)]:
+                    err = f"rank {self.comm.rank}: probe writes of its peers did not arrive ({seen})"
+            except (RuntimeError, OSError) as exc:
+                err = str(exc)
+            errs = [e for e in self.comm.gather_host(err) if e]
+        if errs:
+            self._peer_off = True
+            if self.comm.rank == 0:
+                import sys
+                print(f"[xmhd] peer-memory strip transport unavailable ({errs[0]}); using NCCL",
+                      file=sys.stderr, flush=True)
+            return False
         self._peer = True
         return True
 

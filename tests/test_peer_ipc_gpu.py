@@ -60,3 +60,41 @@ def test_peer_regions_mapped_across_processes(tmp_path):
         vals = [float(x) for x in open(f"{out}.{rank}").read().split()]
         # entry q: (100 + q, q) written by rank q into this rank's board
         assert vals == [100.0, 0.0, 101.0, 1.0]
+
+
+def _strip_worker(rank, world, port, out_path, fail_rank):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_13622_b200 as xb
+        from paper_2108_13622_b200 import _lib, strips
+        torch.cuda.set_device(0)
+        if rank == fail_rank:
+            # this rank cannot map its peers (what a box without P2P access would report)
+            lib = _lib.load()
+            lib.xmhd_p2p_connect = lambda *a: 3
+        mhd = strips.StripMhd(xb.StateGrid(32, 12, 0.1, 0.1, None),
+                              xb.MHDParams(0.01, 0.01, 0.01), strips.Comm())
+        first = mhd.peer_transport()
+        again = mhd.peer_transport()
+        with open(f"{out_path}.{rank}", "w") as fh:
+            fh.write(f"{int(first)} {int(again)}")
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_strip_peer_link_is_verified_or_all_ranks_fall_back(tmp_path, fail_rank):
+    """StripMhd.peer_transport(): handles, mapping and a probe write per peer are
+    checked on every rank; when any rank fails, every rank reports False (NCCL
+    transport) instead of some ranks spinning on a peer that never posts."""
+    import torch.multiprocessing as mp
+    world = 2
+    out = str(tmp_path / "peer")
+    mp.spawn(_strip_worker, args=(world, _free_port(), out, fail_rank), nprocs=world, join=True)
+    want = "1 1" if fail_rank < 0 else "0 0"
+    for rank in range(world):
+        assert open(f"{out}.{rank}").read() == want
