@@ -11,8 +11,10 @@ coefficient cache cleared per step so the host coefficient work is included.
           plain (pageable) NumPy arrays in, NumPy arrays out; per step u and
           the 4 right-hand vectors go H2D and the 4 results D2H.  ``e2e_pinned``
           is the same with page-locked torch host tensors.
-  roofline : the fused Leja iteration kernel, timed with CUDA events on its
-          stream.  Algorithmic bytes per cell per Newton term:
+  roofline : the fused Leja iteration kernel: CUDA events on its stream around
+          every batch of term launches inside the timed region, divided by the
+          Newton terms (``kernel_ms``; ``kernel_ms_alone`` / ``by_kind`` come
+          from a burst of back-to-back terms afterwards).  Algorithmic bytes per cell per Newton term:
           320 (lookahead interpolant schedule: an odd term reads u, y, F(u)
           and writes y' = 256 B, the even term reads u, y, F(u), p and writes
           y', p' = 384 B), 384 with XMHD_PDEFER=0; ``by_kind`` gives each term
@@ -37,6 +39,7 @@ device time.  ``--impl reference`` times that CPU implementation alone (rank
 """
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -444,6 +447,9 @@ def main():
     iters_total = 0
     degrees = None
     launches0 = total_launches(mhd)
+    # the fused terms' device time inside the timed region: CUDA events on the
+    # library's stream around every batch of term launches (xmhd_term_timing)
+    _lib.check(_lib.load().xmhd_term_timing(mhd.ctx.bind_stream(), 1, None), "xmhd_term_timing")
     with ClockSampler(local) as clocks:
         job.barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -458,11 +464,18 @@ def main():
         job.barrier()
     launches = total_launches(mhd) - launches0
     ms = job.maxed(ev0.elapsed_time(ev1))
+    term_ms = ctypes.c_double()
+    _lib.check(_lib.load().xmhd_term_timing(mhd.ctx.bind_stream(), 0, ctypes.byref(term_ms)),
+               "xmhd_term_timing")
+    term_ms = job.maxed(term_ms.value)
     # every rank processes its strip of the same iterations: whole-job cell-updates
     value = iters_total * n_cells / (ms * 1e-3)
 
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
-    kern_ms, kind_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
+    alone_ms, kind_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
+    # roofline: the average term inside the timed region (the NCCL strip loop
+    # is not bracketed: the burst figure stands in there)
+    kern_ms = term_ms / iters_total if term_ms > 0.0 else alone_ms
     # single domain only: in y-strip mode the stencil needs exchanged ghost rows
     stencil_ms = time_stencil_modes(_lib, lin, mhd, v_dev) if world == 1 else {}
     local_cells = u_dev.numel() // 8
@@ -551,6 +564,14 @@ def main():
                          "frac_at_384B": 384.0 * local_cells / (kern_ms * 1e-3) / 1e9 / peak,
                          "kernel": "stencil_kernel<MODE_LEJA> (fused FD-JVP + Newton update)",
                          "kernel_ms": kern_ms, "bytes_per_cell": bpc,
+                         "timed": ("CUDA events around every batch of term launches inside the "
+                                   "timed region, / Newton terms" if term_ms > 0.0 else
+                                   "burst of back-to-back terms after the timed region"),
+                         "share_of_step": term_ms / ms if term_ms > 0.0 else None,
+                         # the same kernel in a burst of 48 back-to-back launches after the
+                         # timed region (clocks recover between phases: box- and state-dependent)
+                         "kernel_ms_alone": alone_ms,
+                         "frac_alone": bpc * local_cells / (alone_ms * 1e-3) / 1e9 / peak,
                          "by_kind": kinds,
                          "traffic": ncu_traffic(args.n, local_cells)},
             # the other two stencil kernels of the metric's "RHS/Jv", timed the same

@@ -450,6 +450,16 @@ int xmhd_leja_schedule(int l, double q, double theta, const double* xi, double* 
 int xmhd_h2d_staged(void* dst_dev, const void* src_host, long long bytes, void* stream);
 int xmhd_h2d_threads(void);
 
+/* Measurement aid (bench.py's roofline): device time of the fused Leja terms
+ * inside a timed region.  While enabled, every batch of term launches of this
+ * context (xmhd_leja, xmhd_leja_launch) is bracketed by two CUDA events on the
+ * context's stream; the pairs are read at the call's next host synchronisation.
+ * enable = 1 / 0: synchronise, write the milliseconds accumulated so far to
+ * *total_ms (may be NULL), reset the sum and switch the brackets on / off;
+ * enable < 0: read the sum only.  Launches that exit at once (past a stop, the
+ * idle variant of a pair) are inside the brackets. */
+int xmhd_term_timing(xmhd_ctx* ctx, int enable, double* total_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -141,6 +141,7 @@ _SIGS = {
     "xmhd_final_pair": (_I, [_P, _I, _P, _L, ctypes.POINTER(_P), _PD, _PD, _PI]),
     "xmhd_h2d_staged": (_I, [_P, _P, _L, _P]),
     "xmhd_h2d_threads": (_I, []),
+    "xmhd_term_timing": (_I, [_P, _I, _PD]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -76,6 +76,10 @@ struct xmhd_ctx {
   bool leja_adaptive = true;   // variant pairs near the expected end (XMHD_ADAPTIVE=0: off)
   int leja_next_term = 1;      // Newton term index of the next iteration launch
   long long launches = 0;
+  // xmhd_term_timing: CUDA-event brackets around the batches of fused-term launches
+  int tt_on = 0;
+  double tt_ms = 0.0;
+  std::vector<cudaEvent_t> tt_free, tt_open;   // idle events; recorded (begin, end) pairs
   int batch_max = 64;
   int hint_iters = 2;          // expected degree of the next fused Leja call (batch sizing)
   int dual_from = 0;           // first term enqueued as a variant pair (0: parity schedule only)
@@ -232,9 +236,37 @@ int launch_term(xmhd_ctx* c, const StencilArgs& a, bool peer = false) {
   return XMHD_OK;
 }
 
+// Term timing (xmhd_term_timing): one event before and one after every batch of
+// fused-term launches; the pairs are read at the next host synchronisation.
+static int tt_mark(xmhd_ctx* c) {
+  if (!c->tt_on) return XMHD_OK;
+  cudaEvent_t e;
+  if (c->tt_free.empty()) {
+    CK(cudaEventCreate(&e));
+  } else {
+    e = c->tt_free.back();
+    c->tt_free.pop_back();
+  }
+  CK(cudaEventRecord(e, c->stream));
+  c->tt_open.push_back(e);
+  return XMHD_OK;
+}
+
+static int tt_harvest(xmhd_ctx* c) {
+  for (size_t k = 0; k + 1 < c->tt_open.size(); k += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->tt_open[k], c->tt_open[k + 1]));
+    c->tt_ms += (double)ms;
+  }
+  for (cudaEvent_t e : c->tt_open) c->tt_free.push_back(e);
+  c->tt_open.clear();
+  return XMHD_OK;
+}
+
 int sync_ctl(xmhd_ctx* c) {
   CK(cudaMemcpyAsync(c->ctl_h, c->ctl, sizeof(LejaCtl), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (!c->tt_open.empty()) return tt_harvest(c);
   return XMHD_OK;
 }
 
@@ -263,11 +295,15 @@ int leja_run(xmhd_ctx* c, xmhd_leja_state* st, bool peer = false) {
   if (batch < 2) batch = 2;
   if (batch > c->batch_max) batch = c->batch_max;
   for (;;) {
+    int rc = tt_mark(c);
+    if (rc) return rc;
     for (int k = 0; k < batch; ++k) {
-      int rc = launch_term(c, a, peer);
+      rc = launch_term(c, a, peer);
       if (rc) return rc;
     }
-    int rc = sync_ctl(c);
+    rc = tt_mark(c);
+    if (rc) return rc;
+    rc = sync_ctl(c);
     if (rc) return rc;
     c->leja_next_term = c->ctl_h->m;   // kernels launched past a stop exited
     if (c->ctl_h->status != LJ_RUNNING) break;
@@ -460,6 +496,8 @@ int xmhd_destroy(xmhd_ctx* c) {
     cudaFree(c->ybuf[k]);
     cudaFree(c->pbuf[k]);
   }
+  for (cudaEvent_t e : c->tt_open) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->tt_free) cudaEventDestroy(e);
   cudaFreeHost(c->ctl_h);
   cudaFreeHost(c->h_dbl);
   cudaFreeHost(c->h_int);
@@ -971,10 +1009,27 @@ int xmhd_leja_launch(xmhd_ctx* c, int n, int peer) {
   }
   StencilArgs a = leja_args(c);
   if (peer) a.p2p = c->p2p;
+  int rc = n > 0 ? tt_mark(c) : XMHD_OK;
+  if (rc) return rc;
   for (int k = 0; k < n; ++k) {
-    int rc = launch_term(c, a, peer != 0);
+    rc = launch_term(c, a, peer != 0);
     if (rc) return rc;
   }
+  return n > 0 ? tt_mark(c) : XMHD_OK;
+}
+
+int xmhd_term_timing(xmhd_ctx* c, int enable, double* total_ms) {
+  if (!c) return fail(XMHD_BADARG, "null arg");
+  if (enable >= 0) {
+    CK(cudaStreamSynchronize(c->stream));
+    int rc = tt_harvest(c);
+    if (rc) return rc;
+    if (total_ms) *total_ms = c->tt_ms;
+    c->tt_on = enable ? 1 : 0;
+    c->tt_ms = 0.0;
+    return XMHD_OK;
+  }
+  if (total_ms) *total_ms = c->tt_ms;
   return XMHD_OK;
 }
 

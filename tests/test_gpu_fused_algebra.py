@@ -282,3 +282,42 @@ def test_staged_pageable_upload_is_exact():
         torch.cuda.synchronize()
         assert np.array_equal(dst.cpu().numpy(), src)
     assert lib.xmhd_h2d_threads() >= 1
+
+
+def test_term_timing_brackets_the_term_launches():
+    """xmhd_term_timing (bench.py's in-region roofline timer): the fused terms of
+    host-paced calls are bracketed by CUDA events while it is on, the sum is
+    read and reset when it is switched, and the calls' results do not change."""
+    from paper_2108_13622_b200 import _lib, leja
+    xb, st, op = _problem(n=48)
+    u = st.flat()
+    lib = _lib.load()
+    with sync_per_term():
+        lin = xb.FrozenLinearization(op, u)
+        alpha = xb.estimate_alpha(lin, None, rng=np.random.default_rng(0)).alpha
+        mv = xb.JacobianAction(lin)
+        v = _dev(np.random.default_rng(3).standard_normal(u.numel()))
+        h = lin.mhd.ctx.bind_stream()
+
+        def call():
+            leja._coeff_cache.clear()
+            dt = 8.0 / alpha
+            return xb.apply_phi_leja(1, mv, v, dt, xb.shift_and_scale(alpha * dt), 1e-9)
+
+        base = call()
+        got = ctypes.c_double(-1.0)
+        assert lib.xmhd_term_timing(h, -1, ctypes.byref(got)) == 0 and got.value == 0.0
+        assert lib.xmhd_term_timing(h, 1, None) == 0
+        timed = [call() for _ in range(3)]
+        assert lib.xmhd_term_timing(h, -1, ctypes.byref(got)) == 0
+        running = got.value
+        assert lib.xmhd_term_timing(h, 0, ctypes.byref(got)) == 0
+        assert got.value == running > 0.0
+        # a plausible device time: microseconds to milliseconds per term on this grid
+        per_term = got.value / sum(r.iterations for r in timed)
+        assert 1e-3 < per_term < 5.0
+        after = call()
+        assert lib.xmhd_term_timing(h, -1, ctypes.byref(got)) == 0 and got.value == 0.0
+    for r in timed + [after]:
+        assert (r.iterations, r.converged) == (base.iterations, base.converged)
+        assert torch.equal(r.vector, base.vector)
