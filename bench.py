@@ -56,6 +56,9 @@ sys.path.insert(0, REPO)
 METRIC = "RHS/Jv cell-updates/s (fp64 GB/s vs HBM peak); wall-s per EXPRB step"
 SWEEP = (1.0, 10.0, 100.0, 300.0)
 LEJA_TOL = 1e-10
+# XMHD_BENCH_SHARED_GPU=1: N ranks share device 0 over gloo (a check of the N>1
+# host logic where only one GPU exists; its line says so and is not a measurement)
+SHARED_GPU = bool(int(os.environ.get("XMHD_BENCH_SHARED_GPU", "0") or "0"))
 # algorithmic bytes per cell per Newton term
 def bytes_per_cell_term(world):
     return 384.0 if os.environ.get("XMHD_PDEFER", "1") == "0" else 320.0
@@ -67,7 +70,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=2048, help="grid size (config 1: 2048)")
+    ap.add_argument("--n", "--grid", dest="n", type=int, default=2048,
+                    help="grid size (config 1: 2048)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exprb", action="store_true")
     ap.add_argument("--no-scale-case", action="store_true")
@@ -81,7 +85,7 @@ def maybe_spawn(args):
     Returns an exit code, or None when this process is already a rank."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
         return None
-    if args.impl != "reference":
+    if args.impl != "reference" and not SHARED_GPU:
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -94,7 +98,10 @@ def maybe_spawn(args):
         port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+           "--master-port", str(port), os.path.abspath(__file__)]
+    # torchrun's own parser would read a bare `--n` as an abbreviation of its options
+    for a in sys.argv[1:]:
+        cmd.append("--grid" + a[3:] if a == "--n" or a.startswith("--n=") else a)
     return subprocess.call(cmd)
 
 
@@ -406,9 +413,17 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    if SHARED_GPU and world > 1:
+        # host-logic check of the N>1 paths on a one-GPU box: every rank on device
+        # 0, gloo, the torch.distributed strip transport (no kernel waits on a peer)
+        local = 0
+        os.environ["XMHD_STRIP_TRANSPORT"] = "nccl"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     job = Job(world, rank, local)
 
     import paper_2108_13622_b200 as xb
@@ -472,10 +487,12 @@ def main():
     value = iters_total * n_cells / (ms * 1e-3)
 
     # ---- the dominant kernel alone: CUDA events around back-to-back fused iterations
-    alone_ms, kind_ms = time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha)
-    # roofline: the average term inside the timed region (the NCCL strip loop
-    # is not bracketed: the burst figure stands in there)
-    kern_ms = term_ms / iters_total if term_ms > 0.0 else alone_ms
+    # (single domain only: a strip's terms need its neighbours' ghost rows and sums)
+    alone_ms, kind_ms = (time_fused_iteration(xb, _lib, lin, mhd, v_dev, alpha) if world == 1
+                         else (None, None))
+    # roofline: the average term inside the timed region; the torch.distributed
+    # strip loop is not bracketed, there the whole region / terms is the upper bound
+    kern_ms = term_ms / iters_total if term_ms > 0.0 else ms / iters_total
     # single domain only: in y-strip mode the stencil needs exchanged ghost rows
     stencil_ms = time_stencil_modes(_lib, lin, mhd, v_dev) if world == 1 else {}
     local_cells = u_dev.numel() // 8
@@ -566,12 +583,14 @@ def main():
                          "kernel_ms": kern_ms, "bytes_per_cell": bpc,
                          "timed": ("CUDA events around every batch of term launches inside the "
                                    "timed region, / Newton terms" if term_ms > 0.0 else
-                                   "burst of back-to-back terms after the timed region"),
+                                   "timed region / Newton terms (upper bound: halo exchange and "
+                                   "all-reduce of the torch.distributed transport included)"),
                          "share_of_step": term_ms / ms if term_ms > 0.0 else None,
                          # the same kernel in a burst of 48 back-to-back launches after the
                          # timed region (clocks recover between phases: box- and state-dependent)
                          "kernel_ms_alone": alone_ms,
-                         "frac_alone": bpc * local_cells / (alone_ms * 1e-3) / 1e9 / peak,
+                         "frac_alone": (bpc * local_cells / (alone_ms * 1e-3) / 1e9 / peak
+                                        if alone_ms else None),
                          "by_kind": kinds,
                          "traffic": ncu_traffic(args.n, local_cells)},
             # the other two stencil kernels of the metric's "RHS/Jv", timed the same
@@ -587,6 +606,9 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        if SHARED_GPU and world > 1:
+            line["dry_run"] = (f"{world} ranks sharing one GPU over gloo (XMHD_BENCH_SHARED_GPU): "
+                               "a check of the N>1 host logic, not a measurement")
         if scale is not None:
             line["scale_case"] = scale
         if exprb is not None:

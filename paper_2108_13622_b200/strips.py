@@ -75,6 +75,17 @@ class Comm:
             self.size = dist.get_world_size(group)
         else:
             self.rank, self.size = 0, 1
+        # gloo moves CUDA tensors through collectives but not through send / recv:
+        # point-to-point messages of device tensors are staged through the host
+        # (the CPU-backend check of the N>1 paths on one GPU; NCCL needs no staging)
+        self._host_p2p = (self.size > 1 and dist.get_backend(group) == "gloo")
+
+    def _p2p_buffers(self, tensors):
+        """(tensors to post, copy-back list) for point-to-point messages."""
+        if not self._host_p2p:
+            return list(tensors), []
+        staged = [t.detach().to("cpu").contiguous() if t.is_cuda else t for t in tensors]
+        return staged, [(t, h) for t, h in zip(tensors, staged) if t.is_cuda]
 
     def allreduce_sum(self, t):
         if self.size > 1:
@@ -117,11 +128,12 @@ class Comm:
                     consume(f, r, _ops.to_host(planes[f]))
                 elif self.rank == root:
                     buf = torch.empty(shapes[r][0], dtype=planes[f].dtype,
-                                      device=planes[f].device)
+                                      device="cpu" if self._host_p2p else planes[f].device)
                     dist.recv(buf, src=r, group=self.group)
                     consume(f, r, _ops.to_host(buf))
                 elif self.rank == r:
-                    dist.send(planes[f].contiguous(), dst=root, group=self.group)
+                    (msg,), _ = self._p2p_buffers([planes[f].contiguous()])
+                    dist.send(msg, dst=root, group=self.group)
 
     def exchange_rows(self, send_lo, send_hi, recv_lo, recv_hi, periodic):
         """Send my rows 0,1 down and rows ny-2,ny-1 up; receive the neighbours' rows.
@@ -136,6 +148,8 @@ class Comm:
                 recv_lo.copy_(send_hi)
                 recv_hi.copy_(send_lo)
             return
+        (send_lo, send_hi), _ = self._p2p_buffers([send_lo, send_hi])
+        (recv_lo, recv_hi), back = self._p2p_buffers([recv_lo, recv_hi])
         ops = []
         if above is not None:
             ops.append(dist.P2POp(dist.isend, send_hi, above, self.group))
@@ -147,6 +161,8 @@ class Comm:
             ops.append(dist.P2POp(dist.irecv, recv_hi, above, self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        for dev, host in back:
+            dev.copy_(host)
 
 
 class Reducer:
