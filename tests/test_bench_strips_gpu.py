@@ -51,3 +51,41 @@ def test_multi_rank_bench_path_runs_and_agrees_with_one_rank():
         sc_n, sc_1 = d["scale_case"], one["scale_case"]
         assert sc_n["n_gpus"] == n and sc_n["leja_degrees"][:2] == sc_1["leja_degrees"][:2]
         assert d["roofline"]["kernel_ms_alone"] is None and d["roofline"]["frac"] > 0
+
+
+def _run_config(args, ranks):
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    script = os.path.join(REPO, "scripts", "run_config.py")
+    if ranks == 1:
+        cmd = [sys.executable, script] + args
+    else:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env["XMHD_BENCH_SHARED_GPU"] = "1"
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1", "--master-port",
+               str(port), script] + args
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_adaptive_run_over_real_ranks_keeps_the_counters():
+    """harness.run over y-strips with one process per rank (torch.distributed
+    Comm, each rank its own rows of the initial state and of the start vector):
+    the one-rank run's accept / reject sequence, RHS and Leja counts."""
+    one = _run_config(["2", "8"], 1)
+    assert one["accepted"] == 8 and one.get("ranks") is None
+    for n in (2, 3):
+        d = _run_config(["2", "8"], n)
+        assert d["ranks"] == n
+        for key in ("accepted", "rejected", "rhs_evals", "phi_iterations", "spectrum_rhs_evals"):
+            assert d[key] == one[key], key
+        assert abs(d["t_reached"] / one["t_reached"] - 1) < 1e-6
+        assert abs(d["max_divb"] - one["max_divb"]) <= 1e-9 * max(1.0, abs(one["max_divb"]))
