@@ -316,6 +316,13 @@ DATA = ("synthetic (seeded BASELINE config-1 state: KH 2048^2 + 16 Fourier modes
 def reference_arm(args, rank, world):
     if rank != 0:
         return
+    try:
+        # torchrun exports OMP_NUM_THREADS=1 to its ranks: give the BLAS norms
+        # of the reference path every core again
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:
+        pass
     iters = max(1, args.steps)
     t0 = time.perf_counter()
     samples = []
